@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""Benchmark: Dirac matvec GB/s (% HBM roofline); deflated Hutchinson probes/s.
+
+Contract:
+* headline `value`: fp64 Wilson-Dirac A x on the 48^3 x 96 lattice of
+  BASELINE.json configs[1] (largest single-GPU config of the matvec sweep),
+  algorithmic bytes 960 B/site (24 in + 24 out + 4 x 18 link reals, 8 B),
+  inputs (2 GB spinor, 6 GB links) far larger than the 126 MB L2;
+* `e2e`: the same metric through the public API `WilsonOperator.apply` with
+  pinned host buffers in the reference layout (H2D + layout + apply +
+  layout + D2H inside the timed region);
+* `probes_per_sec`: BASELINE.json configs[0] (8^4, s = 32 Rademacher,
+  tol 1e-8) through `hutchinson(TruncatedInverse, ProbeSet)`;
+* `cpu_baseline`: the oracle port (restated reference CSR matvec) on a
+  bounded 16^4 sample on this host.
+`--impl reference` times the CPU port of the reference path instead.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_SITE_F64 = 960.0
+FLOPS_PER_SITE = 1368.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# CPU leg (oracle port) -- only place besides tests/smoke that runs oracle/
+
+
+def cpu_matvec_sample(dims=(16, 16, 16, 16), eps=0.2, mass=0.1, min_seconds=10.0):
+    from oracle import wilson4d as W
+    from oracle import cbackend
+    links = W.su3_links(dims, eps, 0)
+    A = W.build_wilson4d_csr(links, dims, mass)
+    rng = np.random.default_rng(1)
+    x = (rng.normal(size=A.shape[0]) + 1j * rng.normal(size=A.shape[0])) / np.sqrt(2)
+    V = int(np.prod(dims))
+    mv, cores, kind_desc = cbackend.csr_matvec_callable(A)
+    mv(x)  # warm
+    n, t0 = 0, time.perf_counter()
+    while True:
+        mv(x)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or n >= 2000:
+            break
+    per = el / n
+    return {"value": BYTES_PER_SITE_F64 * V / per / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{n} CSR matvecs (49 nnz/row) on a {'x'.join(map(str, dims))} lattice, "
+                      f"{kind_desc}, {per * 1e3:.2f} ms each"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    t_start = time.perf_counter()
+    res = cpu_matvec_sample(min_seconds=max(10.0, 2.0 * args.steps))
+    line = {
+        "impl": "reference", "metric": "Dirac matvec GB/s (% HBM roofline); deflated Hutchinson probes/sec",
+        "value": res["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": "wilson_dslash_fp64_cpu_sample", "lattice": "16x16x16x16", "eps": 0.2, "m0": 0.1},
+        "cpu_baseline": res,
+        "e2e": {"value": res["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_start,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1909_12234_b200 as M
+    from paper_1909_12234_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dims = tuple(int(v) for v in args.dims.split("x"))
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    gauge = M.generate_gauge(geo, "su3", eps=0.2, seed=0)
+    op = M.build_wilson(gauge, 0.1, prec=args.prec, recon=args.recon)
+    del gauge
+    torch.cuda.empty_cache()
+    V = geo.site_count
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1234 + rank)
+    x = torch.randn((1, 12, V), dtype=op.dtype, device="cuda", generator=g)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        op.apply_native(x, out=y)
+    barrier()
+    l0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            op.apply_native(x, out=y)
+        ev1.record(stream)
+        barrier()
+    launches = _lib.launch_count() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    bytes_per_site = BYTES_PER_SITE_F64 if args.prec == 64 else BYTES_PER_SITE_F64 / 2
+    value = bytes_per_site * V * world / (ms_max * 1e-3) / 1e9
+    kernel_gbs = bytes_per_site * V / (ms * 1e-3) / 1e9
+    peak, peak_kind = _peaks()
+
+    # e2e through the public API with pinned host buffers (reference layout)
+    del y
+    torch.cuda.empty_cache()
+    xh = torch.empty((op.dim,), dtype=torch.complex128, pin_memory=True)
+    xh.copy_(op.from_native(x.to(torch.complex128) if args.prec == 32 else x)[0].cpu())
+    e2e_steps = max(1, min(3, args.steps))
+    op.apply(xh)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        yh = op.apply(xh)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    tt = torch.tensor([e2e_s], device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_value = bytes_per_site * V * world / float(tt.item()) / 1e9
+    del xh, yh, x
+    torch.cuda.empty_cache()
+
+    # probes/s, BASELINE configs[0]: 8^4, s=32 Rademacher, tol 1e-8
+    probes = None
+    if not args.skip_probes:
+        probes = probes_per_sec(M, rank, world)
+
+    if rank == 0:
+        line = {
+            "metric": "Dirac matvec GB/s (% HBM roofline); deflated Hutchinson probes/sec",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128" if args.prec == 64 else "c64", "data": "synthetic",
+            "config": {"workload": f"wilson_dslash_{'fp64' if args.prec == 64 else 'fp32'}_"
+                                   f"{args.dims}", "lattice": args.dims, "eps": 0.2, "m0": 0.1,
+                       "boundary": "antiperiodic", "n_rhs": 1, "link_recon": args.recon,
+                       "l2": "inputs larger than L2 (spinor %.2f GB, links %.2f GB)" % (
+                           V * 12 * 16 / 1e9 * (1 if args.prec == 64 else 0.5),
+                           V * 4 * 9 * 16 / 1e9 * (1 if args.prec == 64 else 0.5)),
+                       "parallelism": f"replicas x{world}" if world > 1 else "single"},
+            "roofline": {"bound": "hbm", "achieved": kernel_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": kernel_gbs / peak, "traffic": None, "peak_kind": peak_kind,
+                         "bytes_per_site": bytes_per_site},
+            "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": V * 12 * 16,
+                    "d2h_bytes_per_step": V * 12 * 16},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "probes_per_sec": probes,
+        }
+        if world == 1 and not args.skip_cpu:
+            try:
+                line["cpu_baseline"] = cpu_matvec_sample(min_seconds=args.cpu_seconds)
+            except Exception as e:  # reported, not fatal
+                line["cpu_baseline"] = {"error": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def probes_per_sec(M, rank, world, dims=(8, 8, 8, 8), s=32, tol=1e-8):
+    import torch
+    import torch.distributed as dist
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.2, seed=0), 0.1)
+    # probe sharding: rank r takes probes j = r, r + world, ...
+    mine = list(range(rank, s, world))
+    probes = M.build_probe_set(geo, 12, len(mine), hp_count=1, dilution=False, kind="rademacher", seed=0)
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
+    M.hutchinson(inv, M.build_probe_set(geo, 12, 4, dilution=False, kind="rademacher", seed=1000))  # warm
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    est = M.hutchinson(inv, probes)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    t = torch.tensor([el], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    el = float(t.item())
+    its = inv.total_iterations / max(1, inv.n_solves)
+    return {"config": "8x8x8x8 eps=0.2 m0=0.1 s=32 rademacher tol=1e-8 (BASELINE configs[0])",
+            "value": s / el, "unit": "probes/s", "seconds": el, "mean_iterations": its,
+            "solver": "BiCGStab, 4 rhs per solve", "estimate_re": float(est.mean.real) if world == 1 else None}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dims", default="48x48x48x96")
+    ap.add_argument("--prec", type=int, default=64, choices=[64, 32])
+    ap.add_argument("--recon", type=int, default=18, choices=[18, 12])
+    ap.add_argument("--skip-probes", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

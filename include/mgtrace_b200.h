@@ -1,0 +1,165 @@
+/*
+ * mgtrace-b200 C ABI -- the drop-in boundary for the deflated-Hutchinson hot
+ * path of arXiv:1909.12234 (reference: /root/reference/pkg/src/mgtrace).
+ *
+ * The reference has no C ABI: its boundary is a duck-typed Python protocol
+ * (SURVEY.md section 8(b)).  Every entry point below replaces one reference
+ * interface, cited as file:line; the Python host package
+ * `paper_1909_12234_b200` binds these through ctypes and re-exports the
+ * reference's Python signatures on top of them.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Every `*_dev` pointer is CUDA device
+ *    memory owned by the caller; every call is stream-ordered on `stream`
+ *    (a cudaStream_t passed as void*, NULL = legacy default stream).
+ *  - Return value: MGT_OK (0) or an error code; mgt_last_error() returns the
+ *    message of the last failing call on the calling thread.  No C++
+ *    exception crosses the ABI.
+ *  - Reference layout ("ref"): complex128 index `site*12 + spin*3 + colour`,
+ *    site lexicographic over dims[0..3] with dims[3] (= t) FASTEST
+ *    (lattice.py:10, :70-74).  Links ref layout: (V, 4, 3, 3) complex.
+ *  - Native layout ("native", what the kernels stream): structure of arrays,
+ *    element (rhs, comp, site) at ((rhs*12 + comp)*V + site), one complex
+ *    (double2 / float2) per element, site order with t SLOWEST:
+ *        site = ((x3*L0 + x0)*L1 + x1)*L2 + x2.
+ *  - prec: 64 = complex128 (double2), 32 = complex64 (float2).
+ */
+#ifndef MGTRACE_B200_H
+#define MGTRACE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGT_OK 0
+#define MGT_ERR_INVALID 1  /* bad argument -> ValueError in the shim       */
+#define MGT_ERR_CUDA 2     /* CUDA runtime failure -> RuntimeError          */
+#define MGT_ERR_SIZE 3     /* dimension mismatch (lattice.py:215-216)       */
+#define MGT_ERR_BLOCKING 4 /* BlockingError (multigrid.py:24, :39-44)       */
+
+/* apply flags (lattice.py:219-247) */
+#define MGT_G5_IN 1  /* y = A (g5 x)          : a_gamma5()        lattice.py:244-247 */
+#define MGT_G5_OUT 2 /* y = g5 (A x)          : hermitian_form()  lattice.py:240-242 */
+#define MGT_DAGGER 4 /* y = A^dag x = g5 A g5 : apply_dagger()    lattice.py:219-222 */
+
+typedef struct mgt_wilson_s *mgt_wilson_t;
+
+/* ---- diagnostics --------------------------------------------------------- */
+const char *mgt_last_error(void);
+int mgt_version(void);
+/* number of kernel launches issued by this library since load (evidence). */
+uint64_t mgt_launch_count(void);
+
+/* ---- layout (reference <-> native) -------------------------------------- */
+/* Replaces the implicit reference ordering of lattice.py:70-74; n_rhs fields
+ * stored back to back in both layouts. */
+int mgt_spinor_from_ref(const int dims[4], int prec, const void *ref_dev,
+                        void *native_dev, int n_rhs, void *stream);
+int mgt_spinor_to_ref(const int dims[4], int prec, const void *native_dev,
+                      void *ref_dev, int n_rhs, void *stream);
+
+/* ---- gauge links --------------------------------------------------------- */
+/* SU(3) U = expm(i eps H) for `nsites` reference-order sites starting at
+ * `site_begin`; normals_dev holds (nsites, 4, 8) float64 draws (the draw
+ * order is defined in paper_1909_12234_b200/gauge.py).  Output: ref layout
+ * (V,4,3,3) complex128.  Replaces generate_gauge (lattice.py:126-144), which
+ * only knows U(1). */
+int mgt_su3_expm(double eps, const double *normals_dev, int64_t site_begin,
+                 int64_t nsites, void *links_ref_dev, void *stream);
+
+/* ---- Wilson-Dirac operator ----------------------------------------------- */
+/* Replaces build_wilson (lattice.py:274-318) + LatticeOperator
+ * (lattice.py:194-256).  Copies the ref-layout links into the handle's own
+ * native link layout (precision `prec`; recon = 18 full links or 12 =
+ * two rows + unitarity reconstruction).  antiperiodic != 0: -1 phase on
+ * links wrapping in dims[3] (lattice.py:91-102). */
+int mgt_wilson_create(mgt_wilson_t *out, const int dims[4], int antiperiodic,
+                      double mass, int prec, int recon,
+                      const void *links_ref_dev, void *stream);
+int mgt_wilson_destroy(mgt_wilson_t h);
+int mgt_wilson_info(mgt_wilson_t h, int dims[4], int *prec, int *recon,
+                    int64_t *volume);
+
+/* y = flags-variant of (A + i tau g5) applied to x; native layout, n_rhs
+ * fields.  Replaces LatticeOperator.apply / apply_dagger / apply_shifted /
+ * hermitian_form / a_gamma5 (lattice.py:214-247) and _ShiftedOperator.apply
+ * (eigen.py:140-151). */
+int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs,
+                     int flags, double tau, void *stream);
+
+/* ---- BLAS-1 on native fields (fp64) -------------------------------------- */
+/* out[r] = sum_i conj(a_i) b_i for each of n_rhs fields of `len` complex
+ * entries (deterministic fixed-order reduction; numpy vdot semantics). */
+int mgt_cdot(const void *a_dev, const void *b_dev, int64_t len, int n_rhs,
+             double *out_dev /* 2*n_rhs doubles */, void *stream);
+
+/* ---- Krylov solver -------------------------------------------------------- */
+/* Replaces gcr_solve (krylov.py:52-118) as the TruncatedInverse solver
+ * plugin (krylov.py:200-229): GPU-resident BiCGStab for (A + i tau g5) x = b
+ * (flags as in mgt_wilson_apply), zero initial guess, convergence confirmed
+ * on the explicitly recomputed residual ||b - A x|| <= tol ||b||
+ * (krylov.py:78-85, :113-118).  b_dev/x_dev: native layout, n_rhs
+ * independent systems solved together (shared link loads).
+ * report_out: per rhs, 4 int64 {iterations, matvecs, converged, reason}
+ * reason: 0 none, 1 max_iter, 2 breakdown; relres_out: per rhs final
+ * explicit relative residual.  If dot_out_host != NULL it receives per rhs
+ * the complex vdot(b, x) (2 doubles; the Hutchinson quadratic form,
+ * trace.py:104).  Host report arrays are written before the call returns. */
+size_t mgt_bicgstab_workspace_bytes(mgt_wilson_t h, int n_rhs);
+int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev,
+                       int n_rhs, int flags, double tau, double tol,
+                       int max_iter, void *workspace_dev,
+                       int64_t *report_out, double *relres_out,
+                       double *dot_out_host, void *stream);
+
+/* Fixed-iteration restarted GCR(m) with zero start (krylov.py:52-118 with
+ * max_iter = restart = m, as called by generate_null_vectors,
+ * multigrid.py:87-94): x <- GCR_m(A, b).  Returns the report like above. */
+size_t mgt_gcr_workspace_bytes(mgt_wilson_t h, int m);
+int mgt_gcr_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m,
+                  int max_iter, double tol, void *workspace_dev,
+                  int64_t *report_out, double *relres_out, void *stream);
+
+/* ---- probes -------------------------------------------------------------- */
+/* Bit-exact numpy PCG64 noise (probing.py:94-107): field j of n_fields is
+ * make_noise(N, kind, seed0 + j) with N = 12 V, given the seeded 128-bit
+ * states/incs of those seeds (host SeedSequence, 4 uint64 per field:
+ * state_hi, state_lo, inc_hi, inc_lo).  kind: 0 rademacher, 1 z4.
+ * Written in NATIVE layout (layout != 0) or ref layout (layout == 0). */
+int mgt_noise(const int dims[4], int kind, const uint64_t *seeds_host,
+              int n_fields, int native_layout, void *out_dev, void *stream);
+
+/* ---- prolongator ------------------------------------------------------------ */
+/* Block-orthonormal chirality-split prolongator (multigrid.py:116-225).
+ * P storage (native): for aggregate b (native coarse order, t slowest),
+ * chirality c, vector k < nv: 1536-entry (for 4^4 blocks) column
+ * P[((b*2 + c)*nv + k)*bs + j], j = q*S + s, S = sites per aggregate,
+ * q < 6 the spin-colour index within the chirality, s the site within the
+ * aggregate (native order).  Coarse vectors: (coarse_site_native, 2*nv)
+ * complex128, column order c*nv + k (multigrid.py:189-216). */
+int mgt_prolong_build(const int dims[4], const int block[4], int nv,
+                      const void *null_native_dev /* nv native fields */,
+                      void *P_dev, int *dropped_out, void *stream);
+int mgt_prolong(const int dims[4], const int block[4], int nv,
+                const void *P_dev, const void *xc_dev, void *x_native_dev,
+                int n_rhs, void *stream);
+int mgt_restrict(const int dims[4], const int block[4], int nv,
+                 const void *P_dev, const void *x_native_dev, void *xc_dev,
+                 int n_rhs, int gamma5_in, void *stream);
+
+/* ---- deflation projection (trace.py:161-188, :266-267; eigen.py:79-86) --- */
+/* H (k x s, column major, complex128) = V^H X;  V: (k, len) row-major
+ * vectors, X: (s, len). */
+int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k,
+                 int s, void *H_dev, void *stream);
+/* X[j] <- X[j] - sum_i V[i] H[i, j]   (X - V (V^H X) when H = V^H X) */
+int mgt_proj_sub(const void *V_dev, const void *H_dev, void *X_dev,
+                 int64_t len, int k, int s, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGTRACE_B200_H */

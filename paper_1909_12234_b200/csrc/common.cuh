@@ -1,0 +1,143 @@
+// Shared helpers for the mgtrace-b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/mgtrace_b200.h"
+
+namespace mgt {
+
+// ---- error plumbing (thread-local message, int codes across the ABI) -----
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+void note_launch(uint64_t n = 1);
+
+#define MGT_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return ::mgt::cuda_fail(_e, #call); \
+  } while (0)
+
+#define MGT_LAUNCH_CHECK(what)                          \
+  do {                                                  \
+    ::mgt::note_launch();                               \
+    cudaError_t _e = cudaGetLastError();                \
+    if (_e != cudaSuccess) return ::mgt::cuda_fail(_e, what); \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int kNumSMs = 148;
+
+// ---- complex arithmetic on double2 / float2 ------------------------------
+template <typename R> struct cplx_t;
+template <> struct cplx_t<double> { using type = double2; };
+template <> struct cplx_t<float> { using type = float2; };
+template <typename R> using cplx = typename cplx_t<R>::type;
+
+template <typename R> struct C {
+  R re, im;
+  __host__ __device__ C() = default;
+  __host__ __device__ constexpr C(R r, R i) : re(r), im(i) {}
+};
+
+template <typename R> __device__ __forceinline__ C<R> operator+(C<R> a, C<R> b) { return {a.re + b.re, a.im + b.im}; }
+template <typename R> __device__ __forceinline__ C<R> operator-(C<R> a, C<R> b) { return {a.re - b.re, a.im - b.im}; }
+template <typename R> __device__ __forceinline__ C<R> operator-(C<R> a) { return {-a.re, -a.im}; }
+template <typename R> __device__ __forceinline__ C<R> operator*(C<R> a, C<R> b) {
+  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+template <typename R> __device__ __forceinline__ C<R> operator*(R s, C<R> a) { return {s * a.re, s * a.im}; }
+template <typename R> __device__ __forceinline__ C<R> conj(C<R> a) { return {a.re, -a.im}; }
+// i * a
+template <typename R> __device__ __forceinline__ C<R> times_i(C<R> a) { return {-a.im, a.re}; }
+// conj(a) * b
+template <typename R> __device__ __forceinline__ C<R> cmul_conj(C<R> a, C<R> b) {
+  return {a.re * b.re + a.im * b.im, a.re * b.im - a.im * b.re};
+}
+// acc + a*b
+template <typename R> __device__ __forceinline__ C<R> cfma(C<R> a, C<R> b, C<R> acc) {
+  acc.re = fma(a.re, b.re, acc.re);
+  acc.re = fma(-a.im, b.im, acc.re);
+  acc.im = fma(a.re, b.im, acc.im);
+  acc.im = fma(a.im, b.re, acc.im);
+  return acc;
+}
+// acc + conj(a)*b
+template <typename R> __device__ __forceinline__ C<R> cfma_conj(C<R> a, C<R> b, C<R> acc) {
+  acc.re = fma(a.re, b.re, acc.re);
+  acc.re = fma(a.im, b.im, acc.re);
+  acc.im = fma(a.re, b.im, acc.im);
+  acc.im = fma(-a.im, b.re, acc.im);
+  return acc;
+}
+
+// streaming 128-bit / 64-bit loads through the read-only path
+__device__ __forceinline__ C<double> ldc(const double2 *p) {
+  double2 v = __ldg(p);
+  return {v.x, v.y};
+}
+__device__ __forceinline__ C<float> ldc(const float2 *p) {
+  float2 v = __ldg(p);
+  return {v.x, v.y};
+}
+__device__ __forceinline__ void stc(double2 *p, C<double> v) { *p = make_double2(v.re, v.im); }
+__device__ __forceinline__ void stc(float2 *p, C<float> v) { *p = make_float2(v.re, v.im); }
+// streaming store (evict-first): output fields are not re-read by this kernel
+__device__ __forceinline__ void stc_cs(double2 *p, C<double> v) { __stcs(p, make_double2(v.re, v.im)); }
+__device__ __forceinline__ void stc_cs(float2 *p, C<float> v) { __stcs(p, make_float2(v.re, v.im)); }
+
+// ---- lattice geometry -----------------------------------------------------
+// dims in reference order (L0, L1, L2, L3 = t).  Native site order:
+//   s = ((x3*L0 + x0)*L1 + x1)*L2 + x2   (x2 fastest, t slowest)
+struct Geom {
+  int L[4];
+  int64_t V;
+  // native strides for directions mu = 0..3
+  int64_t stride[4];
+};
+
+inline Geom make_geom(const int dims[4]) {
+  Geom g;
+  for (int i = 0; i < 4; ++i) g.L[i] = dims[i];
+  g.V = (int64_t)dims[0] * dims[1] * dims[2] * dims[3];
+  g.stride[2] = 1;
+  g.stride[1] = dims[2];
+  g.stride[0] = (int64_t)dims[1] * dims[2];
+  g.stride[3] = (int64_t)dims[0] * dims[1] * dims[2];
+  return g;
+}
+
+// native site -> coords (x0..x3)
+__host__ __device__ __forceinline__ void native_coords(const Geom &g, int64_t s, int x[4]) {
+  int64_t r = s;
+  x[2] = (int)(r % g.L[2]);
+  r /= g.L[2];
+  x[1] = (int)(r % g.L[1]);
+  r /= g.L[1];
+  x[0] = (int)(r % g.L[0]);
+  x[3] = (int)(r / g.L[0]);
+}
+
+__host__ __device__ __forceinline__ int64_t ref_site(const Geom &g, const int x[4]) {
+  return (((int64_t)x[0] * g.L[1] + x[1]) * g.L[2] + x[2]) * g.L[3] + x[3];
+}
+
+__host__ __device__ __forceinline__ int64_t native_site(const Geom &g, const int x[4]) {
+  return (((int64_t)x[3] * g.L[0] + x[0]) * g.L[1] + x[1]) * g.L[2] + x[2];
+}
+
+inline int grid_for(int64_t n, int block, int max_blocks_per_sm = 16) {
+  int64_t b = (n + block - 1) / block;
+  int64_t cap = (int64_t)kNumSMs * max_blocks_per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace mgt

@@ -1,0 +1,201 @@
+// Wilson-Dirac stencil core (4D, SU(3), DeGrand-Rossi gammas), sm_100a.
+//
+// Operator (restated from the reference's 2D assembly, lattice.py:274-318,
+// generalised to 4D SU(3)):
+//   (A z)(x) = (4 + m0) z(x)
+//            - 1/2 sum_mu [ (1 - g_mu) U_mu(x)        z(x+mu) ph_f
+//                         + (1 + g_mu) U_mu(x-mu)^dag z(x-mu) ph_b ]
+// ph = -1 on the hops that wrap in t when the boundary is antiperiodic
+// (lattice.py:91-102).  In the chiral DeGrand-Rossi basis every gamma_mu is
+// [[0, B_mu], [B_mu^dag, 0]] with B_mu unitary and monomial, so
+//   (1 -/+ g_mu) psi = ( h, -/+ B^dag h ),   h = psi_up -/+ B psi_dn,
+// i.e. each hop is a spin projection to a half spinor (6 complex), one
+// SU(3) multiply per half-spinor row, and a free reconstruction.  That is
+// 1320 flop/site for the 8 hops; the data each site streams is its 8
+// neighbour spinors (mostly cache hits) and its 4 forward links.
+#pragma once
+#include "common.cuh"
+
+namespace mgt {
+
+// (B_mu psi_dn): returns (o0, o1) from (psi2, psi3)
+template <int MU, typename R>
+__device__ __forceinline__ void b_mul(C<R> p2, C<R> p3, C<R> &o0, C<R> &o1) {
+  if constexpr (MU == 0) {  // B = [[0, i], [i, 0]]
+    o0 = times_i(p3);
+    o1 = times_i(p2);
+  } else if constexpr (MU == 1) {  // B = [[0, -1], [1, 0]]
+    o0 = -p3;
+    o1 = p2;
+  } else if constexpr (MU == 2) {  // B = [[i, 0], [0, -i]]
+    o0 = times_i(p2);
+    o1 = -times_i(p3);
+  } else {  // B = I
+    o0 = p2;
+    o1 = p3;
+  }
+}
+
+// (B_mu^dag w): returns (o2, o3) from (w0, w1)
+template <int MU, typename R>
+__device__ __forceinline__ void bdag_mul(C<R> w0, C<R> w1, C<R> &o2, C<R> &o3) {
+  if constexpr (MU == 0) {  // B^dag = [[0, -i], [-i, 0]]
+    o2 = -times_i(w1);
+    o3 = -times_i(w0);
+  } else if constexpr (MU == 1) {  // B^dag = [[0, 1], [-1, 0]]
+    o2 = w1;
+    o3 = -w0;
+  } else if constexpr (MU == 2) {  // B^dag = [[-i, 0], [0, i]]
+    o2 = -times_i(w0);
+    o3 = times_i(w1);
+  } else {
+    o2 = w0;
+    o3 = w1;
+  }
+}
+
+// Native link storage: element e of link (mu, site) at ((mu*NL + e)*V + site),
+// NL = 9 (full 3x3, row-major) or 6 (rows 0 and 1; row 2 = conj(r0 x r1)).
+template <typename R, int RECON>
+struct LinkField {
+  static constexpr int NL = RECON / 2;
+  const cplx<R> *__restrict__ p;
+  int64_t V;
+  __device__ __forceinline__ void load(int mu, int64_t site, C<R> (&u)[3][3]) const {
+    const cplx<R> *q = p + (int64_t)mu * NL * V + site;
+#pragma unroll
+    for (int e = 0; e < NL; ++e) u[e / 3][e % 3] = ldc(q + e * V);
+    if constexpr (RECON == 12) {
+      // u2 = conj(u0 x u1)  (exact for SU(3): det = 1, unitary)
+      u[2][0] = conj(u[0][1] * u[1][2] - u[0][2] * u[1][1]);
+      u[2][1] = conj(u[0][2] * u[1][0] - u[0][0] * u[1][2]);
+      u[2][2] = conj(u[0][0] * u[1][1] - u[0][1] * u[1][0]);
+    }
+  }
+};
+
+// Accumulate one hop into acc[spin][colour] (without the -1/2).
+template <int MU, bool FWD, typename R, int RECON>
+__device__ __forceinline__ void wilson_hop(const Geom &g, const cplx<R> *__restrict__ in,
+                                           const LinkField<R, RECON> &links, int64_t site,
+                                           const int (&x)[4], R g5in, bool antiperiodic,
+                                           C<R> (&acc)[4][3]) {
+  const int L = g.L[MU];
+  const int64_t st = g.stride[MU];
+  int64_t nb;
+  R ph = R(1);
+  if constexpr (FWD) {
+    nb = (x[MU] == L - 1) ? site - (int64_t)(L - 1) * st : site + st;
+    if (MU == 3 && antiperiodic && x[3] == L - 1) ph = R(-1);
+  } else {
+    nb = (x[MU] == 0) ? site + (int64_t)(L - 1) * st : site - st;
+    if (MU == 3 && antiperiodic && x[3] == 0) ph = R(-1);
+  }
+  const int64_t V = g.V;
+  // spin projection
+  C<R> h[2][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    C<R> p0 = ldc(in + (0 * 3 + c) * V + nb);
+    C<R> p1 = ldc(in + (1 * 3 + c) * V + nb);
+    C<R> p2 = g5in * ldc(in + (2 * 3 + c) * V + nb);
+    C<R> p3 = g5in * ldc(in + (3 * 3 + c) * V + nb);
+    C<R> b0, b1;
+    b_mul<MU>(p2, p3, b0, b1);
+    if constexpr (FWD) {
+      h[0][c] = p0 - b0;
+      h[1][c] = p1 - b1;
+    } else {
+      h[0][c] = p0 + b0;
+      h[1][c] = p1 + b1;
+    }
+  }
+  // colour multiply: U h (forward) or U^dag h (backward, link of x - mu)
+  C<R> u[3][3];
+  links.load(MU, FWD ? site : nb, u);
+  C<R> w[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      C<R> s(R(0), R(0));
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if constexpr (FWD)
+          s = cfma(u[i][j], h[a][j], s);
+        else
+          s = cfma_conj(u[j][i], h[a][j], s);
+      }
+      w[a][i] = ph * s;
+    }
+  }
+  // reconstruction
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    acc[0][i] = acc[0][i] + w[0][i];
+    acc[1][i] = acc[1][i] + w[1][i];
+    C<R> o2, o3;
+    bdag_mul<MU>(w[0][i], w[1][i], o2, o3);
+    if constexpr (FWD) {
+      acc[2][i] = acc[2][i] - o2;
+      acc[3][i] = acc[3][i] - o3;
+    } else {
+      acc[2][i] = acc[2][i] + o2;
+      acc[3][i] = acc[3][i] + o3;
+    }
+  }
+}
+
+struct WilsonParams {
+  Geom g;
+  int antiperiodic;
+  double diag_up_re, diag_up_im;  // (4 + m0) + i tau   acting on spins 0,1
+  double diag_dn_re, diag_dn_im;  // (4 + m0) - i tau   acting on spins 2,3
+  double g5in, g5out;             // +1 or -1
+};
+
+// y = G_out [ diag z - 1/2 hop(z) ],  z = G_in x.  Also returns the raw input
+// x at the site (xc, before G_in) for fused epilogues.
+template <typename R, int RECON>
+__device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R> *__restrict__ in,
+                                            const LinkField<R, RECON> &links, int64_t site,
+                                            C<R> (&y)[4][3], C<R> (&xc)[4][3]) {
+  int x[4];
+  native_coords(P.g, site, x);
+  const R g5in = (R)P.g5in;
+  const bool ap = P.antiperiodic != 0;
+  C<R> acc[4][3];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[a][c] = C<R>(R(0), R(0));
+  wilson_hop<0, true>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<0, false>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<1, true>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<1, false>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<2, true>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<2, false>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<3, true>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<3, false>(P.g, in, links, site, x, g5in, ap, acc);
+  const C<R> dup((R)P.diag_up_re, (R)P.diag_up_im);
+  const C<R> ddn((R)P.diag_dn_re, (R)P.diag_dn_im);
+  const R half = R(0.5);
+  const R g5out = (R)P.g5out;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      C<R> v = ldc(in + (a * 3 + c) * P.g.V + site);
+      xc[a][c] = v;
+      if (a >= 2) {
+        v = g5in * v;
+        C<R> r = ddn * v - half * acc[a][c];
+        y[a][c] = g5out * r;
+      } else {
+        y[a][c] = dup * v - half * acc[a][c];
+      }
+    }
+  }
+}
+
+}  // namespace mgt

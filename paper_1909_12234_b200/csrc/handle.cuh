@@ -1,0 +1,51 @@
+// The opaque Wilson operator handle shared by the operator / solver units.
+#pragma once
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "dslash_core.cuh"
+
+struct mgt_wilson_s {
+  mgt::Geom g;
+  int antiperiodic;
+  double mass;
+  int prec;   // 64 or 32
+  int recon;  // 18 or 12
+  void *links;  // native link storage (owned)
+  size_t link_bytes;
+  // pinned host mailbox for solver convergence flags
+  int *host_flags;
+};
+
+namespace mgt {
+
+inline WilsonParams make_params(const mgt_wilson_s *h, int flags, double tau) {
+  WilsonParams P;
+  P.g = h->g;
+  P.antiperiodic = h->antiperiodic;
+  double g5in = 1.0, g5out = 1.0, t = tau;
+  if (flags & MGT_G5_IN) g5in = -g5in;
+  if (flags & MGT_G5_OUT) g5out = -g5out;
+  if (flags & MGT_DAGGER) {
+    // (A + i tau g5)^dag = g5 (A - i tau g5) g5
+    g5in = -g5in;
+    g5out = -g5out;
+    t = -t;
+  }
+  P.diag_up_re = 4.0 + h->mass;
+  P.diag_up_im = t;
+  P.diag_dn_re = 4.0 + h->mass;
+  P.diag_dn_im = -t;
+  P.g5in = g5in;
+  P.g5out = g5out;
+  return P;
+}
+
+// launch y = op(x) for n_rhs native fields (defined in wilson.cu)
+int wilson_apply_native(const mgt_wilson_s *h, const void *x, void *y, int n_rhs, int flags,
+                        double tau, cudaStream_t st);
+
+}  // namespace mgt

@@ -1,0 +1,75 @@
+// Deterministic fixed-order reductions fused into streaming kernels.
+//
+// Each kernel runs a fixed grid (grid-stride loops), so the assignment of
+// sites to threads, the in-thread summation order, the warp-shuffle trees
+// and the final cross-block sum are all fixed: results are bitwise
+// reproducible run to run (the reference promises byte-identical reruns,
+// trace.py:95-97).  The last block to finish (atomic ticket)
+// sums the per-block partials and runs a scalar "finisher" callback, so a
+// reduction costs no extra launch.
+#pragma once
+#include "common.cuh"
+
+namespace mgt {
+
+constexpr int kRedBlock = 128;  // threads per block in reducing kernels
+constexpr int kRedWarps = kRedBlock / 32;
+
+// Sum `v[NV]` over the threads of the block that share the same rhs slot
+// (rhs = lane % NR) and publish NR*NV partials for this block.  Returns true
+// in every thread of the LAST block to arrive, after which `partials` holds
+// all blocks' values.
+template <int NR, int NV>
+__device__ __forceinline__ bool reduce_publish(double (&v)[NV], double *partials, unsigned *ticket) {
+  __shared__ double sm[kRedWarps][NR * NV];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int off = 16; off >= NR; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    v[k] = x;
+  }
+  if (lane < NR) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sm[warp][lane * NV + k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < NR * NV) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kRedWarps; ++w) s += sm[w][threadIdx.x];
+    partials[(size_t)blockIdx.x * NR * NV + threadIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  return last;
+}
+
+// In the last block: out[j] = sum_b partials[b*M + j] for j < M (fixed
+// order), then reset the ticket.  Result visible to the whole block.
+template <int M>
+__device__ __forceinline__ void reduce_finish(const double *partials, unsigned *ticket, double (&out)[M]) {
+  __shared__ double res[M > 0 ? M : 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = gridDim.x;
+  for (int j = warp; j < M; j += kRedWarps) {
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += __ldcg(partials + (size_t)b * M + j);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) res[j] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < M; ++j) out[j] = res[j];
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+}  // namespace mgt

@@ -1,0 +1,202 @@
+// Wilson-Dirac operator handle and the plain apply kernel (C ABI).
+#include <atomic>
+#include <cstring>
+#include <string>
+
+#include "handle.cuh"
+
+namespace mgt {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char *what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return MGT_ERR_CUDA;
+}
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------------------
+// links: reference layout (V_ref, 4, 3, 3) complex128 -> native SoA
+template <typename R, int RECON>
+__global__ void links_from_ref_kernel(Geom g, const double2 *__restrict__ ref, cplx<R> *__restrict__ out) {
+  constexpr int NL = RECON / 2;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < g.V; s += (int64_t)gridDim.x * blockDim.x) {
+    int x[4];
+    native_coords(g, s, x);
+    const int64_t r = ref_site(g, x);
+#pragma unroll
+    for (int mu = 0; mu < 4; ++mu) {
+#pragma unroll
+      for (int e = 0; e < NL; ++e) {
+        double2 v = ref[(r * 4 + mu) * 9 + e];
+        cplx<R> o;
+        o.x = (R)v.x;
+        o.y = (R)v.y;
+        out[((int64_t)mu * NL + e) * g.V + s] = o;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plain apply: one thread per (site, rhs-in-group of NR), links shared by the
+// NR threads of a site through L1 broadcast.
+template <typename R, int RECON, int NR>
+__global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4)) wilson_apply_kernel(WilsonParams P, const cplx<R> *__restrict__ in,
+                                                           cplx<R> *__restrict__ out, LinkField<R, RECON> links) {
+  const int64_t n = P.g.V * NR;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t site = idx / NR;
+    const int rhs = (int)(idx % NR);
+    const cplx<R> *inr = in + (int64_t)rhs * 12 * P.g.V;
+    cplx<R> *outr = out + (int64_t)rhs * 12 * P.g.V;
+    C<R> y[4][3], xc[4][3];
+    wilson_eval<R, RECON>(P, inr, links, site, y, xc);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) stc_cs(outr + (a * 3 + c) * P.g.V + site, y[a][c]);
+  }
+}
+
+template <typename R, int RECON, int NR>
+static int launch_apply(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, cudaStream_t st) {
+  LinkField<R, RECON> lf{reinterpret_cast<const cplx<R> *>(h->links), h->g.V};
+  const int block = 128;
+  const int grid = grid_for(h->g.V * NR, block, 64);
+  wilson_apply_kernel<R, RECON, NR><<<grid, block, 0, st>>>(P, reinterpret_cast<const cplx<R> *>(x),
+                                                             reinterpret_cast<cplx<R> *>(y), lf);
+  MGT_LAUNCH_CHECK("wilson_apply_kernel");
+  return MGT_OK;
+}
+
+template <typename R, int RECON>
+static int apply_groups(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, int n_rhs,
+                        cudaStream_t st) {
+  const size_t field = (size_t)12 * h->g.V * sizeof(cplx<R>);
+  const char *xb = reinterpret_cast<const char *>(x);
+  char *yb = reinterpret_cast<char *>(y);
+  int r = 0;
+  while (r < n_rhs) {
+    int left = n_rhs - r, rc;
+    if (left >= 4) {
+      rc = launch_apply<R, RECON, 4>(h, P, xb + r * field, yb + r * field, st);
+      r += 4;
+    } else if (left >= 2) {
+      rc = launch_apply<R, RECON, 2>(h, P, xb + r * field, yb + r * field, st);
+      r += 2;
+    } else {
+      rc = launch_apply<R, RECON, 1>(h, P, xb + r * field, yb + r * field, st);
+      r += 1;
+    }
+    if (rc) return rc;
+  }
+  return MGT_OK;
+}
+
+int wilson_apply_native(const mgt_wilson_s *h, const void *x, void *y, int n_rhs, int flags, double tau,
+                        cudaStream_t st) {
+  WilsonParams P = make_params(h, flags, tau);
+  if (h->prec == 64) {
+    if (h->recon == 18) return apply_groups<double, 18>(h, P, x, y, n_rhs, st);
+    return apply_groups<double, 12>(h, P, x, y, n_rhs, st);
+  }
+  if (h->recon == 18) return apply_groups<float, 18>(h, P, x, y, n_rhs, st);
+  return apply_groups<float, 12>(h, P, x, y, n_rhs, st);
+}
+
+}  // namespace mgt
+
+using namespace mgt;
+
+extern "C" {
+
+const char *mgt_last_error(void) { return g_last_error.c_str(); }
+int mgt_version(void) { return 1; }
+uint64_t mgt_launch_count(void) { return g_launches.load(); }
+
+int mgt_wilson_create(mgt_wilson_t *out, const int dims[4], int antiperiodic, double mass, int prec, int recon,
+                      const void *links_ref_dev, void *stream) {
+  if (!out || !dims || !links_ref_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_create: null argument");
+  for (int i = 0; i < 4; ++i)
+    if (dims[i] < 2) return fail(MGT_ERR_INVALID, "extent < 2 is not a valid lattice");
+  if (prec != 64 && prec != 32) return fail(MGT_ERR_INVALID, "prec must be 64 or 32");
+  if (recon != 18 && recon != 12) return fail(MGT_ERR_INVALID, "recon must be 18 or 12");
+  Geom g = make_geom(dims);
+  if (g.V * 12 * 8 >= ((int64_t)1 << 31) * 8) return fail(MGT_ERR_INVALID, "lattice too large for one GPU handle");
+  auto *h = new mgt_wilson_s();
+  h->g = g;
+  h->antiperiodic = antiperiodic;
+  h->mass = mass;
+  h->prec = prec;
+  h->recon = recon;
+  const size_t csz = prec == 64 ? sizeof(double2) : sizeof(float2);
+  h->link_bytes = (size_t)4 * (recon / 2) * g.V * csz;
+  cudaError_t e = cudaMalloc(&h->links, h->link_bytes);
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_fail(e, "cudaMalloc(links)");
+  }
+  e = cudaMallocHost(&h->host_flags, 64 * sizeof(int));
+  if (e != cudaSuccess) {
+    cudaFree(h->links);
+    delete h;
+    return cuda_fail(e, "cudaMallocHost(flags)");
+  }
+  cudaStream_t st = as_stream(stream);
+  const int block = 256, grid = grid_for(g.V, block, 8);
+  const double2 *ref = reinterpret_cast<const double2 *>(links_ref_dev);
+  if (prec == 64 && recon == 18)
+    links_from_ref_kernel<double, 18><<<grid, block, 0, st>>>(g, ref, (double2 *)h->links);
+  else if (prec == 64)
+    links_from_ref_kernel<double, 12><<<grid, block, 0, st>>>(g, ref, (double2 *)h->links);
+  else if (recon == 18)
+    links_from_ref_kernel<float, 18><<<grid, block, 0, st>>>(g, ref, (float2 *)h->links);
+  else
+    links_from_ref_kernel<float, 12><<<grid, block, 0, st>>>(g, ref, (float2 *)h->links);
+  note_launch();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFree(h->links);
+    cudaFreeHost(h->host_flags);
+    delete h;
+    return cuda_fail(e, "links_from_ref_kernel");
+  }
+  *out = h;
+  return MGT_OK;
+}
+
+int mgt_wilson_destroy(mgt_wilson_t h) {
+  if (!h) return MGT_OK;
+  cudaFree(h->links);
+  cudaFreeHost(h->host_flags);
+  delete h;
+  return MGT_OK;
+}
+
+int mgt_wilson_info(mgt_wilson_t h, int dims[4], int *prec, int *recon, int64_t *volume) {
+  if (!h) return fail(MGT_ERR_INVALID, "null handle");
+  if (dims)
+    for (int i = 0; i < 4; ++i) dims[i] = h->g.L[i];
+  if (prec) *prec = h->prec;
+  if (recon) *recon = h->recon;
+  if (volume) *volume = h->g.V;
+  return MGT_OK;
+}
+
+int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs, int flags, double tau,
+                     void *stream) {
+  if (!h || !x_dev || !y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply: null argument");
+  if (n_rhs < 1) return fail(MGT_ERR_INVALID, "n_rhs must be >= 1");
+  if (x_dev == y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply: in-place apply is not supported");
+  return wilson_apply_native(h, x_dev, y_dev, n_rhs, flags, tau, as_stream(stream));
+}
+
+}  // extern "C"

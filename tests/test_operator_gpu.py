@@ -1,0 +1,140 @@
+"""GPU parity of the Wilson-Dirac stencil against the CPU oracle
+(oracle/wilson4d.py, the 4D restatement of lattice.py:274-318).
+
+Tolerance (BASELINE.json north_star): A x agrees to 1e-12 relative in fp64;
+complex64 is checked against the fp64 oracle at 2e-6 relative."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import wilson4d as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu():
+    import paper_1909_12234_b200 as M
+    return M
+
+
+def _setup(dims, eps, seed=0, mass=0.1, prec=64, recon=18, boundary="antiperiodic"):
+    M = _gpu()
+    geo = M.LatticeGeometry(dims, boundary)
+    gauge = M.generate_gauge(geo, "su3", eps=eps, seed=seed)
+    op = M.build_wilson(gauge, mass, prec=prec, recon=recon)
+    links = gauge.links.cpu().numpy()
+    return M, geo, gauge, op, links
+
+
+def _rand(n, seed, k=None):
+    rng = np.random.default_rng(seed)
+    shape = (n,) if k is None else (n, k)
+    return (rng.normal(size=shape) + 1j * rng.normal(size=shape)) / np.sqrt(2)
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("dims,eps", [((4, 4, 4, 4), 0.2), ((4, 6, 8, 10), 0.5), ((2, 4, 2, 6), 0.3)])
+def test_links_match_oracle_generator(cuda, dims, eps):
+    M, geo, gauge, op, links = _setup(dims, eps, seed=3)
+    ref = W.su3_links(dims, eps, 3)
+    assert np.abs(links - ref).max() < 1e-13
+    gauge.validate(1e-12)
+
+
+@pytest.mark.parametrize("dims,eps", [((8, 8, 8, 8), 0.2), ((8, 8, 8, 8), 0.5), ((4, 6, 8, 10), 0.2),
+                                      ((2, 4, 2, 6), 0.3)])
+@pytest.mark.parametrize("recon", [18, 12])
+def test_apply_matches_oracle_csr(cuda, dims, eps, recon):
+    M, geo, gauge, op, links = _setup(dims, eps, recon=recon)
+    A = W.build_wilson4d_csr(links, dims, 0.1)
+    x = _rand(op.dim, 11)
+    y = op.apply(x)
+    assert _rel(y, A @ x) < 1e-12
+
+
+@pytest.mark.parametrize("boundary", ["periodic", "antiperiodic"])
+def test_apply_variants(cuda, boundary):
+    dims = (4, 4, 6, 8)
+    M, geo, gauge, op, links = _setup(dims, 0.3, boundary=boundary)
+    A = W.build_wilson4d_csr(links, dims, 0.1, antiperiodic=boundary == "antiperiodic")
+    g5 = W.gamma5_diag(geo.site_count)
+    x = _rand(op.dim, 5)
+    assert _rel(op.apply(x), A @ x) < 1e-12
+    assert _rel(op.apply_dagger(x), A.conj().T @ x) < 1e-12
+    assert _rel(op.hermitian_form().apply(x), g5 * (A @ x)) < 1e-12
+    assert _rel(op.a_gamma5().apply(x), A @ (g5 * x)) < 1e-12
+    assert _rel(op.apply_shifted(0.5, x), A @ x + 0.5j * g5 * x) < 1e-12
+    assert np.array_equal(op.apply_shifted(0.0, x), op.apply(x))
+    assert _rel(op.shifted(-0.25).apply(x), A @ x - 0.25j * g5 * x) < 1e-12
+    # gamma5-Hermiticity (SPEC.md lattice invariants)
+    y = _rand(op.dim, 6)
+    lhs = np.vdot(y, g5 * op.apply(g5 * x))
+    rhs = np.vdot(op.apply(y), x)
+    assert abs(lhs - rhs) < 1e-12 * np.linalg.norm(x) * np.linalg.norm(y) * 10
+
+
+def test_multi_rhs_columns(cuda):
+    dims = (4, 4, 4, 8)
+    M, geo, gauge, op, links = _setup(dims, 0.2)
+    A = W.build_wilson4d_csr(links, dims, 0.1)
+    for k in (2, 3, 4, 5, 8):
+        X = _rand(op.dim, 20 + k, k)
+        Y = op.apply(X)
+        assert Y.shape == X.shape
+        assert _rel(Y, A @ X) < 1e-12
+
+
+def test_large_lattice_matches_stencil(cuda):
+    dims = (16, 16, 16, 16)
+    M, geo, gauge, op, links = _setup(dims, 0.2)
+    x = _rand(op.dim, 2)
+    assert _rel(op.apply(x), W.apply_stencil(links, dims, 0.1, x)) < 1e-12
+
+
+def test_plane_wave_kat(cuda):
+    dims = (4, 4, 6, 8)
+    M = _gpu()
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    op = M.build_wilson(M.generate_gauge(geo, "unit"), 0.1)
+    rng = np.random.default_rng(0)
+    for k in [(1, 2, 3, 4), (0, 0, 0, 0), (3, 1, 5, 7)]:
+        p, Mp = W.plane_wave_symbol(dims, 0.1, k)
+        chi = rng.normal(size=(4, 3)) + 1j * rng.normal(size=(4, 3))
+        v = W.plane_wave(dims, p, chi)
+        assert _rel(op.apply(v), W.plane_wave(dims, p, Mp @ chi)) < 1e-13
+
+
+def test_complex64_against_fp64_oracle(cuda):
+    dims = (8, 8, 8, 8)
+    for recon in (18, 12):
+        M, geo, gauge, op, links = _setup(dims, 0.2, prec=32, recon=recon)
+        A = W.build_wilson4d_csr(links, dims, 0.1)
+        x = _rand(op.dim, 9)
+        assert _rel(op.apply(x), A @ x) < 2e-6
+
+
+def test_layout_roundtrip_exact(cuda):
+    M, geo, gauge, op, links = _setup((4, 6, 8, 10), 0.2)
+    x = torch.as_tensor(_rand(op.dim, 3, 3).T.copy(), device=cuda)
+    back = op.from_native(op.to_native(x))
+    assert torch.equal(back, x)
+
+
+def test_dimension_mismatch_raises(cuda):
+    M, geo, gauge, op, links = _setup((4, 4, 4, 4), 0.2)
+    with pytest.raises(ValueError):
+        op.apply(np.zeros(op.dim - 12, dtype=np.complex128))
+
+
+def test_dense_guard(cuda):
+    M, geo, gauge, op, links = _setup((4, 4, 4, 4), 0.2)
+    with pytest.raises(M.SizeGuardError):
+        op.dense()
+    M2, geo2, gauge2, op2, links2 = _setup((2, 2, 2, 4), 0.2)
+    D = op2.dense()
+    A = W.build_wilson4d_csr(links2, (2, 2, 2, 4), 0.1).toarray()
+    assert np.abs(D - A).max() < 1e-13
