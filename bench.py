@@ -287,7 +287,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dims", default="48x48x48x96")
     ap.add_argument("--prec", type=int, default=64, choices=[64, 32])
-    ap.add_argument("--recon", type=int, default=18, choices=[18, 12])
+    ap.add_argument("--recon", type=int, default=12, choices=[18, 12])
     ap.add_argument("--skip-probes", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -105,17 +105,16 @@ __global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *_
 
 // K1: v = A p ; sigma = (rhat, v)
 template <int NR, int RECON>
-__global__ void __launch_bounds__(kRedBlock) bi_k1(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
   if (!any_running<NR>(w.st)) return;
-  int run[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) run[r] = (w.st[r].status == ST_RUN);
+  const int my = threadIdx.x % NR;  // blockDim and the grid stride are multiples of NR
+  const bool run_me = (w.st[my].status == ST_RUN);
   const int64_t V = P.g.V, n = V * NR;
   double acc[2] = {0.0, 0.0};
   FOR_SITES(NR) {
-    const int64_t site = idx / NR;
+    const int64_t site = sched_site(P.sched, idx / NR);
     const int rhs = (int)(idx % NR);
-    if (!run[rhs]) continue;
+    if (!run_me) continue;
     const int64_t off = (int64_t)rhs * 12 * V;
     C<double> y[4][3], xc[4][3];
     wilson_eval<double, RECON>(P, w.p + off, L, site, y, xc);
@@ -133,7 +132,7 @@ __global__ void __launch_bounds__(kRedBlock) bi_k1(WilsonParams P, LinkField<dou
   if (reduce_publish<NR, 2>(acc, w.partials, w.ticket)) {
     double out[NR * 2];
     reduce_finish<NR * 2>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && run[threadIdx.x]) {
+    if (threadIdx.x < NR && run_me) {
       BiState &s = w.st[threadIdx.x];
       C<double> sigma(out[2 * threadIdx.x], out[2 * threadIdx.x + 1]);
       s.matvecs += 1;
@@ -151,21 +150,16 @@ __global__ void __launch_bounds__(kRedBlock) bi_k1(WilsonParams P, LinkField<dou
 template <int NR>
 __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
   if (!any_running<NR>(w.st)) return;
-  int run[NR];
-  C<double> alpha[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    run[r] = (w.st[r].status == ST_RUN);
-    alpha[r] = w.st[r].alpha;
-  }
+  const int my = threadIdx.x % NR;
+  const bool run_me = (w.st[my].status == ST_RUN);
+  const C<double> al = w.st[my].alpha;
   const int64_t n = V * NR;
   double acc[1] = {0.0};
   FOR_SITES(NR) {
     const int64_t site = idx / NR;
     const int rhs = (int)(idx % NR);
-    if (!run[rhs]) continue;
+    if (!run_me) continue;
     const int64_t base = (int64_t)rhs * 12 * V + site;
-    const C<double> al = alpha[rhs];
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
       const int64_t o = base + (int64_t)c * V;
@@ -178,7 +172,7 @@ __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && run[threadIdx.x]) {
+    if (threadIdx.x < NR && run_me) {
       BiState &s = w.st[threadIdx.x];
       s.s2 = out[threadIdx.x];
       s.half = (s.s2 <= s.tol2) ? 1 : 0;
@@ -188,17 +182,16 @@ __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
 
 // K3: t = A s ; (t, s), |t|^2
 template <int NR, int RECON>
-__global__ void __launch_bounds__(kRedBlock) bi_k3(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
   if (!any_running<NR>(w.st)) return;
-  int run[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) run[r] = (w.st[r].status == ST_RUN);
+  const int my = threadIdx.x % NR;  // blockDim and the grid stride are multiples of NR
+  const bool run_me = (w.st[my].status == ST_RUN);
   const int64_t V = P.g.V, n = V * NR;
   double acc[3] = {0.0, 0.0, 0.0};
   FOR_SITES(NR) {
-    const int64_t site = idx / NR;
+    const int64_t site = sched_site(P.sched, idx / NR);
     const int rhs = (int)(idx % NR);
-    if (!run[rhs]) continue;
+    if (!run_me) continue;
     const int64_t off = (int64_t)rhs * 12 * V;
     C<double> y[4][3], xc[4][3];
     wilson_eval<double, RECON>(P, w.s + off, L, site, y, xc);
@@ -217,7 +210,7 @@ __global__ void __launch_bounds__(kRedBlock) bi_k3(WilsonParams P, LinkField<dou
   if (reduce_publish<NR, 3>(acc, w.partials, w.ticket)) {
     double out[NR * 3];
     reduce_finish<NR * 3>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && run[threadIdx.x]) {
+    if (threadIdx.x < NR && run_me) {
       BiState &s = w.st[threadIdx.x];
       C<double> ts(out[3 * threadIdx.x], out[3 * threadIdx.x + 1]);
       const double tt = out[3 * threadIdx.x + 2];
@@ -238,22 +231,16 @@ __global__ void __launch_bounds__(kRedBlock) bi_k3(WilsonParams P, LinkField<dou
 template <int NR>
 __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, double2 *__restrict__ x, BiWS w) {
   if (!any_running<NR>(w.st)) return;
-  int run[NR];
-  C<double> alpha[NR], omega[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    run[r] = (w.st[r].status == ST_RUN);
-    alpha[r] = w.st[r].alpha;
-    omega[r] = w.st[r].omega;
-  }
+  const int my = threadIdx.x % NR;
+  const bool run_me = (w.st[my].status == ST_RUN);
+  const C<double> al = w.st[my].alpha, om = w.st[my].omega;
   const int64_t n = V * NR;
   double acc[3] = {0.0, 0.0, 0.0};
   FOR_SITES(NR) {
     const int64_t site = idx / NR;
     const int rhs = (int)(idx % NR);
-    if (!run[rhs]) continue;
+    if (!run_me) continue;
     const int64_t base = (int64_t)rhs * 12 * V + site;
-    const C<double> al = alpha[rhs], om = omega[rhs];
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
       const int64_t o = base + (int64_t)c * V;
@@ -270,7 +257,7 @@ __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, double2 *__restric
   if (reduce_publish<NR, 3>(acc, w.partials, w.ticket)) {
     double out[NR * 3];
     reduce_finish<NR * 3>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && run[threadIdx.x]) {
+    if (threadIdx.x < NR && run_me) {
       BiState &s = w.st[threadIdx.x];
       C<double> rho_new(out[3 * threadIdx.x], out[3 * threadIdx.x + 1]);
       s.r2 = out[3 * threadIdx.x + 2];
@@ -296,21 +283,15 @@ __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, double2 *__restric
 template <int NR>
 __global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWS w) {
   if (!any_running<NR>(w.st)) return;
-  int run[NR];
-  C<double> beta[NR], omega[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    run[r] = (w.st[r].status == ST_RUN);
-    beta[r] = w.st[r].beta;
-    omega[r] = w.st[r].omega;
-  }
+  const int my = threadIdx.x % NR;
+  const bool run_me = (w.st[my].status == ST_RUN);
+  const C<double> be = w.st[my].beta, om = w.st[my].omega;
   const int64_t n = V * NR;
   FOR_SITES(NR) {
     const int64_t site = idx / NR;
     const int rhs = (int)(idx % NR);
-    if (!run[rhs]) continue;
+    if (!run_me) continue;
     const int64_t base = (int64_t)rhs * 12 * V + site;
-    const C<double> be = beta[rhs], om = omega[rhs];
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
       const int64_t o = base + (int64_t)c * V;
@@ -323,23 +304,24 @@ __global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWS w) {
 // True residual r = b - A x for every rhs that stopped (status CONV/MAXIT/
 // BREAK); records |r|^2 in true_r2.
 template <int NR, int RECON>
-__global__ void __launch_bounds__(kRedBlock) bi_resid(WilsonParams P, LinkField<double, RECON> L, const double2 *__restrict__ b,
+__global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkField<double, RECON> L, const double2 *__restrict__ b,
                                                       const double2 *__restrict__ x, BiWS w) {
-  int act[NR];
   bool any = false;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const int st = w.st[r].status;
-    act[r] = (st == ST_CONV || st == ST_MAXIT || st == ST_BREAK);
-    any |= act[r];
+    any |= (st == ST_CONV || st == ST_MAXIT || st == ST_BREAK);
   }
   if (!any) return;
+  const int my = threadIdx.x % NR;
+  const int st_me = w.st[my].status;
+  const bool act_me = (st_me == ST_CONV || st_me == ST_MAXIT || st_me == ST_BREAK);
   const int64_t V = P.g.V, n = V * NR;
   double acc[1] = {0.0};
   FOR_SITES(NR) {
-    const int64_t site = idx / NR;
+    const int64_t site = sched_site(P.sched, idx / NR);
     const int rhs = (int)(idx % NR);
-    if (!act[rhs]) continue;
+    if (!act_me) continue;
     const int64_t off = (int64_t)rhs * 12 * V;
     C<double> y[4][3], xc[4][3];
     wilson_eval<double, RECON>(P, x + off, L, site, y, xc);
@@ -356,7 +338,7 @@ __global__ void __launch_bounds__(kRedBlock) bi_resid(WilsonParams P, LinkField<
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && act[threadIdx.x]) {
+    if (threadIdx.x < NR && act_me) {
       BiState &s = w.st[threadIdx.x];
       s.true_r2 = out[threadIdx.x];
       s.matvecs += 1;
@@ -377,20 +359,15 @@ __global__ void __launch_bounds__(kRedBlock) bi_resid(WilsonParams P, LinkField<
 // Restart for rhs flagged ST_RESTART: rhat = p = r (r holds the true residual)
 template <int NR>
 __global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w) {
-  int act[NR];
-  bool any = false;
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    act[r] = (w.st[r].status == ST_RESTART);
-    any |= act[r];
-  }
-  if (!any) return;
+  if (!any_running<NR>(w.st, ST_RESTART)) return;
+  const int my = threadIdx.x % NR;
+  const bool act_me = (w.st[my].status == ST_RESTART);
   const int64_t n = V * NR;
   double acc[1] = {0.0};
   FOR_SITES(NR) {
     const int64_t site = idx / NR;
     const int rhs = (int)(idx % NR);
-    if (!act[rhs]) continue;
+    if (!act_me) continue;
     const int64_t base = (int64_t)rhs * 12 * V + site;
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
@@ -404,7 +381,7 @@ __global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w) {
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && act[threadIdx.x]) {
+    if (threadIdx.x < NR && act_me) {
       BiState &s = w.st[threadIdx.x];
       s.r2 = out[threadIdx.x];
       s.rho = C<double>(s.r2, 0.0);
@@ -452,7 +429,7 @@ struct WSLayout {
 static WSLayout ws_layout(int64_t V, int NRmax) {
   WSLayout L;
   L.field = align_up((size_t)NRmax * 12 * V * sizeof(double2), 256);
-  L.grid = grid_for(V * NRmax, kRedBlock, 8);
+  L.grid = kNumSMs * 16;  // upper bound of any resident grid at 128 threads
   L.partials = align_up((size_t)L.grid * NRmax * 4 * sizeof(double), 256);
   L.total = 6 * L.field + L.partials + 256 /*ticket*/ + align_up(NRmax * sizeof(BiState), 256);
   return L;
@@ -474,7 +451,12 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, const double2 *b,
   w.ticket = (unsigned *)q; q += 256;
   w.st = (BiState *)q;
   LinkField<double, RECON> lf{reinterpret_cast<const double2 *>(h->links), V};
-  const int grid = grid_for(V * NR, kRedBlock, 8);
+  // resident grids (occupancy-derived), cached per template instance
+  static int g_dsl = 0, g_str = 0;
+  if (!g_dsl) g_dsl = resident_grid(bi_k1<NR, RECON>, kRedBlock, (int64_t)1 << 40);
+  if (!g_str) g_str = resident_grid(bi_k4<NR>, kRedBlock, (int64_t)1 << 40);
+  const int64_t need = (V * NR + kRedBlock - 1) / kRedBlock;
+  const int gd = (int)std::min<int64_t>(g_dsl, need), grid = (int)std::min<int64_t>(g_str, need);
   MGT_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(unsigned), st));
   bi_init<NR><<<grid, kRedBlock, 0, st>>>(V, b, x, w, tol, max_iter);
   MGT_LAUNCH_CHECK("bi_init");
@@ -482,9 +464,9 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, const double2 *b,
   int chunk = 4;
   for (int round = 0; round < 1000000; ++round) {
     for (int it = 0; it < chunk; ++it) {
-      bi_k1<NR, RECON><<<grid, kRedBlock, 0, st>>>(P, lf, w);
+      bi_k1<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
       bi_k2<NR><<<grid, kRedBlock, 0, st>>>(V, w);
-      bi_k3<NR, RECON><<<grid, kRedBlock, 0, st>>>(P, lf, w);
+      bi_k3<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
       bi_k4<NR><<<grid, kRedBlock, 0, st>>>(V, x, w);
       bi_k5<NR><<<grid, kRedBlock, 0, st>>>(V, w);
       note_launch(5);
@@ -499,7 +481,7 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, const double2 *b,
       chunk = std::min(chunk * 2, 16);
       continue;
     }
-    bi_resid<NR, RECON><<<grid, kRedBlock, 0, st>>>(P, lf, b, x, w);
+    bi_resid<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, b, x, w);
     bi_restart<NR><<<grid, kRedBlock, 0, st>>>(V, w);
     note_launch(2);
     MGT_LAUNCH_CHECK("bicgstab residual");

@@ -132,6 +132,51 @@ __host__ __device__ __forceinline__ int64_t native_site(const Geom &g, const int
   return (((int64_t)x[3] * g.L[0] + x[0]) * g.L[1] + x[1]) * g.L[2] + x[2];
 }
 
+// L2-friendly traversal order.  Blocks walk the lattice slab by slab
+// (slabs of w consecutive x0 planes), and inside a slab t-plane by t-plane,
+// so the largest neighbour reuse distance is the slab's t-stride
+// (w*L1*L2 sites, chosen to fit comfortably in L2) instead of the full
+// spatial volume L0*L1*L2.  Ordered index o -> native site.
+struct Sched {
+  int64_t slab_sites;  // w * L1 * L2
+  int64_t plane;       // L0 * L1 * L2 (native t stride)
+  int L3;
+};
+
+inline Sched make_sched(const Geom &g, int64_t bytes_per_site, int64_t budget = (int64_t)24 << 20) {
+  const int64_t row = (int64_t)g.L[1] * g.L[2];
+  int w = 1;
+  for (int d = 1; d <= g.L[0]; ++d)
+    if (g.L[0] % d == 0 && d * row * bytes_per_site <= budget) w = d;
+  Sched s;
+  s.slab_sites = w * row;
+  s.plane = (int64_t)g.L[0] * row;
+  s.L3 = g.L[3];
+  return s;
+}
+
+__host__ __device__ __forceinline__ int64_t sched_site(const Sched &s, int64_t o) {
+  const int64_t q = o / s.slab_sites;
+  const int64_t r = o - q * s.slab_sites;
+  const int64_t t = q % s.L3;
+  const int64_t k = q / s.L3;
+  return t * s.plane + k * s.slab_sites + r;
+}
+
+// Resident-grid size for a kernel (blocks per SM from the occupancy
+// calculator): grid-stride loops then march one contiguous window through the
+// schedule instead of scattering a block's iterations across the lattice.
+template <typename K>
+inline int resident_grid(K kernel, int block, int64_t work_items) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  int64_t need = (work_items + block - 1) / block;
+  int64_t g = (int64_t)kNumSMs * per_sm;
+  if (g > need) g = need;
+  return (int)(g < 1 ? 1 : g);
+}
+
 inline int grid_for(int64_t n, int block, int max_blocks_per_sm = 16) {
   int64_t b = (n + block - 1) / block;
   int64_t cap = (int64_t)kNumSMs * max_blocks_per_sm;

@@ -148,6 +148,7 @@ __device__ __forceinline__ void wilson_hop(const Geom &g, const cplx<R> *__restr
 
 struct WilsonParams {
   Geom g;
+  Sched sched;
   int antiperiodic;
   double diag_up_re, diag_up_im;  // (4 + m0) + i tau   acting on spins 0,1
   double diag_dn_re, diag_dn_im;  // (4 + m0) - i tau   acting on spins 2,3
@@ -169,14 +170,27 @@ __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R>
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int c = 0; c < 3; ++c) acc[a][c] = C<R>(R(0), R(0));
-  wilson_hop<0, true>(P.g, in, links, site, x, g5in, ap, acc);
-  wilson_hop<0, false>(P.g, in, links, site, x, g5in, ap, acc);
-  wilson_hop<1, true>(P.g, in, links, site, x, g5in, ap, acc);
-  wilson_hop<1, false>(P.g, in, links, site, x, g5in, ap, acc);
-  wilson_hop<2, true>(P.g, in, links, site, x, g5in, ap, acc);
-  wilson_hop<2, false>(P.g, in, links, site, x, g5in, ap, acc);
+  // The compiler would otherwise hoist the loads of all 8 hops (168 loads per
+  // thread) and spill; one hop's 21 independent 16-byte loads in flight per
+  // thread is already ~4x the bytes-in-flight HBM needs at this occupancy.
+#define MGT_HOP_FENCE asm volatile("" ::: "memory")
   wilson_hop<3, true>(P.g, in, links, site, x, g5in, ap, acc);
+  MGT_HOP_FENCE;
   wilson_hop<3, false>(P.g, in, links, site, x, g5in, ap, acc);
+  MGT_HOP_FENCE;
+  wilson_hop<0, true>(P.g, in, links, site, x, g5in, ap, acc);
+  MGT_HOP_FENCE;
+  wilson_hop<0, false>(P.g, in, links, site, x, g5in, ap, acc);
+  MGT_HOP_FENCE;
+  wilson_hop<1, true>(P.g, in, links, site, x, g5in, ap, acc);
+  MGT_HOP_FENCE;
+  wilson_hop<1, false>(P.g, in, links, site, x, g5in, ap, acc);
+  MGT_HOP_FENCE;
+  wilson_hop<2, true>(P.g, in, links, site, x, g5in, ap, acc);
+  MGT_HOP_FENCE;
+  wilson_hop<2, false>(P.g, in, links, site, x, g5in, ap, acc);
+  MGT_HOP_FENCE;
+#undef MGT_HOP_FENCE
   const C<R> dup((R)P.diag_up_re, (R)P.diag_up_im);
   const C<R> ddn((R)P.diag_dn_re, (R)P.diag_dn_im);
   const R half = R(0.5);
@@ -196,6 +210,74 @@ __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R>
       }
     }
   }
+}
+
+// Two threads per site: lane parity h = 0 applies the t and x0 hops, h = 1 the
+// x1 and x2 hops; the partial sums are exchanged with one shuffle round and
+// thread h finalises spins 2h, 2h+1 (comps 6h .. 6h+5).  Halves the serial
+// hop chain per thread and doubles the loads in flight per site.
+// y6/xc6: this thread's 6 output comps and raw input comps.
+template <typename R, int RECON>
+__device__ __forceinline__ void wilson_eval_split2(const WilsonParams &P, const cplx<R> *__restrict__ in,
+                                                   const LinkField<R, RECON> &links, int64_t site, int h,
+                                                   C<R> (&y6)[2][3], C<R> (&xc6)[2][3]) {
+  int x[4];
+  native_coords(P.g, site, x);
+  const R g5in = (R)P.g5in;
+  const bool ap = P.antiperiodic != 0;
+  C<R> acc[4][3];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[a][c] = C<R>(R(0), R(0));
+#define MGT_HOP_FENCE asm volatile("" ::: "memory")
+  if (h == 0) {
+    wilson_hop<3, true>(P.g, in, links, site, x, g5in, ap, acc);
+    MGT_HOP_FENCE;
+    wilson_hop<3, false>(P.g, in, links, site, x, g5in, ap, acc);
+    MGT_HOP_FENCE;
+    wilson_hop<0, true>(P.g, in, links, site, x, g5in, ap, acc);
+    MGT_HOP_FENCE;
+    wilson_hop<0, false>(P.g, in, links, site, x, g5in, ap, acc);
+  } else {
+    wilson_hop<1, true>(P.g, in, links, site, x, g5in, ap, acc);
+    MGT_HOP_FENCE;
+    wilson_hop<1, false>(P.g, in, links, site, x, g5in, ap, acc);
+    MGT_HOP_FENCE;
+    wilson_hop<2, true>(P.g, in, links, site, x, g5in, ap, acc);
+    MGT_HOP_FENCE;
+    wilson_hop<2, false>(P.g, in, links, site, x, g5in, ap, acc);
+  }
+#undef MGT_HOP_FENCE
+  // exchange: h = 0 keeps spins 0,1 and ships 2,3; h = 1 the reverse
+  C<R> mine[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      C<R> send = h ? acc[a][c] : acc[2 + a][c];
+      C<R> keep = h ? acc[2 + a][c] : acc[a][c];
+      C<R> got;
+      got.re = __shfl_xor_sync(0xffffffffu, send.re, 1);
+      got.im = __shfl_xor_sync(0xffffffffu, send.im, 1);
+      mine[a][c] = keep + got;
+    }
+  const C<R> dup((R)P.diag_up_re, (R)P.diag_up_im);
+  const C<R> ddn((R)P.diag_dn_re, (R)P.diag_dn_im);
+  const R half = R(0.5);
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      C<R> v = ldc(in + ((2 * h + a) * 3 + c) * P.g.V + site);
+      xc6[a][c] = v;
+      if (h) {
+        C<R> r = ddn * (g5in * v) - half * mine[a][c];
+        y6[a][c] = (R)P.g5out * r;
+      } else {
+        y6[a][c] = dup * v - half * mine[a][c];
+      }
+    }
 }
 
 }  // namespace mgt

@@ -14,6 +14,8 @@ struct mgt_wilson_s {
   double mass;
   int prec;   // 64 or 32
   int recon;  // 18 or 12
+  int variant;         // dslash kernel variant (0: thread/site, 1: 2 threads/site)
+  int64_t slab_bytes;  // L2 budget of one slab t-plane (schedule)
   void *links;  // native link storage (owned)
   size_t link_bytes;
   // pinned host mailbox for solver convergence flags
@@ -25,6 +27,7 @@ namespace mgt {
 inline WilsonParams make_params(const mgt_wilson_s *h, int flags, double tau) {
   WilsonParams P;
   P.g = h->g;
+  P.sched = make_sched(h->g, h->prec == 64 ? 1024 : 512, h->slab_bytes);
   P.antiperiodic = h->antiperiodic;
   double g5in = 1.0, g5out = 1.0, t = tau;
   if (flags & MGT_G5_IN) g5in = -g5in;

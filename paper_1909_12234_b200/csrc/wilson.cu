@@ -1,5 +1,7 @@
 // Wilson-Dirac operator handle and the plain apply kernel (C ABI).
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -53,7 +55,7 @@ __global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4)) wilson_apply_ke
   const int64_t n = P.g.V * NR;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t site = idx / NR;
+    const int64_t site = sched_site(P.sched, idx / NR);
     const int rhs = (int)(idx % NR);
     const cplx<R> *inr = in + (int64_t)rhs * 12 * P.g.V;
     cplx<R> *outr = out + (int64_t)rhs * 12 * P.g.V;
@@ -66,11 +68,47 @@ __global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4)) wilson_apply_ke
   }
 }
 
+// split variant: two threads per site (single rhs)
+template <typename R, int RECON>
+__global__ void __launch_bounds__(128, 3) wilson_apply_split2_kernel(WilsonParams P, const cplx<R> *__restrict__ in,
+                                                                    cplx<R> *__restrict__ out,
+                                                                    LinkField<R, RECON> links) {
+  const int64_t n = P.g.V * 2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t site = sched_site(P.sched, idx >> 1);
+    const int h = (int)(idx & 1);
+    C<R> y[2][3], xc[2][3];
+    wilson_eval_split2<R, RECON>(P, in, links, site, h, y, xc);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) stc_cs(out + ((2 * h + a) * 3 + c) * P.g.V + site, y[a][c]);
+  }
+}
+
+template <typename R, int RECON>
+static int launch_split2(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, cudaStream_t st) {
+  LinkField<R, RECON> lf{reinterpret_cast<const cplx<R> *>(h->links), h->g.V};
+  const int block = 128;
+  static int grid_cache = 0;
+  if (!grid_cache) grid_cache = resident_grid(wilson_apply_split2_kernel<R, RECON>, block, (int64_t)1 << 40);
+  int64_t need = (h->g.V * 2 + block - 1) / block;
+  const int grid = (int)std::min<int64_t>(grid_cache, need);
+  wilson_apply_split2_kernel<R, RECON><<<grid, block, 0, st>>>(P, reinterpret_cast<const cplx<R> *>(x),
+                                                               reinterpret_cast<cplx<R> *>(y), lf);
+  MGT_LAUNCH_CHECK("wilson_apply_split2_kernel");
+  return MGT_OK;
+}
+
 template <typename R, int RECON, int NR>
 static int launch_apply(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, cudaStream_t st) {
   LinkField<R, RECON> lf{reinterpret_cast<const cplx<R> *>(h->links), h->g.V};
   const int block = 128;
-  const int grid = grid_for(h->g.V * NR, block, 64);
+  static int grid_cache = 0;  // per template instance; V-independent part
+  if (!grid_cache) grid_cache = resident_grid(wilson_apply_kernel<R, RECON, NR>, block, (int64_t)1 << 40);
+  int64_t need = (h->g.V * NR + block - 1) / block;
+  const int grid = (int)std::min<int64_t>(grid_cache, need);
   wilson_apply_kernel<R, RECON, NR><<<grid, block, 0, st>>>(P, reinterpret_cast<const cplx<R> *>(x),
                                                              reinterpret_cast<cplx<R> *>(y), lf);
   MGT_LAUNCH_CHECK("wilson_apply_kernel");
@@ -93,7 +131,10 @@ static int apply_groups(const mgt_wilson_s *h, const WilsonParams &P, const void
       rc = launch_apply<R, RECON, 2>(h, P, xb + r * field, yb + r * field, st);
       r += 2;
     } else {
-      rc = launch_apply<R, RECON, 1>(h, P, xb + r * field, yb + r * field, st);
+      if (h->variant == 1)
+        rc = launch_split2<R, RECON>(h, P, xb + r * field, yb + r * field, st);
+      else
+        rc = launch_apply<R, RECON, 1>(h, P, xb + r * field, yb + r * field, st);
       r += 1;
     }
     if (rc) return rc;
@@ -137,6 +178,10 @@ int mgt_wilson_create(mgt_wilson_t *out, const int dims[4], int antiperiodic, do
   h->mass = mass;
   h->prec = prec;
   h->recon = recon;
+  h->variant = 0;
+  if (const char *v = getenv("MGT_DSLASH_VARIANT")) h->variant = atoi(v);
+  h->slab_bytes = (int64_t)32 << 20;
+  if (const char *v = getenv("MGT_SLAB_MB")) h->slab_bytes = (int64_t)atoi(v) << 20;
   const size_t csz = prec == 64 ? sizeof(double2) : sizeof(float2);
   h->link_bytes = (size_t)4 * (recon / 2) * g.V * csz;
   cudaError_t e = cudaMalloc(&h->links, h->link_bytes);

@@ -131,7 +131,7 @@ def test_dimension_mismatch_raises(cuda):
 
 
 def test_dense_guard(cuda):
-    M, geo, gauge, op, links = _setup((4, 4, 4, 4), 0.2)
+    M, geo, gauge, op, links = _setup((4, 4, 8, 8), 0.2)
     with pytest.raises(M.SizeGuardError):
         op.dense()
     M2, geo2, gauge2, op2, links2 = _setup((2, 2, 2, 4), 0.2)
