@@ -135,20 +135,46 @@ int mgt_noise(const int dims[4], int kind, const uint64_t *seeds_host,
 /* ---- prolongator ------------------------------------------------------------ */
 /* Block-orthonormal chirality-split prolongator (multigrid.py:116-225).
  * P storage (native): for aggregate b (native coarse order, t slowest),
- * chirality c, vector k < nv: 1536-entry (for 4^4 blocks) column
- * P[((b*2 + c)*nv + k)*bs + j], j = q*S + s, S = sites per aggregate,
- * q < 6 the spin-colour index within the chirality, s the site within the
- * aggregate (native order).  Coarse vectors: (coarse_site_native, 2*nv)
- * complex128, column order c*nv + k (multigrid.py:189-216). */
+ * chirality c, vector k < nv: bs = 6*S entries (S sites per aggregate)
+ * P[((b*2 + c)*nv + k)*bs + j], j = q*S + s, q < 6 the spin-colour index
+ * within the chirality, s the site within the aggregate (native order).
+ * Coarse vectors: (coarse_site_native, 2*nv) complex128, column order
+ * c*nv + k (multigrid.py:189-216).
+ * mgt_prolong_build replaces build_prolongator (multigrid.py:163-225):
+ * gathers the nv native null-vector fields and runs the per-(block,
+ * chirality) modified Gram-Schmidt twice with the < 1e-8 drop rule;
+ * keep_host (nb*2*nv ints, may be NULL) receives 1 per surviving column.
+ * Errors: MGT_ERR_BLOCKING if a block extent does not divide the lattice
+ * (BlockingScheme.validate, multigrid.py:39-44). */
 int mgt_prolong_build(const int dims[4], const int block[4], int nv,
                       const void *null_native_dev /* nv native fields */,
-                      void *P_dev, int *dropped_out, void *stream);
+                      void *P_dev, int *keep_host, void *stream);
+/* x = P xc (Prolongator.prolong, multigrid.py:156-157) */
 int mgt_prolong(const int dims[4], const int block[4], int nv,
                 const void *P_dev, const void *xc_dev, void *x_native_dev,
                 int n_rhs, void *stream);
+/* xc = P^H x, or P^H (g5 x) = g5_c P^H x if gamma5_in (Prolongator.restrict,
+ * multigrid.py:153-154; trace.py:266) */
 int mgt_restrict(const int dims[4], const int block[4], int nv,
                  const void *P_dev, const void *x_native_dev, void *xc_dev,
                  int n_rhs, int gamma5_in, void *stream);
+/* coarse vectors native <-> reference order (coarse site lexicographic,
+ * last coarse dim fastest; multigrid.py:52-57, :144-147) */
+int mgt_coarse_perm(const int dims[4], const int block[4], int nc, int n_rhs,
+                    const void *in_dev, void *out_dev, int to_ref,
+                    void *stream);
+
+/* ---- coarse operator (multigrid.py:228-259) ------------------------------ */
+/* C = P^H A P as 9 dense (2nv x 2nv) blocks per aggregate, column-major:
+ * C[((b*9 + dir)*nc + col)*nc + row], dir 0 = self, 1 + 2 mu + s the
+ * neighbour in direction mu (s = 0 forward, 1 backward).  Replaces the
+ * SpGEMM of build_coarse_operator (multigrid.py:248). */
+int mgt_coarse_build(mgt_wilson_t h, const int block[4], int nv,
+                     const void *P_dev, void *C_dev, void *stream);
+/* y = C x on native coarse vectors (CoarseOperator.apply) */
+int mgt_coarse_apply(const int dims[4], const int block[4], int nv,
+                     const void *C_dev, const void *xc_dev, void *yc_dev,
+                     int n_rhs, void *stream);
 
 /* ---- deflation projection (trace.py:161-188, :266-267; eigen.py:79-86) --- */
 /* H (k x s, column major, complex128) = V^H X;  V: (k, len) row-major

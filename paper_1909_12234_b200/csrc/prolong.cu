@@ -1,0 +1,318 @@
+// Multigrid prolongator P (block-orthonormal, chirality split) and its
+// adjoint on the GPU (reference: multigrid.py:116-225, Prolongator.restrict /
+// prolong :153-157).
+//
+// Storage ("native P"): aggregate b in native coarse order (t slowest),
+// chirality c (0: gamma5 = +1 -> spins 0,1; 1: spins 2,3), vector k < nv,
+// entry j < bs = 6*S of the (b, c) support:
+//     P[((b*2 + c)*nv + k)*bs + j],   j = q*S + s,
+// q = (spin - 2c)*3 + colour, s = local site in the aggregate (x2 fastest,
+// t slowest).  The reference orders the support rows by global fine index;
+// the MGS result does not depend on the row order (only the reduction
+// order of the dots, i.e. rounding).  Coarse vectors: (b, 2*nv) complex,
+// column c*nv + k (multigrid.py:189-216).
+#include <vector>
+
+#include "reduce.cuh"
+
+namespace mgt {
+
+struct Agg {
+  Geom g;
+  int B[4];       // block extents (reference dims order)
+  int Cd[4];      // coarse extents
+  int S;          // sites per aggregate
+  int bs;         // 6*S entries per (b, c)
+  int nv;
+  int64_t nb;     // number of aggregates
+};
+
+static int make_agg(const int dims[4], const int block[4], int nv, Agg &a) {
+  a.g = make_geom(dims);
+  a.S = 1;
+  a.nb = 1;
+  for (int i = 0; i < 4; ++i) {
+    if (block[i] < 1 || dims[i] % block[i] != 0)
+      return fail(MGT_ERR_BLOCKING, "block extent does not divide lattice extent");
+    a.B[i] = block[i];
+    a.Cd[i] = dims[i] / block[i];
+    a.S *= block[i];
+    a.nb *= a.Cd[i];
+  }
+  if (nv < 1 || nv > 64) return fail(MGT_ERR_INVALID, "nv must be in [1, 64]");
+  a.bs = 6 * a.S;
+  a.nv = nv;
+  return MGT_OK;
+}
+
+// (b, s) -> native fine site
+__device__ __forceinline__ int64_t agg_site(const Agg &a, int64_t b, int s) {
+  int c[4], l[4];
+  int64_t r = b;
+  c[2] = (int)(r % a.Cd[2]);
+  r /= a.Cd[2];
+  c[1] = (int)(r % a.Cd[1]);
+  r /= a.Cd[1];
+  c[0] = (int)(r % a.Cd[0]);
+  c[3] = (int)(r / a.Cd[0]);
+  int q = s;
+  l[2] = q % a.B[2];
+  q /= a.B[2];
+  l[1] = q % a.B[1];
+  q /= a.B[1];
+  l[0] = q % a.B[0];
+  l[3] = q / a.B[0];
+  int x[4];
+  for (int i = 0; i < 4; ++i) x[i] = c[i] * a.B[i] + l[i];
+  return native_site(a.g, x);
+}
+
+// gather nv native null-vector fields into the (unorthogonalised) P layout
+__global__ void prolong_gather_kernel(Agg a, const double2 *__restrict__ nulls, double2 *__restrict__ P) {
+  const int64_t n = a.nb * 2 * a.nv * (int64_t)a.bs;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx % a.bs);
+    int64_t r = idx / a.bs;
+    const int k = (int)(r % a.nv);
+    r /= a.nv;
+    const int c = (int)(r % 2);
+    const int64_t b = r / 2;
+    const int q = j / a.S, s = j % a.S;
+    const int comp = (2 * c + q / 3) * 3 + q % 3;
+    const int64_t site = agg_site(a, b, s);
+    P[idx] = nulls[((int64_t)k * 12 + comp) * a.g.V + site];
+  }
+}
+
+// block-wide sum of (re, im) with a fixed tree; all threads get the result
+__device__ __forceinline__ C<double> block_sum(C<double> v, double *sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    v.re += __shfl_xor_sync(0xffffffffu, v.re, off);
+    v.im += __shfl_xor_sync(0xffffffffu, v.im, off);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    sm[2 * warp] = v.re;
+    sm[2 * warp + 1] = v.im;
+  }
+  __syncthreads();
+  C<double> t(0.0, 0.0);
+  for (int w = 0; w < nw; ++w) {
+    t.re += sm[2 * w];
+    t.im += sm[2 * w + 1];
+  }
+  return t;
+}
+
+// Per-(b, c) modified Gram-Schmidt, two passes, drop < 1e-8 (multigrid.py:195-205).
+// keep[(b*2+c)*nv + k] = 1 if column k survives.
+__global__ void __launch_bounds__(256) prolong_mgs_kernel(Agg a, double2 *__restrict__ P, int *__restrict__ keep) {
+  __shared__ double sm[64];
+  const int64_t grp = blockIdx.x;  // b*2 + c
+  double2 *G = P + grp * a.nv * (int64_t)a.bs;
+  int *kp = keep + grp * a.nv;
+  for (int i = 0; i < a.nv; ++i) {
+    double2 *v = G + (int64_t)i * a.bs;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int u = 0; u < i; ++u) {
+        if (!kp[u]) continue;
+        const double2 *w = G + (int64_t)u * a.bs;
+        C<double> d(0.0, 0.0);
+        for (int j = threadIdx.x; j < a.bs; j += blockDim.x) d = cfma_conj(ldc(w + j), C<double>(v[j].x, v[j].y), d);
+        d = block_sum(d, sm);
+        for (int j = threadIdx.x; j < a.bs; j += blockDim.x) {
+          C<double> x = C<double>(v[j].x, v[j].y) - d * ldc(w + j);
+          v[j] = make_double2(x.re, x.im);
+        }
+        __syncthreads();
+      }
+    }
+    double s2 = 0.0;
+    for (int j = threadIdx.x; j < a.bs; j += blockDim.x) s2 += v[j].x * v[j].x + v[j].y * v[j].y;
+    const double nrm = sqrt(block_sum(C<double>(s2, 0.0), sm).re);
+    const bool ok = nrm >= 1e-8;
+    if (threadIdx.x == 0) kp[i] = ok ? 1 : 0;
+    const double inv = ok ? 1.0 / nrm : 0.0;
+    for (int j = threadIdx.x; j < a.bs; j += blockDim.x) v[j] = make_double2(v[j].x * inv, v[j].y * inv);
+    __syncthreads();
+  }
+}
+
+// x (native fine) = P xc ; one CTA per (b, c, rhs)
+__global__ void __launch_bounds__(256) prolong_kernel(Agg a, const double2 *__restrict__ P,
+                                                     const double2 *__restrict__ xc, double2 *__restrict__ x) {
+  __shared__ double2 sx[64];
+  const int64_t grp = blockIdx.x;
+  const int rhs = blockIdx.y;
+  const int64_t b = grp >> 1;
+  const int c = (int)(grp & 1);
+  const int nc = 2 * a.nv;
+  const double2 *xcr = xc + (int64_t)rhs * a.nb * nc;
+  double2 *xr = x + (int64_t)rhs * 12 * a.g.V;
+  if (threadIdx.x < a.nv) sx[threadIdx.x] = xcr[b * nc + c * a.nv + threadIdx.x];
+  __syncthreads();
+  const double2 *G = P + grp * a.nv * (int64_t)a.bs;
+  for (int j = threadIdx.x; j < a.bs; j += blockDim.x) {
+    C<double> acc(0.0, 0.0);
+    for (int k = 0; k < a.nv; ++k) acc = cfma(ldc(G + (int64_t)k * a.bs + j), C<double>(sx[k].x, sx[k].y), acc);
+    const int q = j / a.S, s = j % a.S;
+    const int comp = (2 * c + q / 3) * 3 + q % 3;
+    xr[(int64_t)comp * a.g.V + agg_site(a, b, s)] = make_double2(acc.re, acc.im);
+  }
+}
+
+// xc = P^H (g5? x) ; one CTA per (b, c, rhs); nv outputs per CTA reduced by
+// warp shuffles then across warps in fixed order.
+template <int NVMAX>
+__global__ void __launch_bounds__(256) restrict_kernel(Agg a, const double2 *__restrict__ P,
+                                                      const double2 *__restrict__ x, double2 *__restrict__ xc,
+                                                      int gamma5_in) {
+  __shared__ double2 part[8][64];
+  const int64_t grp = blockIdx.x;
+  const int rhs = blockIdx.y;
+  const int64_t b = grp >> 1;
+  const int c = (int)(grp & 1);
+  const int nc = 2 * a.nv;
+  const double2 *xr = x + (int64_t)rhs * 12 * a.g.V;
+  const double2 *G = P + grp * a.nv * (int64_t)a.bs;
+  const double sign = (gamma5_in && c == 1) ? -1.0 : 1.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  C<double> acc[NVMAX];
+#pragma unroll
+  for (int k = 0; k < NVMAX; ++k) acc[k] = C<double>(0.0, 0.0);
+  for (int j = threadIdx.x; j < a.bs; j += blockDim.x) {
+    const int q = j / a.S, s = j % a.S;
+    const int comp = (2 * c + q / 3) * 3 + q % 3;
+    C<double> xv = sign * ldc(xr + (int64_t)comp * a.g.V + agg_site(a, b, s));
+#pragma unroll
+    for (int k = 0; k < NVMAX; ++k)
+      if (k < a.nv) acc[k] = cfma_conj(ldc(G + (int64_t)k * a.bs + j), xv, acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < NVMAX; ++k) {
+    if (k >= a.nv) break;
+    C<double> v = acc[k];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      v.re += __shfl_xor_sync(0xffffffffu, v.re, off);
+      v.im += __shfl_xor_sync(0xffffffffu, v.im, off);
+    }
+    if (lane == 0) part[warp][k] = make_double2(v.re, v.im);
+  }
+  __syncthreads();
+  if (threadIdx.x < a.nv) {
+    C<double> t(0.0, 0.0);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = t + C<double>(part[w][threadIdx.x].x, part[w][threadIdx.x].y);
+    xc[(int64_t)rhs * a.nb * nc + b * nc + c * a.nv + threadIdx.x] = make_double2(t.re, t.im);
+  }
+}
+
+// coarse vectors: reference order (b_ref lexicographic, last coarse dim
+// fastest) <-> native order (t slowest)
+__global__ void coarse_perm_kernel(Agg a, int nc, int n_rhs, const double2 *__restrict__ in,
+                                   double2 *__restrict__ out, int to_ref) {
+  const int64_t n = a.nb * nc * (int64_t)n_rhs;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)(idx % nc);
+    int64_t r = idx / nc;
+    const int64_t bn = r % a.nb;
+    const int64_t rhs = r / a.nb;
+    int64_t q = bn;
+    int c[4];
+    c[2] = (int)(q % a.Cd[2]);
+    q /= a.Cd[2];
+    c[1] = (int)(q % a.Cd[1]);
+    q /= a.Cd[1];
+    c[0] = (int)(q % a.Cd[0]);
+    c[3] = (int)(q / a.Cd[0]);
+    const int64_t br = (((int64_t)c[0] * a.Cd[1] + c[1]) * a.Cd[2] + c[2]) * a.Cd[3] + c[3];
+    const int64_t nat = (rhs * a.nb + bn) * nc + col;
+    const int64_t ref = (rhs * a.nb + br) * nc + col;
+    if (to_ref)
+      out[ref] = in[nat];
+    else
+      out[nat] = in[ref];
+  }
+}
+
+}  // namespace mgt
+
+using namespace mgt;
+
+extern "C" {
+
+int mgt_prolong_build(const int dims[4], const int block[4], int nv, const void *null_native_dev, void *P_dev,
+                      int *keep_host, void *stream) {
+  if (!dims || !block || !null_native_dev || !P_dev) return fail(MGT_ERR_INVALID, "mgt_prolong_build: null argument");
+  Agg a;
+  int rc = make_agg(dims, block, nv, a);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = a.nb * 2 * a.nv * (int64_t)a.bs;
+  prolong_gather_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(a, (const double2 *)null_native_dev, (double2 *)P_dev);
+  MGT_LAUNCH_CHECK("prolong_gather_kernel");
+  int *keep = nullptr;
+  const size_t kb = (size_t)a.nb * 2 * nv * sizeof(int);
+  MGT_CUDA(cudaMallocAsync((void **)&keep, kb, st));
+  prolong_mgs_kernel<<<(unsigned)(a.nb * 2), 256, 0, st>>>(a, (double2 *)P_dev, keep);
+  MGT_LAUNCH_CHECK("prolong_mgs_kernel");
+  if (keep_host) MGT_CUDA(cudaMemcpyAsync(keep_host, keep, kb, cudaMemcpyDeviceToHost, st));
+  MGT_CUDA(cudaFreeAsync(keep, st));
+  MGT_CUDA(cudaStreamSynchronize(st));
+  return MGT_OK;
+}
+
+int mgt_prolong(const int dims[4], const int block[4], int nv, const void *P_dev, const void *xc_dev,
+                void *x_native_dev, int n_rhs, void *stream) {
+  if (!dims || !block || !P_dev || !xc_dev || !x_native_dev || n_rhs < 1)
+    return fail(MGT_ERR_INVALID, "mgt_prolong: bad argument");
+  Agg a;
+  int rc = make_agg(dims, block, nv, a);
+  if (rc) return rc;
+  dim3 grid((unsigned)(a.nb * 2), (unsigned)n_rhs);
+  prolong_kernel<<<grid, 256, 0, as_stream(stream)>>>(a, (const double2 *)P_dev, (const double2 *)xc_dev,
+                                                       (double2 *)x_native_dev);
+  MGT_LAUNCH_CHECK("prolong_kernel");
+  return MGT_OK;
+}
+
+int mgt_restrict(const int dims[4], const int block[4], int nv, const void *P_dev, const void *x_native_dev,
+                 void *xc_dev, int n_rhs, int gamma5_in, void *stream) {
+  if (!dims || !block || !P_dev || !xc_dev || !x_native_dev || n_rhs < 1)
+    return fail(MGT_ERR_INVALID, "mgt_restrict: bad argument");
+  Agg a;
+  int rc = make_agg(dims, block, nv, a);
+  if (rc) return rc;
+  dim3 grid((unsigned)(a.nb * 2), (unsigned)n_rhs);
+  cudaStream_t st = as_stream(stream);
+  const double2 *Pp = (const double2 *)P_dev, *xp = (const double2 *)x_native_dev;
+  double2 *cp = (double2 *)xc_dev;
+  if (nv <= 8)
+    restrict_kernel<8><<<grid, 256, 0, st>>>(a, Pp, xp, cp, gamma5_in);
+  else if (nv <= 24)
+    restrict_kernel<24><<<grid, 256, 0, st>>>(a, Pp, xp, cp, gamma5_in);
+  else if (nv <= 32)
+    restrict_kernel<32><<<grid, 256, 0, st>>>(a, Pp, xp, cp, gamma5_in);
+  else
+    restrict_kernel<64><<<grid, 256, 0, st>>>(a, Pp, xp, cp, gamma5_in);
+  MGT_LAUNCH_CHECK("restrict_kernel");
+  return MGT_OK;
+}
+
+int mgt_coarse_perm(const int dims[4], const int block[4], int nc, int n_rhs, const void *in_dev, void *out_dev,
+                    int to_ref, void *stream) {
+  if (!dims || !block || !in_dev || !out_dev || nc < 1 || n_rhs < 1)
+    return fail(MGT_ERR_INVALID, "mgt_coarse_perm: bad argument");
+  Agg a;
+  int rc = make_agg(dims, block, 1, a);
+  if (rc) return rc;
+  const int64_t n = a.nb * nc * (int64_t)n_rhs;
+  coarse_perm_kernel<<<grid_for(n, 256, 8), 256, 0, as_stream(stream)>>>(a, nc, n_rhs, (const double2 *)in_dev,
+                                                                          (double2 *)out_dev, to_ref);
+  MGT_LAUNCH_CHECK("coarse_perm_kernel");
+  return MGT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,457 @@
+"""GPU multigrid setup: null vectors, chirality-split prolongator P / P^H,
+Galerkin coarse operator and its block-stencil matvec.
+
+Mirrors `mgtrace.multigrid` (`/root/reference/pkg/src/mgtrace/multigrid.py`):
+`BlockingError` (`:24`), `BlockingScheme` (`:28-57`), `NullVectors`
+(`:60-71`), `generate_null_vectors` (`:74-113`), `Prolongator`
+(`:116-160`), `build_prolongator` (`:163-225`), `CoarseOperator`
+(`:228-243`), `build_coarse_operator` (`:246-259`).  P, P^H, the MGS
+orthonormalisation and C = P^H A P are sm_100a kernels (`mgt_prolong_build`,
+`mgt_prolong`, `mgt_restrict`, `mgt_coarse_build`, `mgt_coarse_apply`).
+
+Null vectors follow the reference exactly: one `default_rng(seed)` stream,
+`y0 = normal(N) + 1j normal(N)` per vector in reference layout, relaxed by
+restarted GCR(max_iter, restart = max_iter) on A d = -A y0 from a zero start
+(`gcr_relax`, GPU dslash; the GCR scalar recurrences follow krylov.py:52-118,
+the short BLAS-1 on torch device tensors), y = y0 + d, normalised.
+"""
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import device, ptr, stream_ptr
+from .lattice import LatticeGeometry
+
+
+class BlockingError(ValueError):
+    pass
+
+
+@dataclass(frozen=True)
+class BlockingScheme:
+    block_dims: tuple
+
+    def __post_init__(self):
+        object.__setattr__(self, "block_dims", tuple(int(b) for b in self.block_dims))
+        if any(b < 1 for b in self.block_dims):
+            raise BlockingError("block extents must be >= 1")
+
+    def validate(self, geometry):
+        if len(self.block_dims) != geometry.ndim:
+            raise BlockingError("blocking dimensionality mismatch")
+        for L, b in zip(geometry.dims, self.block_dims):
+            if L % b:
+                raise BlockingError(f"block extent {b} does not divide lattice extent {L}")
+
+    def coarse_dims(self, geometry):
+        return tuple(L // b for L, b in zip(geometry.dims, self.block_dims))
+
+    def block_count(self, geometry):
+        return int(np.prod(self.coarse_dims(geometry)))
+
+
+# ---------------------------------------------------------------------------
+# GCR relaxation on the GPU (krylov.py:52-118 semantics)
+
+
+def _vdot(a, b):
+    return torch.vdot(a.reshape(-1), b.reshape(-1))
+
+
+def gcr_relax(op, b, tol, max_iter, restart):
+    """Restarted GCR from x0 = 0 on native fields (1, 12, V); returns
+    (x, iterations, converged, reason, matvecs)."""
+    bn = torch.linalg.vector_norm(b).item()
+    if bn == 0.0:
+        return torch.zeros_like(b), 0, True, "", 0
+    x = torch.zeros_like(b)
+    r = b.clone()
+    nmv = 0
+    Z, Q = [], []
+    it = 0
+    rel = 1.0
+    why = "max_iter"
+    while it < max_iter:
+        if rel <= tol:
+            r = b - op.apply_native(x)
+            nmv += 1
+            rel = torch.linalg.vector_norm(r).item() / bn
+            if rel <= tol:
+                return x, it, True, "", nmv
+            Z, Q = [], []
+        z = r.clone()
+        q = op.apply_native(z)
+        nmv += 1
+        q0 = torch.linalg.vector_norm(q).item()
+        for zj, qj in zip(Z, Q):
+            c = _vdot(qj, q)
+            q = q - c * qj
+            z = z - c * zj
+        qn = torch.linalg.vector_norm(q).item()
+        if qn <= 1e-14 * max(q0, 1e-300):
+            why = "breakdown"
+            break
+        q = q / qn
+        z = z / qn
+        a = _vdot(q, r)
+        x = x + a * z
+        r = r - a * q
+        Z.append(z)
+        Q.append(q)
+        it += 1
+        rel = torch.linalg.vector_norm(r).item() / bn
+        if len(Z) >= restart:
+            Z, Q = [], []
+            r = b - op.apply_native(x)
+            nmv += 1
+            rel = torch.linalg.vector_norm(r).item() / bn
+    r = b - op.apply_native(x)
+    nmv += 1
+    rel = torch.linalg.vector_norm(r).item() / bn
+    if rel <= tol:
+        return x, it, True, "", nmv
+    return x, it, False, why, nmv
+
+
+@dataclass
+class NullVectors:
+    vectors: torch.Tensor  # (n, 12, V) native layout
+    residual_ratios: np.ndarray
+    seed: int
+    geometry: LatticeGeometry
+    dof: int
+    gamma5_diag: np.ndarray
+    degenerate: np.ndarray = None
+
+    def ref_vectors(self, op):
+        """(n, N) reference-layout numpy copy."""
+        return op.from_native(self.vectors).cpu().numpy()
+
+
+def generate_null_vectors(op, n, tol=1e-2, max_iter=200, seed=0):
+    """Reference generate_null_vectors (multigrid.py:74-113) on the GPU."""
+    if n < 1:
+        raise ValueError("need n >= 1 null vectors")
+    rng = np.random.default_rng(seed)
+    N = op.dim
+    vecs = op.new_field(n)
+    ratios = np.empty(n)
+    degenerate = np.zeros(n, dtype=bool)
+    for i in range(n):
+        for attempt in range(3):
+            y0h = rng.normal(size=N) + 1j * rng.normal(size=N)
+            y0 = op.to_native(torch.from_numpy(y0h).to(device()))
+            b = -op.apply_native(y0)
+            d, its, conv, why, _ = gcr_relax(op, b, tol, max_iter, max_iter)
+            y = y0 + d
+            if conv or why != "breakdown":
+                break
+        else:
+            raise RuntimeError(f"null-vector solve kept breaking down (vector {i})")
+        yn = torch.linalg.vector_norm(y).item()
+        y0n = torch.linalg.vector_norm(y0).item()
+        if yn < 1e-8 * y0n:
+            degenerate[i] = True
+            d1, *_ = gcr_relax(op, b, tol, 1, 1)
+            y = y0 + d1
+            yn = torch.linalg.vector_norm(y).item()
+            if yn < 1e-8 * y0n:
+                y, yn = y0, y0n
+        ratios[i] = torch.linalg.vector_norm(op.apply_native(y)).item() / max(
+            torch.linalg.vector_norm(b).item(), 1e-300)
+        vecs[i] = (y / yn)[0]
+    return NullVectors(vecs, ratios, seed, op.geometry, op.dof, op.gamma5_diag, degenerate)
+
+
+def null_vectors_from_array(op, vectors_ref, seed=0):
+    """Wrap host reference-layout vectors (n, N) (e.g. the reference's own
+    output) as NullVectors on the device."""
+    v = torch.as_tensor(np.ascontiguousarray(vectors_ref, dtype=np.complex128)).to(device())
+    return NullVectors(op.to_native(v), np.zeros(len(vectors_ref)), seed, op.geometry, op.dof,
+                       op.gamma5_diag, np.zeros(len(vectors_ref), dtype=bool))
+
+
+# ---------------------------------------------------------------------------
+
+
+class Prolongator:
+    """Block-orthonormal chirality-preserving basis V on the device
+    (multigrid.py:116-160).  Coarse vectors use the reference order at the
+    `restrict` / `prolong` interface and the native order (t slowest) in the
+    `*_native` methods."""
+
+    def __init__(self, P, geometry, blocking, nv, fine_dof, keep):
+        self.P = P
+        self.geometry = geometry
+        self.blocking = blocking
+        self.nv = nv
+        self.fine_dof = fine_dof
+        m = blocking.block_count(geometry)
+        keep = keep.reshape(m, 2, nv)
+        self.per_block_counts = keep.sum(axis=2)
+        self.dropped = int(keep.size - keep.sum())
+        self.coarse_gamma5 = np.tile(np.concatenate([np.ones(nv), -np.ones(nv)]), m)
+
+    @property
+    def uniform(self):
+        return bool(np.all(self.per_block_counts == self.per_block_counts[0, 0]))
+
+    @property
+    def n_blocks(self):
+        return self.blocking.block_count(self.geometry)
+
+    @property
+    def nc(self):
+        return 2 * self.nv
+
+    @property
+    def fine_dim(self):
+        return self.geometry.site_count * self.fine_dof
+
+    @property
+    def coarse_dim(self):
+        return self.n_blocks * self.nc
+
+    @property
+    def coarse_geometry(self):
+        return LatticeGeometry(self.blocking.coarse_dims(self.geometry), self.geometry.boundary)
+
+    def _dims(self):
+        return _lib.dims_arg(self.geometry.dims), _lib.dims_arg(self.blocking.block_dims)
+
+    def new_coarse(self, n=1):
+        return torch.zeros((n, self.n_blocks, self.nc), dtype=torch.complex128, device=device())
+
+    def coarse_to_ref(self, xc):
+        out = torch.empty_like(xc)
+        d, b = self._dims()
+        _lib.check(_lib.lib().mgt_coarse_perm(d, b, self.nc, xc.shape[0], ptr(xc), ptr(out), 1, stream_ptr()))
+        return out
+
+    def coarse_from_ref(self, xc):
+        out = torch.empty_like(xc)
+        d, b = self._dims()
+        _lib.check(_lib.lib().mgt_coarse_perm(d, b, self.nc, xc.shape[0], ptr(xc), ptr(out), 0, stream_ptr()))
+        return out
+
+    def restrict_native(self, x, gamma5_in=False, out=None):
+        """P^H x (or P^H gamma5 x) for native fine fields (n, 12, V) ->
+        native coarse (n, nb, 2nv)."""
+        x = x.contiguous()
+        out = self.new_coarse(x.shape[0]) if out is None else out
+        d, b = self._dims()
+        _lib.check(_lib.lib().mgt_restrict(d, b, self.nv, ptr(self.P), ptr(x), ptr(out), x.shape[0],
+                                            1 if gamma5_in else 0, stream_ptr()), "restrict")
+        return out
+
+    def prolong_native(self, xc, out=None):
+        xc = xc.contiguous()
+        n = xc.shape[0]
+        out = torch.empty((n, 12, self.geometry.site_count), dtype=torch.complex128,
+                          device=device()) if out is None else out
+        d, b = self._dims()
+        _lib.check(_lib.lib().mgt_prolong(d, b, self.nv, ptr(self.P), ptr(xc), ptr(out), n, stream_ptr()),
+                   "prolong")
+        return out
+
+    # reference-layout interface (multigrid.py:153-157)
+    def restrict(self, x):
+        host = not isinstance(x, torch.Tensor)
+        xd = torch.as_tensor(np.asarray(x, dtype=np.complex128)).to(device()) if host else x
+        nat = self._layout.to_native(xd.reshape(1, -1))
+        xc = self.coarse_to_ref(self.restrict_native(nat)).reshape(-1)
+        return xc.cpu().numpy() if host else xc
+
+    def prolong(self, xc):
+        host = not isinstance(xc, torch.Tensor)
+        xd = torch.as_tensor(np.asarray(xc, dtype=np.complex128)).to(device()) if host else xc
+        nat = self.coarse_from_ref(xd.reshape(1, self.n_blocks, self.nc))
+        y = self._layout.from_native(self.prolong_native(nat)).reshape(-1)
+        return y.cpu().numpy() if host else y
+
+    def dense(self):
+        """Dense N x Nc in reference order (oracle-scale interop only)."""
+        eye = torch.eye(self.coarse_dim, dtype=torch.complex128, device=device())
+        nat = self.coarse_from_ref(eye.reshape(self.coarse_dim, self.n_blocks, self.nc))
+        cols = self._layout.from_native(self.prolong_native(nat))
+        return cols.T.cpu().numpy()
+
+
+def build_prolongator(null_vectors, blocking, layout_op=None):
+    """Reference build_prolongator (multigrid.py:163-225) on the GPU."""
+    geo = null_vectors.geometry
+    blocking.validate(geo)
+    nv = null_vectors.vectors.shape[0]
+    m = blocking.block_count(geo)
+    S = int(np.prod(blocking.block_dims))
+    P = torch.empty(m * 2 * nv * 6 * S, dtype=torch.complex128, device=device())
+    keep = np.zeros(m * 2 * nv, dtype=np.int32)
+    _lib.check(_lib.lib().mgt_prolong_build(
+        _lib.dims_arg(geo.dims), _lib.dims_arg(blocking.block_dims), nv, ptr(null_vectors.vectors.contiguous()),
+        ptr(P), keep.ctypes.data_as(_lib.c_int_p), stream_ptr()), "build_prolongator")
+    pro = Prolongator(P, geo, blocking, nv, null_vectors.dof, keep)
+    pro._layout = layout_op if layout_op is not None else _LayoutOnly(geo)
+    if pro.dropped:
+        warnings.warn(f"dropped {pro.dropped} rank-deficient prolongator columns")
+        for b, c in np.argwhere(pro.per_block_counts == 0):
+            raise BlockingError(f"block {b} chirality {'+-'[c]} lost all columns: blocking too fine")
+    return pro
+
+
+class _LayoutOnly:
+    """Layout conversions for a geometry without an operator handle."""
+
+    def __init__(self, geo):
+        self.geometry = geo
+        self.prec = 64
+
+    def to_native(self, x_ref):
+        n = x_ref.shape[0]
+        out = torch.empty((n, 12, self.geometry.site_count), dtype=torch.complex128, device=device())
+        _lib.check(_lib.lib().mgt_spinor_from_ref(_lib.dims_arg(self.geometry.dims), 64, ptr(x_ref.contiguous()),
+                                                   ptr(out), n, stream_ptr()))
+        return out
+
+    def from_native(self, x):
+        n = x.shape[0]
+        out = torch.empty((n, 12 * self.geometry.site_count), dtype=torch.complex128, device=device())
+        _lib.check(_lib.lib().mgt_spinor_to_ref(_lib.dims_arg(self.geometry.dims), 64, ptr(x.contiguous()),
+                                                 ptr(out), n, stream_ptr()))
+        return out
+
+
+# ---------------------------------------------------------------------------
+
+
+class CoarseOperator:
+    """Galerkin V^H A V as 9 dense blocks per aggregate (multigrid.py:228-243)."""
+
+    def __init__(self, C, prolongator, level=1):
+        if not prolongator.uniform:
+            raise BlockingError("coarse operator needs uniform per-block column counts "
+                                "(rank-deficient blocks were dropped)")
+        self.C = C
+        self.prolongator = prolongator
+        self.level = level
+        self.geometry = prolongator.coarse_geometry
+        self.dof = prolongator.nc
+        self.gamma5_diag = prolongator.coarse_gamma5
+
+    @property
+    def dim(self):
+        return self.prolongator.coarse_dim
+
+    @property
+    def shape(self):
+        return (self.dim, self.dim)
+
+    def apply_native(self, xc, out=None):
+        pr = self.prolongator
+        xc = xc.contiguous()
+        out = torch.empty_like(xc) if out is None else out
+        d, b = pr._dims()
+        _lib.check(_lib.lib().mgt_coarse_apply(d, b, pr.nv, ptr(self.C), ptr(xc), ptr(out), xc.shape[0],
+                                                stream_ptr()), "coarse apply")
+        return out
+
+    def apply(self, x):
+        pr = self.prolongator
+        host = not isinstance(x, torch.Tensor)
+        xd = torch.as_tensor(np.asarray(x, dtype=np.complex128)).to(device()) if host else x
+        if xd.shape[0] != self.dim:
+            raise ValueError(f"dimension mismatch: {xd.shape[0]} != {self.dim}")
+        nat = pr.coarse_from_ref(xd.reshape(1, pr.n_blocks, pr.nc))
+        y = pr.coarse_to_ref(self.apply_native(nat)).reshape(-1)
+        return y.cpu().numpy() if host else y
+
+    def dense_native(self):
+        """Dense Nc x Nc on the device, NATIVE coarse order (blocks of aliased
+        neighbours summed)."""
+        pr = self.prolongator
+        nb, nc = pr.n_blocks, pr.nc
+        nbr = torch.as_tensor(coarse_neighbours(pr.blocking.coarse_dims(pr.geometry)), device=device())
+        blocks = self.C.reshape(nb, 9, nc, nc).transpose(-1, -2)  # -> [b][dir][row][col]
+        D = torch.zeros((nb, nc, nb, nc), dtype=torch.complex128, device=device())
+        rows = torch.arange(nb, device=device())
+        for d in range(9):  # rows are distinct within one direction: no write conflicts
+            D[rows, :, nbr[:, d], :] = D[rows, :, nbr[:, d], :] + blocks[:, d]
+        return D.reshape(nb * nc, nb * nc)
+
+    def dense(self):
+        """Dense matrix in the reference coarse order (host numpy)."""
+        pr = self.prolongator
+        Dn = self.dense_native()
+        perm = torch.as_tensor(native_to_ref_coarse(pr.blocking.coarse_dims(pr.geometry)), device=device())
+        nc = pr.nc
+        idx = (perm[:, None] * nc + torch.arange(nc, device=device())[None, :]).reshape(-1)
+        Dr = torch.empty_like(Dn)
+        Dr[idx[:, None], idx[None, :]] = Dn
+        return Dr.cpu().numpy()
+
+
+def coarse_neighbours(cdims):
+    """(nb, 9) native neighbour table: dir 0 self, 1 + 2 mu + s."""
+    C0, C1, C2, C3 = cdims
+    nb = C0 * C1 * C2 * C3
+    b = np.arange(nb)
+    c2 = b % C2
+    c1 = (b // C2) % C1
+    c0 = (b // (C2 * C1)) % C0
+    c3 = b // (C2 * C1 * C0)
+    coords = [c0, c1, c2, c3]
+    out = np.empty((nb, 9), dtype=np.int64)
+    out[:, 0] = b
+    for mu in range(4):
+        for s, sgn in enumerate((1, -1)):
+            cc = [c.copy() for c in coords]
+            cc[mu] = (cc[mu] + sgn) % cdims[mu]
+            out[:, 1 + 2 * mu + s] = ((cc[3] * C0 + cc[0]) * C1 + cc[1]) * C2 + cc[2]
+    return out
+
+
+def native_to_ref_coarse(cdims):
+    C0, C1, C2, C3 = cdims
+    nb = C0 * C1 * C2 * C3
+    b = np.arange(nb)
+    c2 = b % C2
+    c1 = (b // C2) % C1
+    c0 = (b // (C2 * C1)) % C0
+    c3 = b // (C2 * C1 * C0)
+    return ((c0 * C1 + c1) * C2 + c2) * C3 + c3
+
+
+def build_coarse_operator(op, prolongator, level=1, check=True):
+    """Reference build_coarse_operator (multigrid.py:246-259): C = P^H A P on
+    the GPU, with the inherited gamma5_c-Hermiticity check to 1e-12."""
+    pr = prolongator
+    nb, nc = pr.n_blocks, pr.nc
+    C = torch.empty(nb * 9 * nc * nc, dtype=torch.complex128, device=device())
+    _lib.check(_lib.lib().mgt_coarse_build(op.handle, _lib.dims_arg(pr.blocking.block_dims), pr.nv, ptr(pr.P),
+                                            ptr(C), stream_ptr()), "build_coarse_operator")
+    coarse = CoarseOperator(C, pr, level=level)
+    if check:
+        _check_gamma5_hermitian(coarse)
+    return coarse
+
+
+def _check_gamma5_hermitian(coarse):
+    """g5c C g5c = C^H blockwise: block (b, dir) vs (nbr, opposite)^H."""
+    pr = coarse.prolongator
+    nb, nc = pr.n_blocks, pr.nc
+    nbr = torch.as_tensor(coarse_neighbours(pr.blocking.coarse_dims(pr.geometry)), device=device())
+    B = coarse.C.reshape(nb, 9, nc, nc).transpose(-1, -2)  # [b][dir][row][col]
+    g = torch.as_tensor(np.concatenate([np.ones(pr.nv), -np.ones(pr.nv)]), device=device(),
+                        dtype=torch.complex128)
+    opp = [0, 2, 1, 4, 3, 6, 5, 8, 7]
+    scale = B.abs().max().item()
+    worst = 0.0
+    for d in range(9):
+        lhs = g[:, None] * B[:, d] * g[None, :]
+        rhs = B[nbr[:, d], opp[d]].conj().transpose(-1, -2)
+        worst = max(worst, (lhs - rhs).abs().max().item())
+    if worst > 1e-12 * max(scale, 1e-300):
+        raise ValueError(f"coarse operator lost gamma5-Hermiticity: {worst:.3e}")

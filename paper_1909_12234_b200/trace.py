@@ -131,6 +131,115 @@ def _group_samples_generic(apply_fn, probes, health=None):
     return samples, flagged
 
 
+@dataclass
+class ObliqueFactors:
+    """Small factors of the coarse oblique deflation (trace.py:191-204)."""
+
+    rank: int
+    lam: np.ndarray
+    uhat: np.ndarray
+    s_small: np.ndarray
+    t_small: np.ndarray
+    t0: complex
+
+    def minv(self):
+        return self.uhat @ np.diag(1.0 / self.lam) @ self.uhat.conj().T
+
+
+def factorize_small(s_small, t_small):
+    """trace.py:207-217: eigh of the Hermitian part, |lambda| ascending,
+    spurious-mode guard, t0 = tr(Uhat^H T Uhat Lam^-1)."""
+    k = s_small.shape[0]
+    lam, uhat = np.linalg.eigh(0.5 * (s_small + s_small.conj().T))
+    order = np.argsort(np.abs(lam), kind="stable")
+    lam, uhat = lam[order], uhat[:, order]
+    lam_max = np.abs(lam).max() if k else 0.0
+    for i, l in enumerate(lam):
+        if abs(l) < 1e-12 * lam_max:
+            raise SpuriousModeError(i, l, lam_max)
+    t0 = complex(np.trace(uhat.conj().T @ t_small @ uhat @ np.diag(1.0 / lam))) if k else 0j
+    return lam, uhat, t0
+
+
+class IdentityTriplets:
+    """Full coarse space: Ubar = I (rank = Nc), i.e. deflation with V = P
+    (SURVEY.md finding 8)."""
+
+    def __init__(self, n):
+        self.count = n
+
+
+def _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op):
+    """rank = Nc, Ubar = I: t0 = tr(C^-1); per slot
+    z^H A^-1 z - (P^H z)^H C^-1 (P^H z)  (Y = A^-1 (A P) = P)."""
+    import torch
+    from .multigrid import build_coarse_operator
+    coarse = coarse_op if coarse_op is not None else build_coarse_operator(op, prolongator)
+    D = coarse.dense_native()
+    Dinv = torch.linalg.inv(D)  # dense fp64 LU on the device (setup; Nc x Nc)
+    del D
+    t0 = complex(torch.diagonal(Dinv).sum().item())
+    Nc = prolongator.coarse_dim
+
+    def correction(j0, z, x):
+        h = prolongator.restrict_native(z).reshape(z.shape[0], Nc)
+        ch = h @ Dinv.transpose(0, 1)  # rows: (C^-1 h_j)^T
+        return torch.sum(h.conj() * ch, dim=1).cpu().numpy()
+
+    return t0, correction
+
+
+def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probes, coarse_op=None):
+    """Algorithm-2 trace estimate (trace.py:236-274) on the GPU.
+
+    rank = Nc with identity triplets (`IdentityTriplets`, or None) is the
+    full-prolongator deflation of BASELINE configs 3/5; otherwise the
+    reference's rank-r decoupled form with Y = A^-1_xi (A W Ubar) solved
+    once (r fine solves)."""
+    import torch
+    before = getattr(inv_op, "n_solves", 0)
+    if rank == 0:
+        samples, flagged = group_samples_gpu(inv_op, probes)
+        _warn_flagged(flagged)
+        return finish(0.0, samples, inv_op.n_solves - before, flagged)
+    if coarse_triplets is None or isinstance(coarse_triplets, IdentityTriplets):
+        if rank != prolongator.coarse_dim:
+            raise ValueError("identity coarse triplets need rank = Nc")
+        t0, corr = _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op)
+        samples, flagged = group_samples_gpu(inv_op, probes, correction=corr)
+        _warn_flagged(flagged)
+        return finish(t0, samples, inv_op.n_solves - before, flagged)
+    if rank > coarse_triplets.count:
+        raise ValueError(f"rank {rank} exceeds the {coarse_triplets.count} available triplets")
+    # rank-r form (trace.py:220-233, :251-271)
+    pr = prolongator
+    dev = pr.P.device
+    ubar = np.asarray(coarse_triplets.left)[:, :rank]
+    ub = torch.as_tensor(np.ascontiguousarray(ubar.T), device=dev)  # (r, Nc) reference coarse order
+    ubn = pr.coarse_from_ref(ub.reshape(rank, pr.n_blocks, pr.nc))
+    wu = pr.prolong_native(ubn)  # W Ubar, (r, 12, V)
+    g_cols = op.apply_native(wu)  # A W Ubar
+    g5 = torch.ones(12, device=dev, dtype=torch.float64)
+    g5[6:] = -1.0
+    s_small = torch.einsum("ics,jcs->ij", wu.conj(), g5[None, :, None] * g_cols).cpu().numpy()
+    g5c = pr.coarse_gamma5
+    t_small = ubar.conj().T @ (g5c[:, None] * ubar)
+    lam, uhat, t0 = factorize_small(s_small, t_small)
+    minv = torch.as_tensor(uhat @ np.diag(1.0 / lam) @ uhat.conj().T, device=dev)
+    Y, _, _ = inv_op.solve_native(g_cols)
+    ubn_flat = ubn.reshape(rank, -1)
+
+    def correction(j0, z, x):
+        n = z.shape[0]
+        g = pr.restrict_native(z, gamma5_in=True).reshape(n, -1) @ ubn_flat.conj().T  # (n, r)
+        h = z.reshape(n, -1) @ Y.reshape(rank, -1).conj().T  # (n, r) = Y^H z
+        return torch.sum(h.conj() * (g @ minv.T), dim=1).cpu().numpy()
+
+    samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
+    _warn_flagged(flagged)
+    return finish(t0, samples, inv_op.n_solves - before, flagged)
+
+
 def hutchinson(inv_op, probes):
     """Stochastic trace estimate of the operator behind inv_op
     (trace.py:122-132)."""

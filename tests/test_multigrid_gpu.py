@@ -1,0 +1,123 @@
+"""GPU multigrid setup and Algorithm-2 deflation against the reference's
+golden fixtures (tests/golden/golden_4x4x4x4.npz) and the oracle
+restatements (oracle/multigrid.py).  Tolerance (BASELINE north star):
+P / P^H to 1e-12 relative; trace estimate within xi + 1e-10."""
+
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+from oracle import multigrid as OMG
+from oracle import pcg64 as P
+from oracle import wilson4d as W
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "golden_4x4x4x4.npz")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return dict(np.load(GOLD))
+
+
+@pytest.fixture(scope="module")
+def setup(gold):
+    import paper_1909_12234_b200 as M
+    from paper_1909_12234_b200 import multigrid as MG
+    dims = tuple(int(d) for d in gold["dims"])
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    gauge = M.gauge_from_array(geo, gold["links"])
+    op = M.build_wilson(gauge, float(gold["mass"]))
+    A = W.build_wilson4d_csr(gold["links"], dims, float(gold["mass"]))
+    Pg = sp.coo_matrix((gold["P_val"], (gold["P_row"], gold["P_col"])), shape=tuple(gold["P_shape"])).tocsr()
+    return M, MG, geo, op, A, Pg
+
+
+def test_golden_operator(gold, setup):
+    M, MG, geo, op, A, Pg = setup
+    assert np.linalg.norm(op.apply(gold["x"]) - gold["Ax"]) / np.linalg.norm(gold["Ax"]) < 1e-13
+
+
+def test_null_vectors_match_reference(gold, setup):
+    M, MG, geo, op, A, Pg = setup
+    nv = MG.generate_null_vectors(op, int(gold["null_nv"]), tol=1e-12, max_iter=8, seed=int(gold["null_seed"]))
+    Y = nv.ref_vectors(op)
+    G = gold["null_vectors"]
+    assert np.max(np.linalg.norm(Y - G, axis=1) / np.linalg.norm(G, axis=1)) < 1e-12
+
+
+def test_prolongator_matches_reference(gold, setup):
+    M, MG, geo, op, A, Pg = setup
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    assert pro.uniform and pro.dropped == 0
+    assert np.array_equal(pro.coarse_gamma5, gold["coarse_gamma5"])
+    D = pro.dense()
+    assert np.abs(D - Pg.toarray()).max() < 1e-12
+    # P and P^H applications against the reference CSR on the same P
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=op.dim) + 1j * rng.normal(size=op.dim)
+    xc = rng.normal(size=pro.coarse_dim) + 1j * rng.normal(size=pro.coarse_dim)
+    r_ref = Pg.conj().T @ x
+    p_ref = Pg @ xc
+    assert np.linalg.norm(pro.restrict(x) - r_ref) / np.linalg.norm(r_ref) < 1e-12
+    assert np.linalg.norm(pro.prolong(xc) - p_ref) / np.linalg.norm(p_ref) < 1e-12
+    # V^H V = I
+    assert np.abs(D.conj().T @ D - np.eye(pro.coarse_dim)).max() < 1e-13
+
+
+def test_coarse_operator_matches_reference(gold, setup):
+    M, MG, geo, op, A, Pg = setup
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    C = MG.build_coarse_operator(op, pro)
+    Cd = C.dense()
+    G = gold["C_dense"]
+    assert np.abs(Cd - G).max() < 1e-12 * np.abs(G).max()
+    xc = np.random.default_rng(2).normal(size=C.dim) + 0.5j
+    assert np.linalg.norm(C.apply(xc) - G @ xc) / np.linalg.norm(G @ xc) < 1e-12
+
+
+def test_full_coarse_deflation_matches_reference(gold, setup):
+    M, MG, geo, op, A, Pg = setup
+    from paper_1909_12234_b200 import trace as TR
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=1e-8))
+    probes = M.build_probe_set(geo, 12, 3, hp_count=1, dilution=False, kind="rademacher",
+                               seed=int(gold["obl_seed0"]))
+    est = TR.deflate_oblique_coarse(op, inv, pro, TR.IdentityTriplets(pro.coarse_dim), pro.coarse_dim, probes)
+    t0 = complex(gold["obl_t0"])
+    assert abs(est.t0 - t0) < 1e-10 * abs(t0)
+    # reference: GCR(32) + Y = A^-1_xi(A P); ours: BiCGStab + Y = P; both O(xi)
+    rel = np.abs(est.samples - gold["obl_samples"]) / np.abs(gold["obl_samples"])
+    assert rel.max() < 1e-6
+    assert abs(est.mean - complex(gold["obl_mean"])) / abs(complex(gold["obl_mean"])) < 1e-8 + 1e-10
+
+
+def test_config3_shape_against_oracle(cuda):
+    """8^4, 4^4 aggregates, nv = 24 (the config-3 blocking at reduced volume):
+    GPU null vectors + P + C against the oracle restatement."""
+    import paper_1909_12234_b200 as M
+    from paper_1909_12234_b200 import multigrid as MG
+    dims = (8, 8, 8, 8)
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    gauge = M.generate_gauge(geo, "su3", eps=0.2, seed=0)
+    op = M.build_wilson(gauge, 0.1)
+    links = gauge.links.cpu().numpy()
+    A = W.build_wilson4d_csr(links, dims, 0.1)
+    nvs = MG.generate_null_vectors(op, 24, tol=1e-12, max_iter=8, seed=9)
+    Yo = OMG.null_vectors(lambda v: A @ v, A.shape[0], 24, tol=1e-12, max_iter=8, seed=9)
+    Yg = nvs.ref_vectors(op)
+    assert np.max(np.linalg.norm(Yg - Yo, axis=1)) < 1e-11
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme((4, 4, 4, 4)), layout_op=op)
+    Po, g5c, counts, dropped = OMG.prolongator(Yo, dims, (4, 4, 4, 4), W.gamma5_diag(geo.site_count))
+    rng = np.random.default_rng(3)
+    x = rng.normal(size=op.dim) + 1j * rng.normal(size=op.dim)
+    assert np.linalg.norm(pro.restrict(x) - Po.conj().T @ x) / np.linalg.norm(Po.conj().T @ x) < 1e-11
+    C = MG.build_coarse_operator(op, pro)
+    Co = OMG.coarse_operator(A, Po, g5c).toarray()
+    assert np.abs(C.dense() - Co).max() < 1e-11 * np.abs(Co).max()
