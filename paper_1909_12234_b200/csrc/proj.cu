@@ -1,0 +1,208 @@
+// Tall-skinny deflation projections (reference: trace.py:179-183, :266-267;
+// eigen.py:79-86 CGS2 `v - Q (Q^H v)`):
+//   H = V^H X            (k x s),   V: k vectors, X: s vectors, length len
+//   X <- X - V H         (the projected probes X - V (V^H X) when H = V^H X)
+// fp64 complex on the FP64 pipe (B200 has no fp64 tensor-core advantage).
+// V^H X is split over the long dimension: every block produces a k x s
+// partial in a fixed order and a final kernel sums the partials in block
+// order, so results are bitwise reproducible.
+//  * s <= 8 ("GEMV-like", HBM-bound on V): thread per element, each warp
+//    owns 8 vectors, a block 64; X comes from L1 to the 8 warps.
+//  * s > 8  ("GEMM-like", FP64-bound): 64x64 output tiles staged through
+//    shared memory with 4x4 complex register micro-tiles.
+#include <algorithm>
+
+#include "reduce.cuh"
+
+namespace mgt {
+
+constexpr int kWarpVecs = 8;
+constexpr int kBlockVecs = 64;
+
+template <int S>
+__global__ void __launch_bounds__(256) vhx_small_kernel(const double2 *__restrict__ V, const double2 *__restrict__ X,
+                                                        int64_t len, int k, double2 *__restrict__ part) {
+  __shared__ double2 red[8][kWarpVecs * S];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = blockIdx.y * kBlockVecs + warp * kWarpVecs;
+  C<double> acc[kWarpVecs][S];
+#pragma unroll
+  for (int a = 0; a < kWarpVecs; ++a)
+#pragma unroll
+    for (int j = 0; j < S; ++j) acc[a][j] = C<double>(0.0, 0.0);
+  for (int64_t e = blockIdx.x * 32 + lane; e < len; e += (int64_t)gridDim.x * 32) {
+    C<double> xv[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) xv[j] = ldc(X + (int64_t)j * len + e);
+#pragma unroll
+    for (int a = 0; a < kWarpVecs; ++a) {
+      if (i0 + a < k) {
+        C<double> v = ldc(V + (int64_t)(i0 + a) * len + e);
+#pragma unroll
+        for (int j = 0; j < S; ++j) acc[a][j] = cfma_conj(v, xv[j], acc[a][j]);
+      }
+    }
+  }
+  // warp reduce, then each warp writes its own 8 x S values (distinct i)
+#pragma unroll
+  for (int a = 0; a < kWarpVecs; ++a)
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      C<double> v = acc[a][j];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        v.re += __shfl_xor_sync(0xffffffffu, v.re, off);
+        v.im += __shfl_xor_sync(0xffffffffu, v.im, off);
+      }
+      if (lane == 0) red[warp][a * S + j] = make_double2(v.re, v.im);
+    }
+  __syncwarp();
+  for (int q = lane; q < kWarpVecs * S; q += 32) {
+    const int a = q / S, j = q % S;
+    if (i0 + a < k) part[((int64_t)blockIdx.x * k + (i0 + a)) * S + j] = red[warp][q];
+  }
+}
+
+// 64 x 64 tile of V^H X over an e-chunk range; part: [block.x][k][s]
+__global__ void __launch_bounds__(256) vhx_tile_kernel(const double2 *__restrict__ V, const double2 *__restrict__ X,
+                                                       int64_t len, int k, int s, double2 *__restrict__ part) {
+  constexpr int T = 64, E = 8;
+  __shared__ double2 sV[E][T + 1];
+  __shared__ double2 sX[E][T + 1];
+  const int ti = threadIdx.x / 16, tj = threadIdx.x % 16;  // 16 x 16 threads, 4 x 4 each
+  const int i0 = blockIdx.y * T, j0 = blockIdx.z * T;
+  C<double> acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = C<double>(0.0, 0.0);
+  for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < len; e0 += (int64_t)gridDim.x * E) {
+    // stage: 256 threads load 64 x 8 of V and of X (2 each)
+    for (int q = threadIdx.x; q < T * E; q += 256) {
+      const int r = q / E, c = q % E;
+      const int64_t e = e0 + c;
+      sV[c][r] = (i0 + r < k && e < len) ? V[(int64_t)(i0 + r) * len + e] : make_double2(0.0, 0.0);
+      sX[c][r] = (j0 + r < s && e < len) ? X[(int64_t)(j0 + r) * len + e] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < E; ++c) {
+      C<double> va[4], xb[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) va[a] = C<double>(sV[c][ti * 4 + a].x, sV[c][ti * 4 + a].y);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) xb[b] = C<double>(sX[c][tj * 4 + b].x, sX[c][tj * 4 + b].y);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = cfma_conj(va[a], xb[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + ti * 4 + a, j = j0 + tj * 4 + b;
+      if (i < k && j < s) part[((int64_t)blockIdx.x * k + i) * s + j] = make_double2(acc[a][b].re, acc[a][b].im);
+    }
+}
+
+// H[j*k + i] (column major k x s) = sum over blocks of part[b][i][j]
+__global__ void vhx_reduce_kernel(const double2 *__restrict__ part, int nblk, int k, int s, double2 *__restrict__ H) {
+  const int64_t n = (int64_t)k * s;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(q / s), j = (int)(q % s);
+    C<double> t(0.0, 0.0);
+    for (int b = 0; b < nblk; ++b) t = t + ldc(part + (int64_t)b * n + q);
+    H[(int64_t)j * k + i] = make_double2(t.re, t.im);
+  }
+}
+
+// X[j] -= sum_i V[i] H[i, j] for j in a 16-wide tile (grid.y)
+template <int TJ>
+__global__ void __launch_bounds__(256) proj_sub_kernel(const double2 *__restrict__ V, const double2 *__restrict__ H,
+                                                       double2 *__restrict__ X, int64_t len, int k, int s) {
+  extern __shared__ double2 sH[];  // k x TJ
+  const int j0 = blockIdx.y * TJ;
+  for (int q = threadIdx.x; q < k * TJ; q += blockDim.x) {
+    const int i = q / TJ, j = q % TJ;
+    sH[q] = (j0 + j < s) ? H[(int64_t)(j0 + j) * k + i] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    C<double> acc[TJ];
+#pragma unroll
+    for (int j = 0; j < TJ; ++j) acc[j] = C<double>(0.0, 0.0);
+    for (int i = 0; i < k; ++i) {
+      const C<double> v = ldc(V + (int64_t)i * len + e);
+#pragma unroll
+      for (int j = 0; j < TJ; ++j) acc[j] = cfma(v, C<double>(sH[i * TJ + j].x, sH[i * TJ + j].y), acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < TJ; ++j) {
+      if (j0 + j < s) {
+        double2 *p = X + (int64_t)(j0 + j) * len + e;
+        const double2 x = *p;
+        *p = make_double2(x.x - acc[j].re, x.y - acc[j].im);
+      }
+    }
+  }
+}
+
+}  // namespace mgt
+
+using namespace mgt;
+
+extern "C" {
+
+int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s, void *H_dev, void *stream) {
+  if (!V_dev || !X_dev || !H_dev || len < 0 || k < 1 || s < 1) return fail(MGT_ERR_INVALID, "mgt_proj_vhx: bad argument");
+  cudaStream_t st = as_stream(stream);
+  const double2 *V = (const double2 *)V_dev, *X = (const double2 *)X_dev;
+  int nblk;
+  double2 *part = nullptr;
+  if (s <= 4) {
+    const int gy = (k + kBlockVecs - 1) / kBlockVecs;
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, (int64_t)kNumSMs * 4 / gy + 1));
+    MGT_CUDA(cudaMallocAsync((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
+    dim3 grid(nblk, gy);
+#define MGT_VHX(SS) vhx_small_kernel<SS><<<grid, 256, 0, st>>>(V, X, len, k, part)
+    switch (s) {
+      case 1: MGT_VHX(1); break;
+      case 2: MGT_VHX(2); break;
+      case 3: MGT_VHX(3); break;
+      default: MGT_VHX(4); break;
+    }
+#undef MGT_VHX
+    MGT_LAUNCH_CHECK("vhx_small_kernel");
+  } else {
+    const int gy = (k + 63) / 64, gz = (s + 63) / 64;
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, (int64_t)kNumSMs * 4 / (gy * gz) + 1));
+    MGT_CUDA(cudaMallocAsync((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
+    dim3 grid(nblk, gy, gz);
+    vhx_tile_kernel<<<grid, 256, 0, st>>>(V, X, len, k, s, part);
+    MGT_LAUNCH_CHECK("vhx_tile_kernel");
+  }
+  vhx_reduce_kernel<<<grid_for((int64_t)k * s, 128, 4), 128, 0, st>>>(part, nblk, k, s, (double2 *)H_dev);
+  MGT_LAUNCH_CHECK("vhx_reduce_kernel");
+  MGT_CUDA(cudaFreeAsync(part, st));
+  return MGT_OK;
+}
+
+int mgt_proj_sub(const void *V_dev, const void *H_dev, void *X_dev, int64_t len, int k, int s, void *stream) {
+  if (!V_dev || !X_dev || !H_dev || len < 0 || k < 1 || s < 1) return fail(MGT_ERR_INVALID, "mgt_proj_sub: bad argument");
+  cudaStream_t st = as_stream(stream);
+  constexpr int TJ = 8;
+  dim3 grid(grid_for(len, 256, 4), (s + TJ - 1) / TJ);
+  const size_t smem = (size_t)k * TJ * sizeof(double2);
+  if (smem > 200 * 1024) return fail(MGT_ERR_INVALID, "mgt_proj_sub: k too large");
+  if (smem > 48 * 1024)
+    MGT_CUDA(cudaFuncSetAttribute(proj_sub_kernel<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  proj_sub_kernel<TJ><<<grid, 256, smem, st>>>((const double2 *)V_dev, (const double2 *)H_dev, (double2 *)X_dev, len,
+                                               k, s);
+  MGT_LAUNCH_CHECK("proj_sub_kernel");
+  return MGT_OK;
+}
+
+}  // extern "C"

@@ -131,6 +131,43 @@ def _group_samples_generic(apply_fn, probes, health=None):
     return samples, flagged
 
 
+def deflate_orthogonal(inv_op, U, probes, op=None):
+    """Algorithm-1 trace estimate with the orthogonal projector of U
+    (trace.py:161-188): t0 = sum_i u_i^H A^-1 u_i and per slot
+    z^H (A^-1 z - Y U^H z) = q - (Y^H z)^H (U^H z), Y = A^-1 U solved once.
+
+    U: native fields (k, 12, V) CUDA tensor, or reference-layout (N, k)
+    array/tensor (then `op` or inv_op.op converts the layout)."""
+    import torch
+    from .linalg import vhx
+    before = getattr(inv_op, "n_solves", 0)
+    base = op if op is not None else inv_op.op
+    if not (isinstance(U, torch.Tensor) and U.dim() == 3):
+        Ut = torch.as_tensor(np.ascontiguousarray(np.asarray(U).T)) if not isinstance(U, torch.Tensor) \
+            else U.transpose(0, 1).contiguous()
+        U = base.to_native(Ut.to(torch.complex128).cuda()) if Ut.numel() else None
+    k = 0 if U is None else U.shape[0]
+    if k == 0:
+        samples, flagged = group_samples_gpu(inv_op, probes)
+        _warn_flagged(flagged)
+        return finish(0.0, samples, (inv_op.n_solves - before) or probes.slot_count, flagged)
+    gram = vhx(U, U) - torch.eye(k, dtype=torch.complex128, device=U.device)
+    gmax = gram.abs().max().item()
+    if gmax > 1e-6:
+        raise DeflationContractError(f"U not orthonormal: ||U^dag U - I||_max = {gmax:.3e}")
+    Y, _, _ = inv_op.solve_native(U)
+    t0 = complex(torch.diagonal(vhx(U, Y)).sum().item())
+
+    def correction(j0, z, x):
+        a = vhx(U, z)  # (k, n)  U^H z
+        h = vhx(Y, z)  # (k, n)  Y^H z
+        return torch.sum(h.conj() * a, dim=0).cpu().numpy()
+
+    samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
+    _warn_flagged(flagged)
+    return finish(t0, samples, inv_op.n_solves - before, flagged)
+
+
 @dataclass
 class ObliqueFactors:
     """Small factors of the coarse oblique deflation (trace.py:191-204)."""

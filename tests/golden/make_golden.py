@@ -90,6 +90,23 @@ def main():
     out["obl_samples"] = est2.samples
     out["obl_mean"] = est2.mean
     out["obl_seed0"] = 40
+    # Algorithm 1: inexact Davidson eigenpairs of A gamma5, then orthogonal
+    # deflation with the reference's own U
+    from mgtrace import eigen
+    econf = eigen.EigenConfig(k=6, tol=1e-4, inner=krylov.SolveConfig(tol=1e-10))
+    fac = eigen.shift_inverter_factory(op, econf.inner)
+    res = eigen.inexact_eigensolve(op, op.gamma5_diag, econf, fac)
+    out["eig_lambdas"] = res.lambdas
+    out["eig_residuals"] = res.residuals
+    out["eig_converged"] = res.converged
+    out["eig_vectors"] = res.vectors
+    out["eig_exact"] = eigen.dense_triplets(op).lambdas[:6]
+    inv3 = krylov.TruncatedInverse(op, krylov.SolveConfig(tol=1e-8))
+    ps3 = probing.build_probe_set(geo, 12, 3, hp_count=1, dilution=False, kind="rademacher", seed=70)
+    est3 = trace.deflate_orthogonal(inv3, res.vectors, ps3)
+    out["orth_t0"] = est3.t0
+    out["orth_samples"] = est3.samples
+    out["orth_seed0"] = 70
     np.savez_compressed(os.path.join(HERE, "golden_4x4x4x4.npz"), **out)
     print("wrote golden_4x4x4x4.npz", {k: np.shape(v) for k, v in out.items()})
 

@@ -186,3 +186,18 @@ def test_full_coarse_deflation_restatement_matches_golden(gold, small_op):
     assert abs(est["t0"] - complex(gold["obl_t0"])) < 1e-10 * abs(complex(gold["obl_t0"]))
     # the reference uses Y = A^-1_xi (A P) in place of P: differences O(xi)
     assert np.max(np.abs(est["samples"] - gold["obl_samples"]) / np.abs(gold["obl_samples"])) < 1e-6
+
+
+def test_orthogonal_deflation_restatement_matches_golden(gold, small_op):
+    dims, A = small_op
+    inv = K.TruncatedInverse(lambda v: A @ v, 1e-8)
+    N = A.shape[0]
+    probes = [[P.rademacher(N, int(gold["orth_seed0"]) + j)] for j in range(3)]
+    est = T.deflate_orthogonal(inv, gold["eig_vectors"], probes)
+    assert est["t0"] == complex(gold["orth_t0"])
+    assert np.array_equal(est["samples"], gold["orth_samples"])
+
+
+def test_reference_eigenvalues_are_accurate(gold):
+    # the reference Davidson's Rayleigh-Ritz values vs the dense oracle
+    assert np.max(np.abs(gold["eig_lambdas"] - gold["eig_exact"]) / np.abs(gold["eig_exact"])) < 1e-6
