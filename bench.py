@@ -215,9 +215,11 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     # probes/s, BASELINE configs[0]: 8^4, s=32 Rademacher, tol 1e-8
-    probes = None
+    probes = probes3 = None
     if not args.skip_probes:
-        probes = probes_per_sec(M, rank, world)
+        probes = probes_config1(M, rank, world)
+        if not args.skip_deflated:
+            probes3 = probes_config3(M, rank, world)
 
     if rank == 0:
         line = {
@@ -240,10 +242,12 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "probes_per_sec": probes,
+            "deflated_probes_per_sec": probes3,
         }
         if world == 1 and not args.skip_cpu:
             try:
                 line["cpu_baseline"] = cpu_matvec_sample(min_seconds=args.cpu_seconds)
+                line["cpu_baseline_probes"] = cpu_probes_sample()
             except Exception as e:  # reported, not fatal
                 line["cpu_baseline"] = {"error": str(e)[:200]}
         print(json.dumps(line), flush=True)
@@ -252,31 +256,95 @@ def run_ours(args):
     return 0
 
 
-def probes_per_sec(M, rank, world, dims=(8, 8, 8, 8), s=32, tol=1e-8):
+def _max_over_ranks(v, world):
     import torch
     import torch.distributed as dist
-    geo = M.LatticeGeometry(dims, "antiperiodic")
-    op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.2, seed=0), 0.1)
-    # probe sharding: rank r takes probes j = r, r + world, ...
-    mine = list(range(rank, s, world))
-    probes = M.build_probe_set(geo, 12, len(mine), hp_count=1, dilution=False, kind="rademacher", seed=0)
-    inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
-    M.hutchinson(inv, M.build_probe_set(geo, 12, 4, dilution=False, kind="rademacher", seed=1000))  # warm
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    est = M.hutchinson(inv, probes)
-    torch.cuda.synchronize()
-    el = time.perf_counter() - t0
-    t = torch.tensor([el], device="cuda")
+    t = torch.tensor([v], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    el = float(t.item())
+    return float(t.item())
+
+
+def _sharded_estimate(M, estimate, geo, s, seed, rank, world, reps=2):
+    """Probe sharding (no data-path collective): rank r solves the contiguous
+    probe block [r*s/world, (r+1)*s/world); probe j keeps seed seed + j, so
+    the union of the shards is exactly the single-GPU probe set.  Returns
+    (estimate, wall seconds max over ranks); the first `reps - 1` runs warm
+    the worker streams, solver workspaces and graphs."""
+    import torch
+    import torch.distributed as dist
+    j0 = rank * s // world
+    j1 = (rank + 1) * s // world
+    probes = M.build_probe_set(geo, 12, j1 - j0, hp_count=1, dilution=False, kind="rademacher", seed=seed + j0)
+    el = None
+    for _ in range(reps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        est = estimate(probes)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+    return est, _max_over_ranks(el, world)
+
+
+def probes_config1(M, rank, world, dims=(8, 8, 8, 8), s=32, tol=1e-8):
+    """BASELINE configs[0]: undeflated Hutchinson, 8^4, s = 32, tol 1e-8."""
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.2, seed=0), 0.1)
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
+    est, el = _sharded_estimate(M, lambda p: M.hutchinson(inv, p), geo, s, 0, rank, world)
     its = inv.total_iterations / max(1, inv.n_solves)
     return {"config": "8x8x8x8 eps=0.2 m0=0.1 s=32 rademacher tol=1e-8 (BASELINE configs[0])",
             "value": s / el, "unit": "probes/s", "seconds": el, "mean_iterations": its,
-            "solver": "BiCGStab, 4 rhs per solve", "estimate_re": float(est.mean.real) if world == 1 else None}
+            "solver": "BiCGStab, 4 rhs per solve, 8 concurrent solves",
+            "estimate_re": float(est.mean.real) if world == 1 else None}
+
+
+def probes_config3(M, rank, world, dims=(16, 16, 16, 16), s=128, tol=1e-8, nv=24):
+    """BASELINE configs[2]: 16^4, 4^4 aggregates, 24 null vectors relaxed by
+    GCR(8), full-prolongator (Algorithm 2, rank Nc) deflated Hutchinson."""
+    import torch
+    from paper_1909_12234_b200 import multigrid as MG
+    from paper_1909_12234_b200 import trace as TR
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.2, seed=0), 0.1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    nvs = MG.generate_null_vectors(op, nv, tol=1e-12, max_iter=8, seed=7)
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme((4, 4, 4, 4)), layout_op=op)
+    coarse = MG.build_coarse_operator(op, pro)
+    torch.cuda.synchronize()
+    setup = _max_over_ranks(time.perf_counter() - t0, world)
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
+    trip = TR.IdentityTriplets(pro.coarse_dim)
+    est, el = _sharded_estimate(
+        M, lambda p: TR.deflate_oblique_coarse(op, inv, pro, trip, pro.coarse_dim, p, coarse_op=coarse),
+        geo, s, 100, rank, world)
+    return {"config": "16^4 eps=0.2 m0=0.1, 4^4 aggregates, nv=24 GCR(8) null vectors, full-V oblique "
+                      "deflation, s=128 rademacher tol=1e-8 (BASELINE configs[2])",
+            "value": s / el, "unit": "probes/s", "seconds": el, "setup_seconds": setup,
+            "value_including_setup": s / (el + setup), "Nc": pro.coarse_dim,
+            "t0_re": float(est.t0.real), "estimate_re": float(est.mean.real) if world == 1 else None,
+            "variance": float(est.variance) if world == 1 else None,
+            "mean_iterations": inv.total_iterations / max(1, inv.n_solves)}
+
+
+def cpu_probes_sample(dims=(8, 8, 8, 8), n=4, tol=1e-8):
+    """Reference path port (restated GCR(32) + Hutchinson, numpy/scipy, one
+    process) on `n` config-1 probes."""
+    from oracle import krylov as OK
+    from oracle import pcg64 as OP
+    from oracle import trace as OT
+    from oracle import wilson4d as W
+    A = W.build_wilson4d_csr(W.su3_links(dims, 0.2, 0), dims, 0.1)
+    inv = OK.TruncatedInverse(lambda v: A @ v, tol)
+    N = A.shape[0]
+    t0 = time.perf_counter()
+    OT.hutchinson(inv, [[OP.rademacher_numpy(N, j)] for j in range(n)])
+    el = time.perf_counter() - t0
+    return {"value": n / el, "unit": "probes/s", "cores": 1, "kind": "port",
+            "sample": f"{n} config-1 probes (8^4, GCR(32) tol 1e-8, scipy CSR), {el:.1f} s"}
 
 
 def main():
@@ -289,6 +357,7 @@ def main():
     ap.add_argument("--prec", type=int, default=64, choices=[64, 32])
     ap.add_argument("--recon", type=int, default=12, choices=[18, 12])
     ap.add_argument("--skip-probes", action="store_true")
+    ap.add_argument("--skip-deflated", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

@@ -2,7 +2,7 @@
 // plugin (reference: krylov.py:200-229; the reference's own solver is GCR,
 // krylov.py:52-118, BASELINE.json names BiCGStab).
 //
-// Per iteration (complex BiCGStab, x0 = 0):
+// Per iteration (complex BiCGStab, x0 = 0), NR right-hand sides at once:
 //   K1  v = A p                       sigma = (rhat, v)      alpha = rho/sigma
 //   K2  s = r - alpha v               |s|^2  (early exit when s is converged)
 //   K3  t = A s                       (t, s), |t|^2          omega = (t,s)/|t|^2
@@ -10,11 +10,16 @@
 //   K5  p = r + beta (p - omega v)
 // Every reduction is fused into the producing kernel (reduce.cuh) and the
 // scalar recurrences run in that kernel's last block, so the host only
-// launches; it reads the per-rhs status word once per chunk of iterations.
-// Convergence is confirmed on the explicitly recomputed residual b - A x
-// (krylov.py:78-85, :113-118); a recursion/true-residual mismatch restarts
-// with rhat = r.
+// launches: chunks of iterations are replayed from a cached CUDA graph and
+// the host reads the per-rhs status words once per chunk.  Kernels of a
+// converged rhs return immediately.  Convergence is confirmed on the
+// explicitly recomputed residual b - A x (krylov.py:78-85, :113-118); a
+// recursion / true-residual mismatch restarts with rhat = r.
 #include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "handle.cuh"
@@ -30,15 +35,16 @@ struct BiState {
   int status, half, iters, maxit, matvecs, reason, pad0, pad1;
 };
 
+// Workspace: fields of NR rhs each (native layout) + reduction scratch.
 struct BiWS {
-  double2 *r, *rhat, *p, *v, *s, *t;
+  double2 *r, *rhat, *p, *v, *s, *t, *x, *b;
   double *partials;
   unsigned *ticket;
   BiState *st;
 };
 
 template <int NR>
-__device__ __forceinline__ bool any_running(const BiState *st, int want = ST_RUN) {
+__device__ __forceinline__ bool any_status(const BiState *st, int want) {
   bool any = false;
 #pragma unroll
   for (int r = 0; r < NR; ++r) any |= (st[r].status == want);
@@ -51,38 +57,38 @@ __device__ __forceinline__ C<double> cdiv(C<double> a, C<double> b) {
 }
 __device__ __forceinline__ bool czero(C<double> a) { return a.re == 0.0 && a.im == 0.0; }
 __device__ __forceinline__ double cabs2(C<double> a) { return a.re * a.re + a.im * a.im; }
+__device__ __forceinline__ bool cfinite(C<double> a) { return isfinite(a.re) && isfinite(a.im); }
 
-#define FOR_SITES(NR)                                                                          \
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;                  \
-       idx += (int64_t)gridDim.x * blockDim.x)
+#define MGT_SITE_LOOP(M, V) for (int64_t o = (M).first(); o < (V); o += (M).stride())
 
 // ---------------------------------------------------------------------------
+// init: b -> workspace, r = rhat = p = b, x = 0, |b|^2
 template <int NR>
-__global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *__restrict__ b, double2 *__restrict__ x,
-                                                     BiWS w, double tol, int maxit) {
-  const int64_t n = V * NR;
+__global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *__restrict__ b, BiWS w, double tol,
+                                                     int maxit) {
+  RhsMap<NR> m;
   double acc[1] = {0.0};
-  FOR_SITES(NR) {
-    const int64_t site = idx / NR;
-    const int rhs = (int)(idx % NR);
-    const int64_t base = (int64_t)rhs * 12 * V + site;
+  MGT_SITE_LOOP(m, V) {
+    const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
-      const int64_t o = base + (int64_t)c * V;
-      double2 bb = b[o];
-      w.r[o] = bb;
-      w.rhat[o] = bb;
-      w.p[o] = bb;
-      x[o] = make_double2(0.0, 0.0);
+      const int64_t q = base + (int64_t)c * V;
+      double2 bb = b[q];
+      w.b[q] = bb;
+      w.r[q] = bb;
+      w.rhat[q] = bb;
+      w.p[q] = bb;
+      w.x[q] = make_double2(0.0, 0.0);
       acc[0] += bb.x * bb.x + bb.y * bb.y;
     }
   }
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR) {
-      BiState &s = w.st[threadIdx.x];
-      const double b2 = out[threadIdx.x];
+    const int r = threadIdx.x;
+    if (r < NR) {
+      BiState &s = w.st[r];
+      const double b2 = out[r];
       s.b2 = b2;
       s.r2 = b2;
       s.s2 = b2;
@@ -106,37 +112,38 @@ __global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *_
 // K1: v = A p ; sigma = (rhat, v)
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
-  if (!any_running<NR>(w.st)) return;
-  const int my = threadIdx.x % NR;  // blockDim and the grid stride are multiples of NR
-  const bool run_me = (w.st[my].status == ST_RUN);
-  const int64_t V = P.g.V, n = V * NR;
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool run_me = w.st[m.rhs].status == ST_RUN;
+  const int64_t V = P.g.V;
   double acc[2] = {0.0, 0.0};
-  FOR_SITES(NR) {
-    const int64_t site = sched_site(P.sched, idx / NR);
-    const int rhs = (int)(idx % NR);
-    if (!run_me) continue;
-    const int64_t off = (int64_t)rhs * 12 * V;
-    C<double> y[4][3], xc[4][3];
-    wilson_eval<double, RECON>(P, w.p + off, L, site, y, xc);
+  if (run_me) {
+    const int64_t off = (int64_t)m.rhs * 12 * V;
+    MGT_SITE_LOOP(m, V) {
+      const int64_t site = sched_site(P.sched, o);
+      C<double> y[4][3], xc[4][3];
+      wilson_eval<double, RECON>(P, w.p + off, L, site, y, xc);
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t o = off + (int64_t)(a * 3 + c) * V + site;
-        stc(w.v + o, y[a][c]);
-        C<double> rh = ldc(w.rhat + o);
-        acc[0] += rh.re * y[a][c].re + rh.im * y[a][c].im;
-        acc[1] += rh.re * y[a][c].im - rh.im * y[a][c].re;
-      }
+        for (int c = 0; c < 3; ++c) {
+          const int64_t q = off + (int64_t)(a * 3 + c) * V + site;
+          stc(w.v + q, y[a][c]);
+          C<double> rh = ldc(w.rhat + q);
+          acc[0] += rh.re * y[a][c].re + rh.im * y[a][c].im;
+          acc[1] += rh.re * y[a][c].im - rh.im * y[a][c].re;
+        }
+    }
   }
   if (reduce_publish<NR, 2>(acc, w.partials, w.ticket)) {
     double out[NR * 2];
     reduce_finish<NR * 2>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && run_me) {
-      BiState &s = w.st[threadIdx.x];
-      C<double> sigma(out[2 * threadIdx.x], out[2 * threadIdx.x + 1]);
+    const int r = threadIdx.x;
+    if (r < NR && w.st[r].status == ST_RUN) {
+      BiState &s = w.st[r];
+      C<double> sigma(out[2 * r], out[2 * r + 1]);
       s.matvecs += 1;
-      if (czero(sigma) || !isfinite(sigma.re) || !isfinite(sigma.im)) {
+      if (czero(sigma) || !cfinite(sigma)) {
         s.status = ST_BREAK;
         s.reason = 2;
       } else {
@@ -149,32 +156,30 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<
 // K2: s = r - alpha v ; |s|^2
 template <int NR>
 __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
-  if (!any_running<NR>(w.st)) return;
-  const int my = threadIdx.x % NR;
-  const bool run_me = (w.st[my].status == ST_RUN);
-  const C<double> al = w.st[my].alpha;
-  const int64_t n = V * NR;
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool run_me = w.st[m.rhs].status == ST_RUN;
+  const C<double> al = w.st[m.rhs].alpha;
   double acc[1] = {0.0};
-  FOR_SITES(NR) {
-    const int64_t site = idx / NR;
-    const int rhs = (int)(idx % NR);
-    if (!run_me) continue;
-    const int64_t base = (int64_t)rhs * 12 * V + site;
+  if (run_me) {
+    MGT_SITE_LOOP(m, V) {
+      const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      const int64_t o = base + (int64_t)c * V;
-      C<double> rr = ldc(w.r + o), vv = ldc(w.v + o);
-      C<double> ss = rr - al * vv;
-      stc(w.s + o, ss);
-      acc[0] += cabs2(ss);
+      for (int c = 0; c < 12; ++c) {
+        const int64_t q = base + (int64_t)c * V;
+        C<double> ss = ldc(w.r + q) - al * ldc(w.v + q);
+        stc(w.s + q, ss);
+        acc[0] += cabs2(ss);
+      }
     }
   }
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && run_me) {
-      BiState &s = w.st[threadIdx.x];
-      s.s2 = out[threadIdx.x];
+    const int r = threadIdx.x;
+    if (r < NR && w.st[r].status == ST_RUN) {
+      BiState &s = w.st[r];
+      s.s2 = out[r];
       s.half = (s.s2 <= s.tol2) ? 1 : 0;
     }
   }
@@ -183,37 +188,37 @@ __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
 // K3: t = A s ; (t, s), |t|^2
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
-  if (!any_running<NR>(w.st)) return;
-  const int my = threadIdx.x % NR;  // blockDim and the grid stride are multiples of NR
-  const bool run_me = (w.st[my].status == ST_RUN);
-  const int64_t V = P.g.V, n = V * NR;
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool run_me = w.st[m.rhs].status == ST_RUN;
+  const int64_t V = P.g.V;
   double acc[3] = {0.0, 0.0, 0.0};
-  FOR_SITES(NR) {
-    const int64_t site = sched_site(P.sched, idx / NR);
-    const int rhs = (int)(idx % NR);
-    if (!run_me) continue;
-    const int64_t off = (int64_t)rhs * 12 * V;
-    C<double> y[4][3], xc[4][3];
-    wilson_eval<double, RECON>(P, w.s + off, L, site, y, xc);
+  if (run_me) {
+    const int64_t off = (int64_t)m.rhs * 12 * V;
+    MGT_SITE_LOOP(m, V) {
+      const int64_t site = sched_site(P.sched, o);
+      C<double> y[4][3], xc[4][3];
+      wilson_eval<double, RECON>(P, w.s + off, L, site, y, xc);
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t o = off + (int64_t)(a * 3 + c) * V + site;
-        stc(w.t + o, y[a][c]);
-        const C<double> tt = y[a][c], ss = xc[a][c];
-        acc[0] += tt.re * ss.re + tt.im * ss.im;
-        acc[1] += tt.re * ss.im - tt.im * ss.re;
-        acc[2] += cabs2(tt);
-      }
+        for (int c = 0; c < 3; ++c) {
+          stc(w.t + off + (int64_t)(a * 3 + c) * V + site, y[a][c]);
+          const C<double> tt = y[a][c], ss = xc[a][c];
+          acc[0] += tt.re * ss.re + tt.im * ss.im;
+          acc[1] += tt.re * ss.im - tt.im * ss.re;
+          acc[2] += cabs2(tt);
+        }
+    }
   }
   if (reduce_publish<NR, 3>(acc, w.partials, w.ticket)) {
     double out[NR * 3];
     reduce_finish<NR * 3>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && run_me) {
-      BiState &s = w.st[threadIdx.x];
-      C<double> ts(out[3 * threadIdx.x], out[3 * threadIdx.x + 1]);
-      const double tt = out[3 * threadIdx.x + 2];
+    const int r = threadIdx.x;
+    if (r < NR && w.st[r].status == ST_RUN) {
+      BiState &s = w.st[r];
+      C<double> ts(out[3 * r], out[3 * r + 1]);
+      const double tt = out[3 * r + 2];
       s.matvecs += 1;
       if (s.half) {
         s.omega = C<double>(0.0, 0.0);
@@ -229,38 +234,37 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<
 
 // K4: x += alpha p + omega s ; r = s - omega t ; rho' = (rhat, r), |r|^2
 template <int NR>
-__global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, double2 *__restrict__ x, BiWS w) {
-  if (!any_running<NR>(w.st)) return;
-  const int my = threadIdx.x % NR;
-  const bool run_me = (w.st[my].status == ST_RUN);
-  const C<double> al = w.st[my].alpha, om = w.st[my].omega;
-  const int64_t n = V * NR;
+__global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w) {
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool run_me = w.st[m.rhs].status == ST_RUN;
+  const C<double> al = w.st[m.rhs].alpha, om = w.st[m.rhs].omega;
   double acc[3] = {0.0, 0.0, 0.0};
-  FOR_SITES(NR) {
-    const int64_t site = idx / NR;
-    const int rhs = (int)(idx % NR);
-    if (!run_me) continue;
-    const int64_t base = (int64_t)rhs * 12 * V + site;
+  if (run_me) {
+    MGT_SITE_LOOP(m, V) {
+      const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      const int64_t o = base + (int64_t)c * V;
-      C<double> xx = ldc(x + o), pp = ldc(w.p + o), ss = ldc(w.s + o), tt = ldc(w.t + o), rh = ldc(w.rhat + o);
-      xx = xx + al * pp + om * ss;
-      C<double> rr = ss - om * tt;
-      stc(x + o, xx);
-      stc(w.r + o, rr);
-      acc[0] += rh.re * rr.re + rh.im * rr.im;
-      acc[1] += rh.re * rr.im - rh.im * rr.re;
-      acc[2] += cabs2(rr);
+      for (int c = 0; c < 12; ++c) {
+        const int64_t q = base + (int64_t)c * V;
+        C<double> xx = ldc(w.x + q), pp = ldc(w.p + q), ss = ldc(w.s + q), tt = ldc(w.t + q), rh = ldc(w.rhat + q);
+        xx = xx + al * pp + om * ss;
+        C<double> rr = ss - om * tt;
+        stc(w.x + q, xx);
+        stc(w.r + q, rr);
+        acc[0] += rh.re * rr.re + rh.im * rr.im;
+        acc[1] += rh.re * rr.im - rh.im * rr.re;
+        acc[2] += cabs2(rr);
+      }
     }
   }
   if (reduce_publish<NR, 3>(acc, w.partials, w.ticket)) {
     double out[NR * 3];
     reduce_finish<NR * 3>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && run_me) {
-      BiState &s = w.st[threadIdx.x];
-      C<double> rho_new(out[3 * threadIdx.x], out[3 * threadIdx.x + 1]);
-      s.r2 = out[3 * threadIdx.x + 2];
+    const int r = threadIdx.x;
+    if (r < NR && w.st[r].status == ST_RUN) {
+      BiState &s = w.st[r];
+      C<double> rho_new(out[3 * r], out[3 * r + 1]);
+      s.r2 = out[3 * r + 2];
       s.iters += 1;
       if (s.r2 <= s.tol2 || s.half) {
         s.status = ST_CONV;
@@ -282,30 +286,23 @@ __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, double2 *__restric
 // K5: p = r + beta (p - omega v)
 template <int NR>
 __global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWS w) {
-  if (!any_running<NR>(w.st)) return;
-  const int my = threadIdx.x % NR;
-  const bool run_me = (w.st[my].status == ST_RUN);
-  const C<double> be = w.st[my].beta, om = w.st[my].omega;
-  const int64_t n = V * NR;
-  FOR_SITES(NR) {
-    const int64_t site = idx / NR;
-    const int rhs = (int)(idx % NR);
-    if (!run_me) continue;
-    const int64_t base = (int64_t)rhs * 12 * V + site;
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  if (w.st[m.rhs].status != ST_RUN) return;
+  const C<double> be = w.st[m.rhs].beta, om = w.st[m.rhs].omega;
+  MGT_SITE_LOOP(m, V) {
+    const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
-      const int64_t o = base + (int64_t)c * V;
-      C<double> rr = ldc(w.r + o), pp = ldc(w.p + o), vv = ldc(w.v + o);
-      stc(w.p + o, rr + be * (pp - om * vv));
+      const int64_t q = base + (int64_t)c * V;
+      stc(w.p + q, ldc(w.r + q) + be * (ldc(w.p + q) - om * ldc(w.v + q)));
     }
   }
 }
 
-// True residual r = b - A x for every rhs that stopped (status CONV/MAXIT/
-// BREAK); records |r|^2 in true_r2.
+// True residual r = b - A x for every rhs that stopped (CONV/MAXIT/BREAK)
 template <int NR, int RECON>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkField<double, RECON> L, const double2 *__restrict__ b,
-                                                      const double2 *__restrict__ x, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
   bool any = false;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
@@ -313,44 +310,47 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
     any |= (st == ST_CONV || st == ST_MAXIT || st == ST_BREAK);
   }
   if (!any) return;
-  const int my = threadIdx.x % NR;
-  const int st_me = w.st[my].status;
+  RhsMap<NR> m;
+  const int st_me = w.st[m.rhs].status;
   const bool act_me = (st_me == ST_CONV || st_me == ST_MAXIT || st_me == ST_BREAK);
-  const int64_t V = P.g.V, n = V * NR;
+  const int64_t V = P.g.V;
   double acc[1] = {0.0};
-  FOR_SITES(NR) {
-    const int64_t site = sched_site(P.sched, idx / NR);
-    const int rhs = (int)(idx % NR);
-    if (!act_me) continue;
-    const int64_t off = (int64_t)rhs * 12 * V;
-    C<double> y[4][3], xc[4][3];
-    wilson_eval<double, RECON>(P, x + off, L, site, y, xc);
+  if (act_me) {
+    const int64_t off = (int64_t)m.rhs * 12 * V;
+    MGT_SITE_LOOP(m, V) {
+      const int64_t site = sched_site(P.sched, o);
+      C<double> y[4][3], xc[4][3];
+      wilson_eval<double, RECON>(P, w.x + off, L, site, y, xc);
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t o = off + (int64_t)(a * 3 + c) * V + site;
-        C<double> rr = ldc(b + o) - y[a][c];
-        stc(w.r + o, rr);
-        acc[0] += cabs2(rr);
-      }
+        for (int c = 0; c < 3; ++c) {
+          const int64_t q = off + (int64_t)(a * 3 + c) * V + site;
+          C<double> rr = ldc(w.b + q) - y[a][c];
+          stc(w.r + q, rr);
+          acc[0] += cabs2(rr);
+        }
+    }
   }
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && act_me) {
-      BiState &s = w.st[threadIdx.x];
-      s.true_r2 = out[threadIdx.x];
-      s.matvecs += 1;
-      const bool ok = s.true_r2 <= s.tol2;
-      if (ok) {
-        s.status = ST_DONE;
-        s.reason = 0;
-      } else if (s.status == ST_CONV && s.iters < s.maxit) {
-        s.status = ST_RESTART;  // recursion drifted from the true residual
-      } else {
-        s.status = ST_DONE;
-        if (s.reason == 0) s.reason = 1;
+    const int r = threadIdx.x;
+    if (r < NR) {
+      BiState &s = w.st[r];
+      const int st = s.status;
+      if (st == ST_CONV || st == ST_MAXIT || st == ST_BREAK) {
+        s.true_r2 = out[r];
+        s.matvecs += 1;
+        if (s.true_r2 <= s.tol2) {
+          s.status = ST_DONE;
+          s.reason = 0;
+        } else if (st == ST_CONV && s.iters < s.maxit) {
+          s.status = ST_RESTART;  // recursion drifted from the true residual
+        } else {
+          s.status = ST_DONE;
+          if (s.reason == 0) s.reason = 1;
+        }
       }
     }
   }
@@ -359,31 +359,30 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
 // Restart for rhs flagged ST_RESTART: rhat = p = r (r holds the true residual)
 template <int NR>
 __global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w) {
-  if (!any_running<NR>(w.st, ST_RESTART)) return;
-  const int my = threadIdx.x % NR;
-  const bool act_me = (w.st[my].status == ST_RESTART);
-  const int64_t n = V * NR;
+  if (!any_status<NR>(w.st, ST_RESTART)) return;
+  RhsMap<NR> m;
+  const bool act_me = w.st[m.rhs].status == ST_RESTART;
   double acc[1] = {0.0};
-  FOR_SITES(NR) {
-    const int64_t site = idx / NR;
-    const int rhs = (int)(idx % NR);
-    if (!act_me) continue;
-    const int64_t base = (int64_t)rhs * 12 * V + site;
+  if (act_me) {
+    MGT_SITE_LOOP(m, V) {
+      const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      const int64_t o = base + (int64_t)c * V;
-      double2 rr = w.r[o];
-      w.rhat[o] = rr;
-      w.p[o] = rr;
-      acc[0] += rr.x * rr.x + rr.y * rr.y;
+      for (int c = 0; c < 12; ++c) {
+        const int64_t q = base + (int64_t)c * V;
+        double2 rr = w.r[q];
+        w.rhat[q] = rr;
+        w.p[q] = rr;
+        acc[0] += rr.x * rr.x + rr.y * rr.y;
+      }
     }
   }
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR && act_me) {
-      BiState &s = w.st[threadIdx.x];
-      s.r2 = out[threadIdx.x];
+    const int r = threadIdx.x;
+    if (r < NR && w.st[r].status == ST_RESTART) {
+      BiState &s = w.st[r];
+      s.r2 = out[r];
       s.rho = C<double>(s.r2, 0.0);
       s.alpha = C<double>(1.0, 0.0);
       s.omega = C<double>(1.0, 0.0);
@@ -393,20 +392,18 @@ __global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w) {
   }
 }
 
-// q = vdot(b, x) per rhs (Hutchinson quadratic form, trace.py:104)
+// copy x out and q = vdot(b, x) per rhs (Hutchinson quadratic form, trace.py:104)
 template <int NR>
-__global__ void __launch_bounds__(kRedBlock) bi_dot(int64_t V, const double2 *__restrict__ b, const double2 *__restrict__ x,
-                                                    BiWS w) {
-  const int64_t n = V * NR;
+__global__ void __launch_bounds__(kRedBlock) bi_final(int64_t V, double2 *__restrict__ xout, BiWS w) {
+  RhsMap<NR> m;
   double acc[2] = {0.0, 0.0};
-  FOR_SITES(NR) {
-    const int64_t site = idx / NR;
-    const int rhs = (int)(idx % NR);
-    const int64_t base = (int64_t)rhs * 12 * V + site;
+  MGT_SITE_LOOP(m, V) {
+    const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
-      const int64_t o = base + (int64_t)c * V;
-      C<double> bb = ldc(b + o), xx = ldc(x + o);
+      const int64_t q = base + (int64_t)c * V;
+      C<double> bb = ldc(w.b + q), xx = ldc(w.x + q);
+      stc(xout + q, xx);
       acc[0] += bb.re * xx.re + bb.im * xx.im;
       acc[1] += bb.re * xx.im - bb.im * xx.re;
     }
@@ -414,89 +411,147 @@ __global__ void __launch_bounds__(kRedBlock) bi_dot(int64_t V, const double2 *__
   if (reduce_publish<NR, 2>(acc, w.partials, w.ticket)) {
     double out[NR * 2];
     reduce_finish<NR * 2>(w.partials, w.ticket, out);
-    if (threadIdx.x < NR) w.st[threadIdx.x].dotq = C<double>(out[2 * threadIdx.x], out[2 * threadIdx.x + 1]);
+    const int r = threadIdx.x;
+    if (r < NR) w.st[r].dotq = C<double>(out[2 * r], out[2 * r + 1]);
   }
 }
 
 // ---------------------------------------------------------------------------
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+constexpr int kMaxGroup = 4;
+constexpr int kChunk = 8;  // iterations per graph replay
+
 struct WSLayout {
   size_t field, partials, total;
-  int grid;
 };
 
-static WSLayout ws_layout(int64_t V, int NRmax) {
+static WSLayout ws_layout(int64_t V) {
   WSLayout L;
-  L.field = align_up((size_t)NRmax * 12 * V * sizeof(double2), 256);
-  L.grid = kNumSMs * 16;  // upper bound of any resident grid at 128 threads
-  L.partials = align_up((size_t)L.grid * NRmax * 4 * sizeof(double), 256);
-  L.total = 6 * L.field + L.partials + 256 /*ticket*/ + align_up(NRmax * sizeof(BiState), 256);
+  L.field = align_up((size_t)kMaxGroup * 12 * V * sizeof(double2), 256);
+  L.partials = align_up((size_t)kNumSMs * 16 * kMaxGroup * 4 * sizeof(double), 256);
+  L.total = 8 * L.field + L.partials + 256 /*ticket*/ + align_up(kMaxGroup * sizeof(BiState), 256);
   return L;
 }
 
-template <int NR, int RECON>
-static int solve_group(mgt_wilson_s *h, const WilsonParams &P, const double2 *b, double2 *x, int64_t V, char *ws,
-                       const WSLayout &Lw, double tol, int max_iter, int64_t *report, double *relres,
-                       double *dot_out, cudaStream_t st) {
+static BiWS carve(char *q, const WSLayout &Lw) {
   BiWS w;
-  char *q = ws;
-  w.r = (double2 *)q; q += Lw.field;
-  w.rhat = (double2 *)q; q += Lw.field;
-  w.p = (double2 *)q; q += Lw.field;
-  w.v = (double2 *)q; q += Lw.field;
-  w.s = (double2 *)q; q += Lw.field;
-  w.t = (double2 *)q; q += Lw.field;
-  w.partials = (double *)q; q += Lw.partials;
-  w.ticket = (unsigned *)q; q += 256;
+  double2 **f[8] = {&w.r, &w.rhat, &w.p, &w.v, &w.s, &w.t, &w.x, &w.b};
+  for (auto *pp : f) {
+    *pp = (double2 *)q;
+    q += Lw.field;
+  }
+  w.partials = (double *)q;
+  q += Lw.partials;
+  w.ticket = (unsigned *)q;
+  q += 256;
   w.st = (BiState *)q;
+  return w;
+}
+
+// Graph cache: one instantiated graph of kChunk iterations per
+// (workspace, NR, RECON, operator variant).
+struct GraphKey {
+  const void *h, *ws;
+  int nr, recon, flags;
+  double tau;
+  bool operator<(const GraphKey &o) const {
+    return std::tie(h, ws, nr, recon, flags, tau) < std::tie(o.h, o.ws, o.nr, o.recon, o.flags, o.tau);
+  }
+};
+static std::mutex g_graph_mu;
+static std::map<GraphKey, cudaGraphExec_t> g_graphs;
+
+void drop_graphs(const void *h) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (auto it = g_graphs.begin(); it != g_graphs.end();) {
+    if (it->first.h == h) {
+      cudaGraphExecDestroy(it->second);
+      it = g_graphs.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+template <int NR, int RECON>
+static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &lf, const BiWS &w, int gd, int grid,
+                        cudaStream_t st) {
+  const int64_t V = P.g.V;
+  for (int it = 0; it < kChunk; ++it) {
+    bi_k1<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
+    bi_k2<NR><<<grid, kRedBlock, 0, st>>>(V, w);
+    bi_k3<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
+    bi_k4<NR><<<grid, kRedBlock, 0, st>>>(V, w);
+    bi_k5<NR><<<grid, kRedBlock, 0, st>>>(V, w);
+  }
+  return MGT_OK;
+}
+
+template <int NR, int RECON>
+static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b, double2 *x,
+                       char *ws, const WSLayout &Lw, double tol, int max_iter, int64_t *report, double *relres,
+                       double *dot_out, cudaStream_t st) {
+  const int64_t V = h->g.V;
+  BiWS w = carve(ws, Lw);
   LinkField<double, RECON> lf{reinterpret_cast<const double2 *>(h->links), V};
-  // resident grids (occupancy-derived), cached per template instance
-  static int g_dsl = 0, g_str = 0;
+  static int g_dsl = 0, g_str = 0;  // resident grids, per template instance
   if (!g_dsl) g_dsl = resident_grid(bi_k1<NR, RECON>, kRedBlock, (int64_t)1 << 40);
   if (!g_str) g_str = resident_grid(bi_k4<NR>, kRedBlock, (int64_t)1 << 40);
-  const int64_t need = (V * NR + kRedBlock - 1) / kRedBlock;
+  const int64_t need = (V + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
   const int gd = (int)std::min<int64_t>(g_dsl, need), grid = (int)std::min<int64_t>(g_str, need);
   MGT_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(unsigned), st));
-  bi_init<NR><<<grid, kRedBlock, 0, st>>>(V, b, x, w, tol, max_iter);
+  bi_init<NR><<<grid, kRedBlock, 0, st>>>(V, b, w, tol, max_iter);
   MGT_LAUNCH_CHECK("bi_init");
-  int *flags = h->host_flags;
-  int chunk = 4;
-  for (int round = 0; round < 1000000; ++round) {
-    for (int it = 0; it < chunk; ++it) {
-      bi_k1<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
-      bi_k2<NR><<<grid, kRedBlock, 0, st>>>(V, w);
-      bi_k3<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
-      bi_k4<NR><<<grid, kRedBlock, 0, st>>>(V, x, w);
-      bi_k5<NR><<<grid, kRedBlock, 0, st>>>(V, w);
-      note_launch(5);
+
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    GraphKey key{h, ws, NR, RECON, flags, tau};
+    auto it = g_graphs.find(key);
+    if (it != g_graphs.end()) {
+      exec = it->second;
+    } else {
+      cudaStream_t cap;
+      MGT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      cudaGraph_t graph;
+      MGT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      launch_chunk<NR, RECON>(P, lf, w, gd, grid, cap);
+      cudaError_t e = cudaStreamEndCapture(cap, &graph);
+      cudaStreamDestroy(cap);
+      if (e != cudaSuccess) return cuda_fail(e, "bicgstab graph capture");
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return cuda_fail(e, "bicgstab graph instantiate");
+      g_graphs[key] = exec;
     }
-    MGT_LAUNCH_CHECK("bicgstab iteration");
-    for (int r = 0; r < NR; ++r)
-      MGT_CUDA(cudaMemcpyAsync(flags + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+  // pinned per-thread mailbox: concurrent solves on several streams may share a handle
+  static thread_local int *hf = nullptr;
+  if (!hf) MGT_CUDA(cudaMallocHost((void **)&hf, 64 * sizeof(int)));
+  for (int round = 0; round < 1000000; ++round) {
+    MGT_CUDA(cudaGraphLaunch(exec, st));
+    note_launch(5 * kChunk);
+    MGT_CUDA(cudaMemcpyAsync(hf, &w.st[0].status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    for (int r = 1; r < NR; ++r)
+      MGT_CUDA(cudaMemcpyAsync(hf + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
     MGT_CUDA(cudaStreamSynchronize(st));
     bool running = false;
-    for (int r = 0; r < NR; ++r) running |= (flags[r] == ST_RUN);
-    if (running) {
-      chunk = std::min(chunk * 2, 16);
-      continue;
-    }
-    bi_resid<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, b, x, w);
+    for (int r = 0; r < NR; ++r) running |= (hf[r] == ST_RUN);
+    if (running) continue;
+    bi_resid<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
     bi_restart<NR><<<grid, kRedBlock, 0, st>>>(V, w);
     note_launch(2);
     MGT_LAUNCH_CHECK("bicgstab residual");
     for (int r = 0; r < NR; ++r)
-      MGT_CUDA(cudaMemcpyAsync(flags + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
+      MGT_CUDA(cudaMemcpyAsync(hf + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
     MGT_CUDA(cudaStreamSynchronize(st));
     bool again = false;
-    for (int r = 0; r < NR; ++r) again |= (flags[r] == ST_RUN);
+    for (int r = 0; r < NR; ++r) again |= (hf[r] == ST_RUN);
     if (!again) break;
-    chunk = 4;
   }
-  if (dot_out) {
-    bi_dot<NR><<<grid, kRedBlock, 0, st>>>(V, b, x, w);
-    MGT_LAUNCH_CHECK("bi_dot");
-  }
+  bi_final<NR><<<grid, kRedBlock, 0, st>>>(V, x, w);
+  MGT_LAUNCH_CHECK("bi_final");
   std::vector<BiState> hs(NR);
   MGT_CUDA(cudaMemcpyAsync(hs.data(), w.st, NR * sizeof(BiState), cudaMemcpyDeviceToHost, st));
   MGT_CUDA(cudaStreamSynchronize(st));
@@ -526,7 +581,7 @@ extern "C" {
 
 size_t mgt_bicgstab_workspace_bytes(mgt_wilson_t h, int n_rhs) {
   if (!h) return 0;
-  return ws_layout(h->g.V, 4).total;
+  return ws_layout(h->g.V).total;
 }
 
 int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau, double tol,
@@ -541,7 +596,7 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs
   cudaStream_t st = as_stream(stream);
   WilsonParams P = make_params(h, flags, tau);
   const int64_t V = h->g.V;
-  WSLayout Lw = ws_layout(V, 4);
+  WSLayout Lw = ws_layout(V);
   const size_t field = (size_t)12 * V;
   int r0 = 0;
   while (r0 < n_rhs) {
@@ -550,12 +605,12 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs
     const double2 *b = (const double2 *)b_dev + r0 * field;
     double2 *x = (double2 *)x_dev + r0 * field;
     double *dot = dot_out_host ? dot_out_host + 2 * r0 : nullptr;
-    int rc;
     char *ws = (char *)workspace_dev;
-#define MGT_SOLVE(NR)                                                                                        \
-  (h->recon == 18 ? solve_group<NR, 18>(h, P, b, x, V, ws, Lw, tol, max_iter, report_out + 4 * r0,           \
-                                         relres_out + r0, dot, st)                                            \
-                  : solve_group<NR, 12>(h, P, b, x, V, ws, Lw, tol, max_iter, report_out + 4 * r0,           \
+    int rc;
+#define MGT_SOLVE(NR)                                                                                           \
+  (h->recon == 18 ? solve_group<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
+                                         relres_out + r0, dot, st)                                               \
+                  : solve_group<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
                                          relres_out + r0, dot, st))
     if (nr == 4)
       rc = MGT_SOLVE(4);

@@ -48,6 +48,9 @@ inline WilsonParams make_params(const mgt_wilson_s *h, int flags, double tau) {
 }
 
 // launch y = op(x) for n_rhs native fields (defined in wilson.cu)
+// forget cached solver graphs of a handle (bicgstab.cu)
+void drop_graphs(const void *h);
+
 int wilson_apply_native(const mgt_wilson_s *h, const void *x, void *y, int n_rhs, int flags,
                         double tau, cudaStream_t st);
 

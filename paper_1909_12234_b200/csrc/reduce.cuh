@@ -15,31 +15,33 @@ namespace mgt {
 constexpr int kRedBlock = 128;  // threads per block in reducing kernels
 constexpr int kRedWarps = kRedBlock / 32;
 
-// Sum `v[NV]` over the threads of the block that share the same rhs slot
-// (rhs = lane % NR) and publish NR*NV partials for this block.  Returns true
-// in every thread of the LAST block to arrive, after which `partials` holds
-// all blocks' values.
+// Multi-rhs kernels map warp w of a block to rhs w % NR (see RhsMap), so a
+// warp's threads all belong to one rhs.  Sum `v[NV]` over each warp, combine
+// the warps of the same rhs in fixed order and publish NR*NV partials for
+// this block.  Returns true in every thread of the LAST block to arrive,
+// after which `partials` holds all blocks' values.
 template <int NR, int NV>
 __device__ __forceinline__ bool reduce_publish(double (&v)[NV], double *partials, unsigned *ticket) {
-  __shared__ double sm[kRedWarps][NR * NV];
+  __shared__ double sm[kRedWarps][NV];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     double x = v[k];
 #pragma unroll
-    for (int off = 16; off >= NR; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
     v[k] = x;
   }
-  if (lane < NR) {
+  if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) sm[warp][lane * NV + k] = v[k];
+    for (int k = 0; k < NV; ++k) sm[warp][k] = v[k];
   }
   __syncthreads();
   if (threadIdx.x < NR * NV) {
+    const int r = threadIdx.x / NV, k = threadIdx.x % NV;
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < kRedWarps; ++w) s += sm[w][threadIdx.x];
+    for (int w = r; w < kRedWarps; w += NR) s += sm[w][k];
     partials[(size_t)blockIdx.x * NR * NV + threadIdx.x] = s;
   }
   __threadfence();
@@ -51,6 +53,22 @@ __device__ __forceinline__ bool reduce_publish(double (&v)[NV], double *partials
   __syncthreads();
   return last;
 }
+
+// Thread -> (rhs, ordered site) map of the multi-rhs kernels: each block
+// iteration covers SPB = 128 / NR consecutive ordered sites; warp w serves
+// rhs w % NR on 32 of them.  Every load instruction streams one field.
+template <int NR>
+struct RhsMap {
+  static constexpr int SPB = kRedBlock / NR;
+  int rhs, local;
+  __device__ __forceinline__ RhsMap() {
+    const int w = threadIdx.x >> 5;
+    rhs = w % NR;
+    local = (w / NR) * 32 + (threadIdx.x & 31);
+  }
+  __device__ __forceinline__ int64_t first() const { return blockIdx.x * (int64_t)SPB + local; }
+  __device__ __forceinline__ int64_t stride() const { return (int64_t)gridDim.x * SPB; }
+};
 
 // In the last block: out[j] = sum_b partials[b*M + j] for j < M (fixed
 // order), then reset the ticket.  Result visible to the whole block.

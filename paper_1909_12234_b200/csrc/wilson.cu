@@ -52,11 +52,15 @@ __global__ void links_from_ref_kernel(Geom g, const double2 *__restrict__ ref, c
 template <typename R, int RECON, int NR>
 __global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4)) wilson_apply_kernel(WilsonParams P, const cplx<R> *__restrict__ in,
                                                            cplx<R> *__restrict__ out, LinkField<R, RECON> links) {
-  const int64_t n = P.g.V * NR;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t site = sched_site(P.sched, idx / NR);
-    const int rhs = (int)(idx % NR);
+  // warp w of the block serves rhs w % NR on 32 consecutive sites: every load
+  // instruction streams one field (like NR = 1) and the NR warps of a site
+  // group share its links through L1.
+  constexpr int SPB = 128 / NR;  // sites per block iteration
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rhs = w % NR;
+  const int local = (w / NR) * 32 + lane;
+  for (int64_t o = blockIdx.x * (int64_t)SPB + local; o < P.g.V; o += (int64_t)gridDim.x * SPB) {
+    const int64_t site = sched_site(P.sched, o);
     const cplx<R> *inr = in + (int64_t)rhs * 12 * P.g.V;
     cplx<R> *outr = out + (int64_t)rhs * 12 * P.g.V;
     C<R> y[4][3], xc[4][3];
@@ -220,6 +224,7 @@ int mgt_wilson_create(mgt_wilson_t *out, const int dims[4], int antiperiodic, do
 
 int mgt_wilson_destroy(mgt_wilson_t h) {
   if (!h) return MGT_OK;
+  drop_graphs(h);
   cudaFree(h->links);
   cudaFreeHost(h->host_flags);
   delete h;

@@ -15,6 +15,7 @@ finding 6).
 """
 
 import ctypes as ct
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -95,14 +96,18 @@ class BiCGStab:
 
 
 _SOLVERS = {}
+_SOLVERS_LOCK = threading.Lock()
 
 
 def _solver_for(op):
-    key = id(op)
-    s = _SOLVERS.get(key)
-    if s is None or s[0] is not op:
-        s = (op, BiCGStab(op))
-        _SOLVERS[key] = s
+    """One solver (device workspace) per (operator, host thread): concurrent
+    solves on several streams never share a workspace."""
+    key = (id(op), threading.get_ident())
+    with _SOLVERS_LOCK:
+        s = _SOLVERS.get(key)
+        if s is None or s[0] is not op:
+            s = (op, BiCGStab(op))
+            _SOLVERS[key] = s
     return s[1]
 
 

@@ -58,63 +58,27 @@ class BlockingScheme:
 # GCR relaxation on the GPU (krylov.py:52-118 semantics)
 
 
-def _vdot(a, b):
-    return torch.vdot(a.reshape(-1), b.reshape(-1))
+_GCR_WS = {}
 
 
 def gcr_relax(op, b, tol, max_iter, restart):
-    """Restarted GCR from x0 = 0 on native fields (1, 12, V); returns
+    """Restarted GCR from x0 = 0 (C ABI `mgt_gcr_solve`, krylov.py:52-118
+    semantics) on a native field (1, 12, V); returns
     (x, iterations, converged, reason, matvecs)."""
-    bn = torch.linalg.vector_norm(b).item()
-    if bn == 0.0:
-        return torch.zeros_like(b), 0, True, "", 0
-    x = torch.zeros_like(b)
-    r = b.clone()
-    nmv = 0
-    Z, Q = [], []
-    it = 0
-    rel = 1.0
-    why = "max_iter"
-    while it < max_iter:
-        if rel <= tol:
-            r = b - op.apply_native(x)
-            nmv += 1
-            rel = torch.linalg.vector_norm(r).item() / bn
-            if rel <= tol:
-                return x, it, True, "", nmv
-            Z, Q = [], []
-        z = r.clone()
-        q = op.apply_native(z)
-        nmv += 1
-        q0 = torch.linalg.vector_norm(q).item()
-        for zj, qj in zip(Z, Q):
-            c = _vdot(qj, q)
-            q = q - c * qj
-            z = z - c * zj
-        qn = torch.linalg.vector_norm(q).item()
-        if qn <= 1e-14 * max(q0, 1e-300):
-            why = "breakdown"
-            break
-        q = q / qn
-        z = z / qn
-        a = _vdot(q, r)
-        x = x + a * z
-        r = r - a * q
-        Z.append(z)
-        Q.append(q)
-        it += 1
-        rel = torch.linalg.vector_norm(r).item() / bn
-        if len(Z) >= restart:
-            Z, Q = [], []
-            r = b - op.apply_native(x)
-            nmv += 1
-            rel = torch.linalg.vector_norm(r).item() / bn
-    r = b - op.apply_native(x)
-    nmv += 1
-    rel = torch.linalg.vector_norm(r).item() / bn
-    if rel <= tol:
-        return x, it, True, "", nmv
-    return x, it, False, why, nmv
+    import ctypes as ct
+    key = (id(op), restart)
+    ws = _GCR_WS.get(key)
+    if ws is None or ws[0] is not op:
+        nbytes = _lib.lib().mgt_gcr_workspace_bytes(op.handle, int(restart))
+        ws = (op, torch.empty(int(nbytes), dtype=torch.uint8, device=device()))
+        _GCR_WS[key] = ws
+    x = torch.empty_like(b)
+    rep = (ct.c_int64 * 4)()
+    rel = (ct.c_double * 1)()
+    _lib.check(_lib.lib().mgt_gcr_solve(op.handle, ptr(b.contiguous()), ptr(x), int(restart), int(max_iter),
+                                         float(tol), ptr(ws[1]), rep, rel, stream_ptr()), "gcr")
+    it, mv, conv, reason = (int(v) for v in rep)
+    return x, it, bool(conv), ("" if conv else ("breakdown" if reason == 2 else "max_iter")), mv
 
 
 @dataclass

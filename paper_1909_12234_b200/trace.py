@@ -10,6 +10,7 @@ Samples are then reduced on the host in the reference's slot order, so the
 mean/variance/jackknife arithmetic is identical to the reference's.
 """
 
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -81,7 +82,64 @@ def _warn_flagged(flagged):
         warnings.warn(f"{int(flagged.sum())} sample(s) used non-converged solves (kept with TSM semantics)")
 
 
-def group_samples_gpu(inv_op, probes, batch=4, correction=None):
+def _solve_batches_concurrently(inv_op, probes, batches, correction, streams):
+    """Solve probe batches (4 rhs each) on `streams` CUDA streams from host
+    worker threads: at small volumes one multi-rhs solve cannot fill 148 SMs,
+    several independent ones can.  Returns [(reports, q)] in batch order;
+    every result is a pure function of its probes (bitwise reproducible)."""
+    import torch
+
+    from .krylov import _solver_for
+
+    def work(j0, j1, stream):
+        with torch.cuda.stream(stream):
+            z = probes.noise_native(j0, j1)
+            solver = _solver_for(inv_op.op)
+            x, reps, q = solver.solve_native(z, inv_op.config.tol, inv_op.config.max_iter, want_dot=True)
+            if correction is not None:
+                q = q - correction(j0, z, x)
+            stream.synchronize()
+        return reps, q
+
+    n = max(1, min(streams, len(batches)))
+    if n == 1:
+        return [work(j0, j1, torch.cuda.current_stream()) for j0, j1 in batches]
+    torch.cuda.current_stream().synchronize()  # shared inputs (deflation factors) are ready
+    dev = torch.cuda.current_device()
+    pool, local = _worker_pool(n)
+
+    def run(j0, j1):
+        if getattr(local, "device", None) != dev:  # one stream per worker thread and device
+            torch.cuda.set_device(dev)
+            local.device = dev
+            local.stream = torch.cuda.Stream()
+        return work(j0, j1, local.stream)
+
+    futs = [pool.submit(run, j0, j1) for j0, j1 in batches]
+    return [f.result() for f in futs]
+
+
+_POOL = {}
+
+
+def _worker_pool(n):
+    """Process-wide worker threads (stable identities, so their solver
+    workspaces and cached solver graphs are reused across calls)."""
+    import concurrent.futures as cf
+    if n not in _POOL:
+        _POOL[n] = (cf.ThreadPoolExecutor(max_workers=n, thread_name_prefix="mgt-solve"), threading.local())
+    return _POOL[n]
+
+
+def default_streams(volume, batch=4):
+    """Concurrent multi-rhs solves needed to fill the GPU: one 4-rhs solve of
+    V sites exposes 4V dslash threads; ~2 resident waves of 148 SMs x 384
+    threads keep the memory system busy.  More streams only add contention."""
+    want = 2 * 148 * 384
+    return int(max(1, min(8, -(-want // (batch * volume)))))
+
+
+def group_samples_gpu(inv_op, probes, batch=4, correction=None, streams=None):
     """Per-group samples sum_slots w * vdot(slot, A^-1 slot) with the solves
     batched on the GPU; `correction(j, slots_native, x_native)` may return a
     per-slot complex array subtracted from the quadratic forms (deflation).
@@ -91,12 +149,13 @@ def group_samples_gpu(inv_op, probes, batch=4, correction=None):
     flagged = np.zeros(ns, dtype=bool)
     w = probes.weights()
     if probes.slots_per_group == 1:
-        for j0 in range(0, ns, batch):
-            j1 = min(ns, j0 + batch)
-            z = probes.noise_native(j0, j1)
-            x, reps, q = inv_op.solve_native(z, want_dot=True)
-            if correction is not None:
-                q = q - correction(j0, z, x)
+        batches = [(j0, min(ns, j0 + batch)) for j0 in range(0, ns, batch)]
+        if streams is None:
+            streams = default_streams(probes.geometry.site_count, batch)
+        results = _solve_batches_concurrently(inv_op, probes, batches, correction, streams)
+        for (j0, j1), (reps, q) in zip(batches, results):
+            for rep in reps:  # counters in probe order, as the reference's
+                inv_op._account(rep)
             for k, j in enumerate(range(j0, j1)):
                 acc = 0.0 + 0.0j
                 acc = acc + w[0] * q[k]
