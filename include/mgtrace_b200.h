@@ -90,6 +90,29 @@ int mgt_wilson_info(mgt_wilson_t h, int dims[4], int *prec, int *recon,
 int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs,
                      int flags, double tau, void *stream);
 
+/* ---- t-slab decomposition (multi-GPU) ------------------ */
+/* The reference is single-process.  A slab handle owns
+ * global t in [t_begin, t_begin + dims_local[3]) of T_global (>= 2 slices);
+ * links: the slab's own links in the reference layout of the LOCAL dims.
+ * mgt_halo_pack writes the two faces this rank sends (n_rhs x 6 x S3
+ * complex, S3 = L0*L1*L2): to_prev = (1 - g4) z of the first slice,
+ * to_next = U_4^dag (1 + g4) z of the last slice (z = G_in x).
+ * mgt_wilson_apply_slab applies the operator with the faces received from
+ * rank+1 (halo_next) and rank-1 (halo_prev); part 0 = all sites, 1 = interior
+ * slices only (no halo needed; overlaps the exchange), 2 = the two boundary
+ * slices.  The plain mgt_wilson_apply rejects slab handles. */
+int mgt_wilson_create_slab(mgt_wilson_t *out, const int dims_local[4],
+                           int t_begin, int T_global, int antiperiodic,
+                           double mass, int prec, int recon,
+                           const void *links_ref_local_dev, void *stream);
+int mgt_halo_pack(mgt_wilson_t h, const void *x_dev, void *to_prev_dev,
+                  void *to_next_dev, int n_rhs, int flags, double tau,
+                  void *stream);
+int mgt_wilson_apply_slab(mgt_wilson_t h, const void *x_dev, void *y_dev,
+                          const void *halo_next_dev, const void *halo_prev_dev,
+                          int n_rhs, int flags, double tau, int part,
+                          void *stream);
+
 /* ---- BLAS-1 on native fields (fp64) -------------------------------------- */
 /* out[r] = sum_i conj(a_i) b_i for each of n_rhs fields of `len` complex
  * entries (deterministic fixed-order reduction; numpy vdot semantics). */

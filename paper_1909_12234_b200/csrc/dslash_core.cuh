@@ -150,17 +150,71 @@ struct WilsonParams {
   Geom g;
   Sched sched;
   int antiperiodic;
+  // t-slab decomposition: this operator owns global t in [t_begin, t_begin + L3)
+  // of T_global; with slab != 0 the t hops that leave the slab read the
+  // neighbours' pre-projected faces (6 complex per spatial site and rhs):
+  //   halo_next: (1 - g_4) projection of rank+1's first slice,
+  //   halo_prev: U_4^dag (1 + g_4) projection of rank-1's last slice.
+  int slab, t_begin, T_global;
+  const void *halo_next, *halo_prev;
   double diag_up_re, diag_up_im;  // (4 + m0) + i tau   acting on spins 0,1
   double diag_dn_re, diag_dn_im;  // (4 + m0) - i tau   acting on spins 2,3
   double g5in, g5out;             // +1 or -1
 };
+
+// t hops across a slab boundary, from the received faces (gamma_4: B = I).
+template <bool FWD, typename R, int RECON>
+__device__ __forceinline__ void wilson_thop_halo(const WilsonParams &P, const LinkField<R, RECON> &links,
+                                                 int64_t site, const int (&x)[4], int rhs, C<R> (&acc)[4][3]) {
+  const int64_t S3 = P.g.stride[3];
+  const int64_t s = site - (int64_t)x[3] * S3;
+  const cplx<R> *hb = reinterpret_cast<const cplx<R> *>(FWD ? P.halo_next : P.halo_prev) + (int64_t)rhs * 6 * S3 + s;
+  const int tg = P.t_begin + x[3];
+  const R ph = (P.antiperiodic && (FWD ? tg == P.T_global - 1 : tg == 0)) ? R(-1) : R(1);
+  C<R> w[2][3];
+  if constexpr (FWD) {
+    C<R> h[2][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) h[a][c] = ldc(hb + (a * 3 + c) * S3);
+    C<R> u[3][3];
+    links.load(3, site, u);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        C<R> t(R(0), R(0));
+#pragma unroll
+        for (int j = 0; j < 3; ++j) t = cfma(u[i][j], h[a][j], t);
+        w[a][i] = ph * t;
+      }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[a][c] = ph * ldc(hb + (a * 3 + c) * S3);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    acc[0][i] = acc[0][i] + w[0][i];
+    acc[1][i] = acc[1][i] + w[1][i];
+    if constexpr (FWD) {
+      acc[2][i] = acc[2][i] - w[0][i];
+      acc[3][i] = acc[3][i] - w[1][i];
+    } else {
+      acc[2][i] = acc[2][i] + w[0][i];
+      acc[3][i] = acc[3][i] + w[1][i];
+    }
+  }
+}
 
 // y = G_out [ diag z - 1/2 hop(z) ],  z = G_in x.  Also returns the raw input
 // x at the site (xc, before G_in) for fused epilogues.
 template <typename R, int RECON>
 __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R> *__restrict__ in,
                                             const LinkField<R, RECON> &links, int64_t site,
-                                            C<R> (&y)[4][3], C<R> (&xc)[4][3]) {
+                                            C<R> (&y)[4][3], C<R> (&xc)[4][3], int rhs = 0) {
   int x[4];
   native_coords(P.g, site, x);
   const R g5in = (R)P.g5in;
@@ -174,9 +228,15 @@ __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R>
   // thread) and spill; one hop's 21 independent 16-byte loads in flight per
   // thread is already ~4x the bytes-in-flight HBM needs at this occupancy.
 #define MGT_HOP_FENCE asm volatile("" ::: "memory")
-  wilson_hop<3, true>(P.g, in, links, site, x, g5in, ap, acc);
+  if (P.slab && x[3] == P.g.L[3] - 1)
+    wilson_thop_halo<true>(P, links, site, x, rhs, acc);
+  else
+    wilson_hop<3, true>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
-  wilson_hop<3, false>(P.g, in, links, site, x, g5in, ap, acc);
+  if (P.slab && x[3] == 0)
+    wilson_thop_halo<false>(P, links, site, x, rhs, acc);
+  else
+    wilson_hop<3, false>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
   wilson_hop<0, true>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;

@@ -20,6 +20,8 @@ struct mgt_wilson_s {
   size_t link_bytes;
   // pinned host mailbox for solver convergence flags
   int *host_flags;
+  // t-slab decomposition: this handle owns global t in [t_begin, t_begin+L3)
+  int slab, t_begin, T_global;
 };
 
 namespace mgt {
@@ -44,12 +46,18 @@ inline WilsonParams make_params(const mgt_wilson_s *h, int flags, double tau) {
   P.diag_dn_im = -t;
   P.g5in = g5in;
   P.g5out = g5out;
+  P.slab = 0;  // a slab handle turns this on per apply, with its halo buffers
+  P.t_begin = h->t_begin;
+  P.T_global = h->T_global;
+  P.halo_next = nullptr;
+  P.halo_prev = nullptr;
   return P;
 }
 
-// launch y = op(x) for n_rhs native fields (defined in wilson.cu)
 // forget cached solver graphs of a handle (bicgstab.cu)
 void drop_graphs(const void *h);
+
+// launch y = op(x) for n_rhs native fields (defined in wilson.cu)
 
 int wilson_apply_native(const mgt_wilson_s *h, const void *x, void *y, int n_rhs, int flags,
                         double tau, cudaStream_t st);

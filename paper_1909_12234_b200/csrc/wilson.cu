@@ -182,6 +182,9 @@ int mgt_wilson_create(mgt_wilson_t *out, const int dims[4], int antiperiodic, do
   h->mass = mass;
   h->prec = prec;
   h->recon = recon;
+  h->slab = 0;
+  h->t_begin = 0;
+  h->T_global = dims[3];
   h->variant = 0;
   if (const char *v = getenv("MGT_DSLASH_VARIANT")) h->variant = atoi(v);
   h->slab_bytes = (int64_t)32 << 20;
@@ -246,6 +249,7 @@ int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs, 
   if (!h || !x_dev || !y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply: null argument");
   if (n_rhs < 1) return fail(MGT_ERR_INVALID, "n_rhs must be >= 1");
   if (x_dev == y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply: in-place apply is not supported");
+  if (h->slab) return fail(MGT_ERR_INVALID, "mgt_wilson_apply: slab handles apply through mgt_wilson_apply_slab");
   return wilson_apply_native(h, x_dev, y_dev, n_rhs, flags, tau, as_stream(stream));
 }
 

@@ -345,6 +345,16 @@ class CoarseOperator:
             D[rows, :, nbr[:, d], :] = D[rows, :, nbr[:, d], :] + blocks[:, d]
         return D.reshape(nb * nc, nb * nc)
 
+    def dense_inverse_native(self):
+        """C^-1 (native coarse order) by a dense fp64 LU on the device; built
+        once and cached (setup of the full-prolongator deflation: Nc = 12,288
+        at 16^4 is 2.4 GB)."""
+        if getattr(self, "_dinv", None) is None:
+            D = self.dense_native()
+            self._dinv = torch.linalg.inv(D)
+            del D
+        return self._dinv
+
     def dense(self):
         """Dense matrix in the reference coarse order (host numpy)."""
         pr = self.prolongator

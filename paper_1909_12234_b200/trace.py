@@ -271,9 +271,7 @@ def _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op):
     import torch
     from .multigrid import build_coarse_operator
     coarse = coarse_op if coarse_op is not None else build_coarse_operator(op, prolongator)
-    D = coarse.dense_native()
-    Dinv = torch.linalg.inv(D)  # dense fp64 LU on the device (setup; Nc x Nc)
-    del D
+    Dinv = coarse.dense_inverse_native()  # setup, cached on the coarse operator
     t0 = complex(torch.diagonal(Dinv).sum().item())
     Nc = prolongator.coarse_dim
 
