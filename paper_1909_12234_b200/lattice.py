@@ -97,9 +97,12 @@ class WilsonOperator:
     (reference protocol: lattice.py:194-263).  Immutable after construction;
     concurrent applies on different streams are safe."""
 
-    def __init__(self, gauge, mass, prec=64, recon=18):
+    def __init__(self, gauge, mass, prec=64, recon="auto"):
         geometry = gauge.geometry
         _check4d(geometry)
+        if recon == "auto":
+            # two-row storage + unitarity reconstruction is exact only for SU(3)
+            recon = 12 if getattr(gauge, "kind", "") in ("su3", "unit") else 18
         self.geometry = geometry
         self.gauge = gauge
         self.mass = float(mass)
@@ -284,6 +287,8 @@ class FormOperator:
         return self.op.apply_native(x, out=out, flags=self.flags, tau=self.tau)
 
 
-def build_wilson(gauge, mass, prec=64, recon=18):
-    """Assemble the GPU 4D Wilson operator (reference: lattice.py:274-318)."""
+def build_wilson(gauge, mass, prec=64, recon="auto"):
+    """Assemble the GPU 4D Wilson operator (reference: lattice.py:274-318).
+    recon 'auto': 12-real link storage for generated SU(3) fields, full 18
+    reals for arbitrary user arrays."""
     return WilsonOperator(gauge, mass, prec=prec, recon=recon)

@@ -135,43 +135,59 @@ def default_streams(volume, batch=4):
     """Concurrent multi-rhs solves needed to fill the GPU: one 4-rhs solve of
     V sites exposes 4V dslash threads; ~2 resident waves of 148 SMs x 384
     threads keep the memory system busy.  More streams only add contention."""
+    import os
+    if os.environ.get("MGT_SOLVE_STREAMS"):
+        return max(1, int(os.environ["MGT_SOLVE_STREAMS"]))
     want = 2 * 148 * 384
     return int(max(1, min(8, -(-want // (batch * volume)))))
 
 
-def group_samples_gpu(inv_op, probes, batch=4, correction=None, streams=None):
+def group_samples_gpu(inv_op, probes, batch=4, correction=None, streams=None, deferred=None):
     """Per-group samples sum_slots w * vdot(slot, A^-1 slot) with the solves
     batched on the GPU; `correction(j, slots_native, x_native)` may return a
     per-slot complex array subtracted from the quadratic forms (deflation).
-    Returns (samples, flagged)."""
+    `deferred = (collect, finish)` instead calls collect(j, slots, x) per
+    batch and finish() once -> per-slot corrections in slot order (one large
+    product instead of one per batch).  The samples are accumulated exactly
+    as the reference's slot loop (trace.py:100-107).  Returns (samples,
+    flagged)."""
     ns = probes.sample_count
-    samples = np.empty(ns, dtype=np.complex128)
     flagged = np.zeros(ns, dtype=bool)
     w = probes.weights()
+    per_group = []  # (reports, q) per group, q per slot
+    if deferred is not None:
+        correction = lambda j0, z, x: deferred[0](j0, z, x) or 0.0  # noqa: E731
     if probes.slots_per_group == 1:
         batches = [(j0, min(ns, j0 + batch)) for j0 in range(0, ns, batch)]
         if streams is None:
             streams = default_streams(probes.geometry.site_count, batch)
         results = _solve_batches_concurrently(inv_op, probes, batches, correction, streams)
         for (j0, j1), (reps, q) in zip(batches, results):
-            for rep in reps:  # counters in probe order, as the reference's
-                inv_op._account(rep)
-            for k, j in enumerate(range(j0, j1)):
-                acc = 0.0 + 0.0j
-                acc = acc + w[0] * q[k]
-                samples[j] = acc
-                flagged[j] = not reps[k].converged
+            for k in range(j1 - j0):
+                per_group.append(([reps[k]], np.atleast_1d(q[k])))
     else:
         for j in range(ns):
             z = probes.slots_native(j)
             x, reps, q = inv_op.solve_native(z, want_dot=True)
             if correction is not None:
                 q = q - correction(j, z, x)
-            acc = 0.0 + 0.0j
-            for k in range(len(w)):
-                acc = acc + w[k] * q[k]
-            samples[j] = acc
-            flagged[j] = not all(r.converged for r in reps)
+            per_group.append((reps, q))
+    if deferred is not None:
+        corr = deferred[1]()
+        pos = 0
+        for g, (reps, q) in enumerate(per_group):
+            per_group[g] = (reps, q - corr[pos:pos + len(q)])
+            pos += len(q)
+    samples = np.empty(ns, dtype=np.complex128)
+    for j, (reps, q) in enumerate(per_group):
+        if probes.slots_per_group == 1:
+            for rep in reps:  # counters in probe order, as the reference's
+                inv_op._account(rep)
+        acc = 0.0 + 0.0j
+        for k in range(len(w)):
+            acc = acc + w[k] * q[k]
+        samples[j] = acc
+        flagged[j] = not all(r.converged for r in reps)
     return samples, flagged
 
 
@@ -274,13 +290,19 @@ def _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op):
     Dinv = coarse.dense_inverse_native()  # setup, cached on the coarse operator
     t0 = complex(torch.diagonal(Dinv).sum().item())
     Nc = prolongator.coarse_dim
+    store = {}
 
-    def correction(j0, z, x):
-        h = prolongator.restrict_native(z).reshape(z.shape[0], Nc)
-        ch = h @ Dinv.transpose(0, 1)  # rows: (C^-1 h_j)^T
-        return torch.sum(h.conj() * ch, dim=1).cpu().numpy()
+    def restrict(j0, z, x):  # per batch: keep P^H z (Nc complex per probe)
+        store[j0] = prolongator.restrict_native(z).reshape(z.shape[0], Nc)
 
-    return t0, correction
+    def corrections():
+        # one (s x Nc) x (Nc x Nc) product for all probes: C^-1 is read once
+        keys = sorted(store)
+        H = torch.cat([store[k] for k in keys])
+        CH = H @ Dinv.transpose(0, 1)
+        return torch.sum(H.conj() * CH, dim=1).cpu().numpy()
+
+    return t0, (restrict, corrections)
 
 
 def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probes, coarse_op=None):
@@ -300,7 +322,7 @@ def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probe
         if rank != prolongator.coarse_dim:
             raise ValueError("identity coarse triplets need rank = Nc")
         t0, corr = _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op)
-        samples, flagged = group_samples_gpu(inv_op, probes, correction=corr)
+        samples, flagged = group_samples_gpu(inv_op, probes, deferred=corr)
         _warn_flagged(flagged)
         return finish(t0, samples, inv_op.n_solves - before, flagged)
     if rank > coarse_triplets.count:
