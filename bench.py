@@ -87,6 +87,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def committed_traffic(dims, prec, recon, n_rhs=1):
+    """DRAM bytes per launch of the headline kernel from the committed ncu
+    capture (profiles/*_dslash_traffic.json) when it matches the config."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_dslash_traffic.json"))):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        if (d.get("lattice"), d.get("prec"), d.get("recon"), d.get("n_rhs")) == (dims, prec, recon, n_rhs):
+            best = d["dram_bytes_read"] + d["dram_bytes_write"]
+    return best
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -271,7 +286,9 @@ def run_ours(args):
                                        f"{dims[3] * world}, {dims[3]} slices per GPU, NCCL halo exchange "
                                        "overlapped with the interior" if world > 1 else "single")},
             "roofline": {"bound": "hbm", "achieved": kernel_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": kernel_gbs / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": kernel_gbs / peak,
+                         "traffic": committed_traffic(args.dims, args.prec, args.recon) if world == 1 else None,
+                         "traffic_unit": "bytes per launch (ncu dram read+write)", "peak_kind": peak_kind,
                          "bytes_per_site": bytes_per_site},
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": V * 12 * 16,
                     "d2h_bytes_per_step": V * 12 * 16},
