@@ -40,6 +40,7 @@ struct BiWS {
   double2 *r, *rhat, *p, *v, *s, *t, *x, *b;
   double *partials;
   unsigned *ticket;
+  unsigned long long *ctr;  // dynamic chunk counter (dslash kernels), reset by their last block
   BiState *st;
 };
 
@@ -60,6 +61,15 @@ __device__ __forceinline__ double cabs2(C<double> a) { return a.re * a.re + a.im
 __device__ __forceinline__ bool cfinite(C<double> a) { return isfinite(a.re) && isfinite(a.im); }
 
 #define MGT_SITE_LOOP(M, V) for (int64_t o = (M).first(); o < (V); o += (M).stride())
+
+// Dynamically scheduled loop over chunks of RhsMap<NR>::SPB ordered sites
+// (next_chunk): every thread of the block iterates (the body must not
+// return/break early); `o` is the thread's ordered site (may be >= V in the
+// last chunk), `chunk` the chunk index; NCH receives the number of chunks.
+#define MGT_DYN_LOOP(M, V, CTR, NCH)                                                  \
+  NCH = ((V) + (M).SPB - 1) / (M).SPB;                                                \
+  for (int64_t chunk = next_chunk(CTR), o = chunk * (M).SPB + (M).local; chunk < NCH; \
+       chunk = next_chunk(CTR), o = chunk * (M).SPB + (M).local)
 
 // ---------------------------------------------------------------------------
 // init: b -> workspace, r = rhat = p = b, x = 0, |b|^2
@@ -116,10 +126,11 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
   const int64_t V = P.g.V;
-  double acc[2] = {0.0, 0.0};
-  if (run_me) {
-    const int64_t off = (int64_t)m.rhs * 12 * V;
-    MGT_SITE_LOOP(m, V) {
+  const int64_t off = (int64_t)m.rhs * 12 * V;
+  int64_t nchunks = 0;
+  MGT_DYN_LOOP(m, V, w.ctr, nchunks) {
+    double acc[2] = {0.0, 0.0};
+    if (run_me && o < V) {
       const int64_t site = sched_site(P.sched, o);
       C<double> y[4][3], xc[4][3];
       wilson_eval<double, RECON>(P, w.p + off, L, site, y, xc);
@@ -134,10 +145,12 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<
           acc[1] += rh.re * y[a][c].im - rh.im * y[a][c].re;
         }
     }
+    chunk_publish<NR, 2>(acc, w.partials + chunk * NR * 2);
   }
-  if (reduce_publish<NR, 2>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR * 2];
-    reduce_finish<NR * 2>(w.partials, w.ticket, out);
+    reduce_finish_n<NR * 2>(w.partials, nchunks, w.ticket, out);
+    if (threadIdx.x == 0) *w.ctr = 0ull;
     const int r = threadIdx.x;
     if (r < NR && w.st[r].status == ST_RUN) {
       BiState &s = w.st[r];
@@ -192,10 +205,11 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
   const int64_t V = P.g.V;
-  double acc[3] = {0.0, 0.0, 0.0};
-  if (run_me) {
-    const int64_t off = (int64_t)m.rhs * 12 * V;
-    MGT_SITE_LOOP(m, V) {
+  const int64_t off = (int64_t)m.rhs * 12 * V;
+  int64_t nchunks = 0;
+  MGT_DYN_LOOP(m, V, w.ctr, nchunks) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    if (run_me && o < V) {
       const int64_t site = sched_site(P.sched, o);
       C<double> y[4][3], xc[4][3];
       wilson_eval<double, RECON>(P, w.s + off, L, site, y, xc);
@@ -210,10 +224,12 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<
           acc[2] += cabs2(tt);
         }
     }
+    chunk_publish<NR, 3>(acc, w.partials + chunk * NR * 3);
   }
-  if (reduce_publish<NR, 3>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR * 3];
-    reduce_finish<NR * 3>(w.partials, w.ticket, out);
+    reduce_finish_n<NR * 3>(w.partials, nchunks, w.ticket, out);
+    if (threadIdx.x == 0) *w.ctr = 0ull;
     const int r = threadIdx.x;
     if (r < NR && w.st[r].status == ST_RUN) {
       BiState &s = w.st[r];
@@ -314,10 +330,11 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
   const int st_me = w.st[m.rhs].status;
   const bool act_me = (st_me == ST_CONV || st_me == ST_MAXIT || st_me == ST_BREAK);
   const int64_t V = P.g.V;
-  double acc[1] = {0.0};
-  if (act_me) {
-    const int64_t off = (int64_t)m.rhs * 12 * V;
-    MGT_SITE_LOOP(m, V) {
+  const int64_t off = (int64_t)m.rhs * 12 * V;
+  int64_t nchunks = 0;
+  MGT_DYN_LOOP(m, V, w.ctr, nchunks) {
+    double acc[1] = {0.0};
+    if (act_me && o < V) {
       const int64_t site = sched_site(P.sched, o);
       C<double> y[4][3], xc[4][3];
       wilson_eval<double, RECON>(P, w.x + off, L, site, y, xc);
@@ -331,10 +348,12 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
           acc[0] += cabs2(rr);
         }
     }
+    chunk_publish<NR, 1>(acc, w.partials + chunk * NR);
   }
-  if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR];
-    reduce_finish<NR>(w.partials, w.ticket, out);
+    reduce_finish_n<NR>(w.partials, nchunks, w.ticket, out);
+    if (threadIdx.x == 0) *w.ctr = 0ull;
     const int r = threadIdx.x;
     if (r < NR) {
       BiState &s = w.st[r];
@@ -429,7 +448,11 @@ struct WSLayout {
 static WSLayout ws_layout(int64_t V) {
   WSLayout L;
   L.field = align_up((size_t)kMaxGroup * 12 * V * sizeof(double2), 256);
-  L.partials = align_up((size_t)kNumSMs * 16 * kMaxGroup * 4 * sizeof(double), 256);
+  // static-grid kernels: one NR*NV slot per block; dynamic kernels: one per
+  // chunk of 128 / NR sites (NR = 4 is the largest)
+  const size_t per_block = (size_t)kNumSMs * 16 * kMaxGroup * 4;
+  const size_t per_chunk = (size_t)((V + 31) / 32) * kMaxGroup * 3;
+  L.partials = align_up(std::max(per_block, per_chunk) * sizeof(double), 256);
   L.total = 8 * L.field + L.partials + 256 /*ticket*/ + align_up(kMaxGroup * sizeof(BiState), 256);
   return L;
 }
@@ -444,6 +467,7 @@ static BiWS carve(char *q, const WSLayout &Lw) {
   w.partials = (double *)q;
   q += Lw.partials;
   w.ticket = (unsigned *)q;
+  w.ctr = (unsigned long long *)(q + 8);
   q += 256;
   w.st = (BiState *)q;
   return w;
@@ -500,7 +524,7 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
   if (!g_str) g_str = resident_grid(bi_k4<NR>, kRedBlock, (int64_t)1 << 40);
   const int64_t need = (V + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
   const int gd = (int)std::min<int64_t>(g_dsl, need), grid = (int)std::min<int64_t>(g_str, need);
-  MGT_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(unsigned), st));
+  MGT_CUDA(cudaMemsetAsync(w.ticket, 0, 16, st));  // ticket and chunk counter
   bi_init<NR><<<grid, kRedBlock, 0, st>>>(V, b, w, tol, max_iter);
   MGT_LAUNCH_CHECK("bi_init");
 

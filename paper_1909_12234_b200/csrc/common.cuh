@@ -163,6 +163,19 @@ __host__ __device__ __forceinline__ int64_t sched_site(const Sched &s, int64_t o
   return t * s.plane + k * s.slab_sites + r;
 }
 
+// Dynamic in-order chunk scheduler for persistent grids: CTAs take
+// consecutive chunks from a global counter, so the chunks in flight always
+// form one contiguous window of the schedule (a static grid-stride split
+// lets CTAs drift apart over hundreds of steps and the neighbour reuse
+// window no longer fits in L2).  Every thread of the block must call it.
+__device__ __forceinline__ int64_t next_chunk(unsigned long long *ctr) {
+  __shared__ long long c;
+  __syncthreads();
+  if (threadIdx.x == 0) c = (long long)atomicAdd(ctr, 1ull);
+  __syncthreads();
+  return c;
+}
+
 // Resident-grid size for a kernel (blocks per SM from the occupancy
 // calculator): grid-stride loops then march one contiguous window through the
 // schedule instead of scattering a block's iterations across the lattice.

@@ -1,5 +1,6 @@
 // The opaque Wilson operator handle shared by the operator / solver units.
 #pragma once
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -22,7 +23,23 @@ struct mgt_wilson_s {
   int *host_flags;
   // t-slab decomposition: this handle owns global t in [t_begin, t_begin+L3)
   int slab, t_begin, T_global;
+  // ring of chunk counters for the dynamic in-order scheduler (one slot per
+  // launch, so concurrent launches on different streams never share one)
+  unsigned long long *ctr_ring;
+  mutable std::atomic<unsigned> ctr_next;
+  int dyn_sched;
 };
+
+namespace mgt {
+constexpr unsigned kCtrRing = 4096;
+// a zeroed counter for the next launch on stream st
+inline unsigned long long *take_counter(const mgt_wilson_s *h, cudaStream_t st) {
+  if (!h->dyn_sched) return nullptr;
+  unsigned long long *c = h->ctr_ring + (h->ctr_next.fetch_add(1) % kCtrRing);
+  cudaMemsetAsync(c, 0, sizeof(unsigned long long), st);
+  return c;
+}
+}  // namespace mgt
 
 namespace mgt {
 

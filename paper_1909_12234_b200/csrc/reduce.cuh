@@ -54,6 +54,60 @@ __device__ __forceinline__ bool reduce_publish(double (&v)[NV], double *partials
   return last;
 }
 
+// Per-chunk variant for dynamically scheduled kernels (next_chunk): the
+// block reduces its chunk's values and writes them to dst[NR*NV] (the
+// chunk's own slot), so the final sum over chunks in chunk order does not
+// depend on which block processed which chunk.  All threads must call it.
+template <int NR, int NV>
+__device__ __forceinline__ void chunk_publish(const double (&v)[NV], double *dst) {
+  __shared__ double sm[kRedWarps][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    if (lane == 0) sm[warp][k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NR * NV) {
+    const int r = threadIdx.x / NV, k = threadIdx.x % NV;
+    double s = 0.0;
+#pragma unroll
+    for (int w = r; w < kRedWarps; w += NR) s += sm[w][k];
+    dst[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// Arrival ticket: true in every thread of the last block to arrive.
+__device__ __forceinline__ bool last_block(unsigned *ticket) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  return last;
+}
+
+// In the last block: out[j] = sum_c partials[c*M + j] over n chunks (fixed order).
+template <int M>
+__device__ __forceinline__ void reduce_finish_n(const double *partials, int64_t n, unsigned *ticket, double (&out)[M]) {
+  __shared__ double res[M > 0 ? M : 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < M; j += kRedWarps) {
+    double s = 0.0;
+    for (int64_t b = lane; b < n; b += 32) s += __ldcg(partials + (size_t)b * M + j);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) res[j] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < M; ++j) out[j] = res[j];
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
 // Thread -> (rhs, ordered site) map of the multi-rhs kernels: each block
 // iteration covers SPB = 128 / NR consecutive ordered sites; warp w serves
 // rhs w % NR on 32 of them.  Every load instruction streams one field.

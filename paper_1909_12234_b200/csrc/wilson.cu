@@ -50,8 +50,9 @@ __global__ void links_from_ref_kernel(Geom g, const double2 *__restrict__ ref, c
 // plain apply: one thread per (site, rhs-in-group of NR), links shared by the
 // NR threads of a site through L1 broadcast.
 template <typename R, int RECON, int NR>
-__global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4)) wilson_apply_kernel(WilsonParams P, const cplx<R> *__restrict__ in,
-                                                           cplx<R> *__restrict__ out, LinkField<R, RECON> links) {
+__global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4))
+    wilson_apply_kernel(WilsonParams P, const cplx<R> *__restrict__ in, cplx<R> *__restrict__ out,
+                        LinkField<R, RECON> links, unsigned long long *ctr) {
   // warp w of the block serves rhs w % NR on 32 consecutive sites: every load
   // instruction streams one field (like NR = 1) and the NR warps of a site
   // group share its links through L1.
@@ -59,7 +60,11 @@ __global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4)) wilson_apply_ke
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int rhs = w % NR;
   const int local = (w / NR) * 32 + lane;
-  for (int64_t o = blockIdx.x * (int64_t)SPB + local; o < P.g.V; o += (int64_t)gridDim.x * SPB) {
+  for (int64_t step = 0;; ++step) {
+    const int64_t chunk = ctr ? next_chunk(ctr) : blockIdx.x + step * (int64_t)gridDim.x;
+    if (chunk * SPB >= P.g.V) break;
+    const int64_t o = chunk * SPB + local;
+    if (o >= P.g.V) continue;
     const int64_t site = sched_site(P.sched, o);
     const cplx<R> *inr = in + (int64_t)rhs * 12 * P.g.V;
     cplx<R> *outr = out + (int64_t)rhs * 12 * P.g.V;
@@ -113,8 +118,9 @@ static int launch_apply(const mgt_wilson_s *h, const WilsonParams &P, const void
   if (!grid_cache) grid_cache = resident_grid(wilson_apply_kernel<R, RECON, NR>, block, (int64_t)1 << 40);
   int64_t need = (h->g.V * NR + block - 1) / block;
   const int grid = (int)std::min<int64_t>(grid_cache, need);
+  unsigned long long *ctr = take_counter(h, st);
   wilson_apply_kernel<R, RECON, NR><<<grid, block, 0, st>>>(P, reinterpret_cast<const cplx<R> *>(x),
-                                                             reinterpret_cast<cplx<R> *>(y), lf);
+                                                             reinterpret_cast<cplx<R> *>(y), lf, ctr);
   MGT_LAUNCH_CHECK("wilson_apply_kernel");
   return MGT_OK;
 }
@@ -202,6 +208,16 @@ int mgt_wilson_create(mgt_wilson_t *out, const int dims[4], int antiperiodic, do
     delete h;
     return cuda_fail(e, "cudaMallocHost(flags)");
   }
+  h->dyn_sched = 1;
+  if (const char *v = getenv("MGT_DYN_SCHED")) h->dyn_sched = atoi(v);
+  h->ctr_next = 0;
+  e = cudaMalloc(&h->ctr_ring, kCtrRing * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    cudaFree(h->links);
+    cudaFreeHost(h->host_flags);
+    delete h;
+    return cuda_fail(e, "cudaMalloc(counters)");
+  }
   cudaStream_t st = as_stream(stream);
   const int block = 256, grid = grid_for(g.V, block, 8);
   const double2 *ref = reinterpret_cast<const double2 *>(links_ref_dev);
@@ -229,6 +245,7 @@ int mgt_wilson_destroy(mgt_wilson_t h) {
   if (!h) return MGT_OK;
   drop_graphs(h);
   cudaFree(h->links);
+  cudaFree(h->ctr_ring);
   cudaFreeHost(h->host_flags);
   delete h;
   return MGT_OK;
