@@ -211,6 +211,33 @@ def apply_stencil(links, dims, mass, x, antiperiodic=True):
     return y[:, 0] if squeeze else y
 
 
+def apply_at_sites(links, dims, mass, x, sites, antiperiodic=True):
+    """(A x) at the given reference-order sites only, (len(sites), 12): the
+    same stencil as build_wilson4d_csr evaluated site by site, for spot checks
+    on lattices whose full CSR or stencil does not fit host memory.
+    links: (V, 4, 3, 3); x: (N,)."""
+    dims = tuple(int(L) for L in dims)
+    X = x.reshape(-1, NSPIN, NCOLOR)
+    U = links
+    eye4 = np.eye(NSPIN, dtype=np.complex128)
+    out = np.empty((len(sites), DOF), dtype=np.complex128)
+    for n, s in enumerate(sites):
+        c = list(np.unravel_index(int(s), dims))
+        acc = np.zeros((NSPIN, NCOLOR), dtype=np.complex128)
+        for mu in range(4):
+            up, dn = list(c), list(c)
+            up[mu] = (c[mu] + 1) % dims[mu]
+            dn[mu] = (c[mu] - 1) % dims[mu]
+            sf = np.ravel_multi_index(up, dims)
+            sb = np.ravel_multi_index(dn, dims)
+            pf = -1.0 if (antiperiodic and mu == 3 and c[3] == dims[3] - 1) else 1.0
+            pb = -1.0 if (antiperiodic and mu == 3 and c[3] == 0) else 1.0
+            acc += pf * (eye4 - GAMMAS[mu]) @ (X[sf] @ U[s, mu].T)
+            acc += pb * (eye4 + GAMMAS[mu]) @ (X[sb] @ U[sb, mu].conj())
+        out[n] = ((mass + 4.0) * X[s] - 0.5 * acc).reshape(-1)
+    return out
+
+
 def plane_wave_symbol(dims, mass, mom_index, antiperiodic=True):
     """Unit-gauge plane-wave KAT: A e^{ipx} chi = M(p) e^{ipx} chi with
     M(p) = (m + sum(1 - cos p)) I + i sum gamma_mu sin p_mu (the 4D version of

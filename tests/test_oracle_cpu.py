@@ -60,6 +60,14 @@ def test_stencil_matches_csr(small_op, gold):
     assert np.linalg.norm(y - gold["Ax"]) / np.linalg.norm(gold["Ax"]) < 1e-14
 
 
+def test_site_local_stencil_matches_csr(small_op, gold):
+    dims, A = small_op
+    sites = [0, 1, 5, 63, 100, 255]
+    got = W.apply_at_sites(gold["links"], dims, float(gold["mass"]), gold["x"], sites)
+    want = gold["Ax"].reshape(-1, 12)[sites]
+    assert np.abs(got - want).max() < 1e-14 * np.abs(want).max()
+
+
 def test_gamma5_hermiticity(small_op):
     dims, A = small_op
     g5 = W.gamma5_diag(A.shape[0] // 12)
