@@ -32,7 +32,7 @@ extern "C" int mgt_cdot(const void *a_dev, const void *b_dev, int64_t len, int n
   const int grid = grid_for(len, kRedBlock, 4);
   void *tmp = nullptr;
   const size_t bytes = (size_t)grid * 2 * sizeof(double) + 256;
-  MGT_CUDA(cudaMallocAsync(&tmp, bytes, st));
+  MGT_CUDA(scratch_alloc(&tmp, bytes, st));
   double *partials = (double *)((char *)tmp + 256);
   unsigned *ticket = (unsigned *)tmp;
   MGT_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));

@@ -174,10 +174,10 @@ int mgt_coarse_build(mgt_wilson_t h, const int block[4], int nv, const void *P_d
   const int64_t V = h->g.V;
   const int nc = cg.nc;
   double2 *v = nullptr, *split = nullptr, *xc = nullptr, *xc9 = nullptr;
-  MGT_CUDA(cudaMallocAsync((void **)&v, (size_t)12 * V * sizeof(double2), st));
-  MGT_CUDA(cudaMallocAsync((void **)&split, (size_t)9 * 12 * V * sizeof(double2), st));
-  MGT_CUDA(cudaMallocAsync((void **)&xc, (size_t)cg.nb * nc * sizeof(double2), st));
-  MGT_CUDA(cudaMallocAsync((void **)&xc9, (size_t)9 * cg.nb * nc * sizeof(double2), st));
+  MGT_CUDA(scratch_alloc((void **)&v, (size_t)12 * V * sizeof(double2), st));
+  MGT_CUDA(scratch_alloc((void **)&split, (size_t)9 * 12 * V * sizeof(double2), st));
+  MGT_CUDA(scratch_alloc((void **)&xc, (size_t)cg.nb * nc * sizeof(double2), st));
+  MGT_CUDA(scratch_alloc((void **)&xc9, (size_t)9 * cg.nb * nc * sizeof(double2), st));
   WilsonParams P = make_params(h, 0, 0.0);
   const int grid = grid_for(V, 128, 3);
   for (int col = 0; col < nc && rc == MGT_OK; ++col) {

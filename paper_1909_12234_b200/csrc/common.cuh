@@ -32,6 +32,11 @@ void note_launch(uint64_t n = 1);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Stream-ordered scratch allocation from the device's default memory pool,
+// with the pool's release threshold raised once so freed scratch stays
+// cached instead of being unmapped at every synchronisation.
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st);
+
 constexpr int kNumSMs = 148;
 
 // ---- complex arithmetic on double2 / float2 ------------------------------

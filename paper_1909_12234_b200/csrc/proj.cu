@@ -165,7 +165,7 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
   if (s <= 4) {
     const int gy = (k + kBlockVecs - 1) / kBlockVecs;
     nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, (int64_t)kNumSMs * 4 / gy + 1));
-    MGT_CUDA(cudaMallocAsync((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
+    MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy);
 #define MGT_VHX(SS) vhx_small_kernel<SS><<<grid, 256, 0, st>>>(V, X, len, k, part)
     switch (s) {
@@ -179,7 +179,7 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
   } else {
     const int gy = (k + 63) / 64, gz = (s + 63) / 64;
     nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, (int64_t)kNumSMs * 4 / (gy * gz) + 1));
-    MGT_CUDA(cudaMallocAsync((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
+    MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy, gz);
     vhx_tile_kernel<<<grid, 256, 0, st>>>(V, X, len, k, s, part);
     MGT_LAUNCH_CHECK("vhx_tile_kernel");

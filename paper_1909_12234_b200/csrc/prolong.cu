@@ -255,7 +255,7 @@ int mgt_prolong_build(const int dims[4], const int block[4], int nv, const void 
   MGT_LAUNCH_CHECK("prolong_gather_kernel");
   int *keep = nullptr;
   const size_t kb = (size_t)a.nb * 2 * nv * sizeof(int);
-  MGT_CUDA(cudaMallocAsync((void **)&keep, kb, st));
+  MGT_CUDA(scratch_alloc((void **)&keep, kb, st));
   prolong_mgs_kernel<<<(unsigned)(a.nb * 2), 256, 0, st>>>(a, (double2 *)P_dev, keep);
   MGT_LAUNCH_CHECK("prolong_mgs_kernel");
   if (keep_host) MGT_CUDA(cudaMemcpyAsync(keep_host, keep, kb, cudaMemcpyDeviceToHost, st));

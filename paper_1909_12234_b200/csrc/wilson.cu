@@ -23,6 +23,21 @@ int cuda_fail(cudaError_t e, const char *what) {
 }
 void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st) {
+  static thread_local int pool_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (pool_dev != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_dev = dev;
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+
 // ---------------------------------------------------------------------------
 // links: reference layout (V_ref, 4, 3, 3) complex128 -> native SoA
 template <typename R, int RECON>
