@@ -239,9 +239,10 @@ def run_ours(args):
     if world == 1:
         xh = torch.empty((op.dim,), dtype=torch.complex128, pin_memory=True)
         xh.copy_(op.from_native(x.to(torch.complex128) if args.prec == 32 else x)[0].cpu())
+        yh_out = torch.empty_like(xh, pin_memory=True)
 
-        def e2e_step():
-            return op.apply(xh)
+        def e2e_step():  # LatticeOperator.apply with host buffers, pipelined C-ABI path
+            return op.apply_host(xh, out=yh_out)
     else:
         xh = torch.empty(tuple(x.shape), dtype=dtype, pin_memory=True)
         xh.copy_(x.cpu())

@@ -90,6 +90,16 @@ int mgt_wilson_info(mgt_wilson_t h, int dims[4], int *prec, int *recon,
 int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs,
                      int flags, double tau, void *stream);
 
+/* Host-buffer apply: y_host = variant(A) x_host for n_rhs REFERENCE-layout
+ * complex128 vectors in host memory (LatticeOperator.apply with numpy
+ * arrays, lattice.py:214-217).  The host->device copies, the layout
+ * permutation, the stencil and the device->host copies are pipelined over
+ * `nchunks` x0-slabs on internal streams (pinned host buffers overlap fully).
+ * Returns after y_host is written. */
+int mgt_wilson_apply_host(mgt_wilson_t h, const void *x_host, void *y_host,
+                          int n_rhs, int flags, double tau, int nchunks,
+                          void *stream);
+
 /* ---- t-slab decomposition (multi-GPU) ------------------ */
 /* The reference is single-process.  A slab handle owns
  * global t in [t_begin, t_begin + dims_local[3]) of T_global (>= 2 slices);

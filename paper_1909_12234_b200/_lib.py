@@ -42,6 +42,7 @@ _SIGNATURES = {
     "mgt_wilson_destroy": (ct.c_int, [vp]),
     "mgt_wilson_info": (ct.c_int, [vp, c_int_p, c_int_p, c_int_p, c_i64_p]),
     "mgt_wilson_apply": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp]),
+    "mgt_wilson_apply_host": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, ct.c_int, vp]),
     "mgt_wilson_create_slab": (ct.c_int, [ct.POINTER(vp), c_int_p, ct.c_int, ct.c_int, ct.c_int, ct.c_double,
                                           ct.c_int, ct.c_int, vp, vp]),
     "mgt_halo_pack": (ct.c_int, [vp, vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp]),

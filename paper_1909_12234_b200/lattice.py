@@ -189,9 +189,29 @@ class WilsonOperator:
         return out
 
     # -- reference-layout API (lattice.py:214-247) ------------------------
+    def apply_host(self, x, out=None, flags=0, tau=0.0, nchunks=32):
+        """Host-memory reference-layout vector(s) (numpy or CPU tensor, (N,) or
+        (n, N) rows) -> host result through the pipelined C-ABI path
+        `mgt_wilson_apply_host` (PCIe copies overlapped with the layout
+        permutation and the stencil).  Pinned CPU tensors overlap fully."""
+        xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128))
+        if xt.dtype != torch.complex128:
+            xt = xt.to(torch.complex128)
+        xt = xt.contiguous()
+        n = 1 if xt.dim() == 1 else xt.shape[0]
+        if xt.numel() != n * self.dim:
+            raise ValueError(f"dimension mismatch: {xt.shape[-1]} != {self.dim}")
+        if out is None:
+            out = torch.empty_like(xt, pin_memory=xt.is_pinned())
+        _lib.check(_lib.lib().mgt_wilson_apply_host(self._handle, xt.data_ptr(), out.data_ptr(), n, int(flags),
+                                                     float(tau), int(nchunks), stream_ptr()), "apply_host")
+        return out if isinstance(x, torch.Tensor) else out.numpy()
+
     def _apply_ref(self, x, flags=0, tau=0.0):
         host = not isinstance(x, torch.Tensor)
         cpu_tensor = (not host) and x.device.type == "cpu"
+        if (host or cpu_tensor) and np.ndim(x) == 1:
+            return self.apply_host(x, flags=flags, tau=tau)
         xa = x
         if host:
             xa = np.asarray(x)
