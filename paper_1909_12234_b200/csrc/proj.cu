@@ -16,12 +16,19 @@
 
 namespace mgt {
 
-constexpr int kWarpVecs = 8;
-constexpr int kBlockVecs = 64;
+// WV vectors per warp (8 warps per block): WV * S complex accumulators per
+// thread; fewer vectors per warp for more rhs keeps the register count (and
+// so the loads in flight per SM) up.
+template <int S>
+constexpr int warp_vecs() {
+  return S <= 2 ? 8 : 4;
+}
 
 template <int S>
 __global__ void __launch_bounds__(256) vhx_small_kernel(const double2 *__restrict__ V, const double2 *__restrict__ X,
                                                         int64_t len, int k, double2 *__restrict__ part) {
+  constexpr int kWarpVecs = warp_vecs<S>();
+  constexpr int kBlockVecs = 8 * kWarpVecs;
   __shared__ double2 red[8][kWarpVecs * S];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i0 = blockIdx.y * kBlockVecs + warp * kWarpVecs;
@@ -109,13 +116,22 @@ __global__ void __launch_bounds__(256) vhx_tile_kernel(const double2 *__restrict
 }
 
 // H[j*k + i] (column major k x s) = sum over blocks of part[b][i][j]
+// one warp per output: lanes stride over the block partials, then a fixed
+// shuffle tree (deterministic)
 __global__ void vhx_reduce_kernel(const double2 *__restrict__ part, int nblk, int k, int s, double2 *__restrict__ H) {
   const int64_t n = (int64_t)k * s;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < n; q += warps) {
     const int i = (int)(q / s), j = (int)(q % s);
     C<double> t(0.0, 0.0);
-    for (int b = 0; b < nblk; ++b) t = t + ldc(part + (int64_t)b * n + q);
-    H[(int64_t)j * k + i] = make_double2(t.re, t.im);
+    for (int b = lane; b < nblk; b += 32) t = t + ldc(part + (int64_t)b * n + q);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      t.re += __shfl_xor_sync(0xffffffffu, t.re, off);
+      t.im += __shfl_xor_sync(0xffffffffu, t.im, off);
+    }
+    if (lane == 0) H[(int64_t)j * k + i] = make_double2(t.re, t.im);
   }
 }
 
@@ -163,8 +179,9 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
   int nblk;
   double2 *part = nullptr;
   if (s <= 4) {
-    const int gy = (k + kBlockVecs - 1) / kBlockVecs;
-    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, (int64_t)kNumSMs * 4 / gy + 1));
+    const int bv = 8 * (s <= 2 ? warp_vecs<1>() : warp_vecs<4>());
+    const int gy = (k + bv - 1) / bv;
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, (int64_t)kNumSMs * 6 / gy + 1));
     MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy);
 #define MGT_VHX(SS) vhx_small_kernel<SS><<<grid, 256, 0, st>>>(V, X, len, k, part)
@@ -184,7 +201,7 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
     vhx_tile_kernel<<<grid, 256, 0, st>>>(V, X, len, k, s, part);
     MGT_LAUNCH_CHECK("vhx_tile_kernel");
   }
-  vhx_reduce_kernel<<<grid_for((int64_t)k * s, 128, 4), 128, 0, st>>>(part, nblk, k, s, (double2 *)H_dev);
+  vhx_reduce_kernel<<<grid_for((int64_t)k * s * 32, 128, 8), 128, 0, st>>>(part, nblk, k, s, (double2 *)H_dev);
   MGT_LAUNCH_CHECK("vhx_reduce_kernel");
   MGT_CUDA(cudaFreeAsync(part, st));
   return MGT_OK;
