@@ -305,6 +305,18 @@ def _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op):
     return t0, (restrict, corrections)
 
 
+def coarse_deflation_triplets(coarse_op, k, tol=1e-2, tau=0.0, inner_tol=1e-2, max_iter=2000, max_basis=0):
+    """Algorithm-2 line 2 (experiments.py:65-74): inexact Davidson on the
+    coarse operator (GPU coarse BiCGStab inner solves), converted to singular
+    triplets whose vectors are native coarse fields."""
+    from . import eigen as E
+    from .krylov import SolveConfig
+    conf = E.EigenConfig(k=k, tol=tol, tau=tau, max_basis=max_basis,
+                         inner=SolveConfig(tol=inner_tol, max_iter=max_iter))
+    res = E.inexact_eigensolve(coarse_op, coarse_op.gamma5_diag, conf, E.shift_inverter_factory(coarse_op, conf.inner))
+    return E.to_singular_triplets(res), res
+
+
 def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probes, coarse_op=None):
     """Algorithm-2 trace estimate (trace.py:236-274) on the GPU.
 
@@ -330,9 +342,14 @@ def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probe
     # rank-r form (trace.py:220-233, :251-271)
     pr = prolongator
     dev = pr.P.device
-    ubar = np.asarray(coarse_triplets.left)[:, :rank]
-    ub = torch.as_tensor(np.ascontiguousarray(ubar.T), device=dev)  # (r, Nc) reference coarse order
-    ubn = pr.coarse_from_ref(ub.reshape(rank, pr.n_blocks, pr.nc))
+    left = coarse_triplets.left
+    if isinstance(left, torch.Tensor):  # GPU triplets: native coarse fields (r, nb, 2nv)
+        ubn = left[:rank].contiguous()
+        ubar = pr.coarse_to_ref(ubn).reshape(rank, -1).T.cpu().numpy()
+    else:  # reference triplets: (Nc, r) in the reference coarse order
+        ubar = np.asarray(left)[:, :rank]
+        ub = torch.as_tensor(np.ascontiguousarray(ubar.T), device=dev)
+        ubn = pr.coarse_from_ref(ub.reshape(rank, pr.n_blocks, pr.nc))
     wu = pr.prolong_native(ubn)  # W Ubar, (r, 12, V)
     g_cols = op.apply_native(wu)  # A W Ubar
     g5 = torch.ones(12, device=dev, dtype=torch.float64)

@@ -107,6 +107,22 @@ def main():
     out["orth_t0"] = est3.t0
     out["orth_samples"] = est3.samples
     out["orth_seed0"] = 70
+    # Algorithm 2 at rank r: coarse Davidson triplets (experiments.py:65-74),
+    # then the rank-r oblique deflation
+    cconf = eigen.EigenConfig(k=8, tol=1e-6, inner=krylov.SolveConfig(tol=1e-12))
+    cfac = eigen.shift_inverter_factory(C, cconf.inner)
+    cres = eigen.inexact_eigensolve(C, C.gamma5_diag, cconf, cfac)
+    ctrip = eigen.to_singular_triplets(cres, C.gamma5_diag)
+    out["ceig_lambdas"] = cres.lambdas
+    out["ceig_exact"] = eigen.dense_triplets(C).lambdas[:8]
+    out["ctrip_left"] = ctrip.left
+    inv4 = krylov.TruncatedInverse(op, krylov.SolveConfig(tol=1e-8))
+    ps4 = probing.build_probe_set(geo, 12, 3, hp_count=1, dilution=False, kind="rademacher", seed=90)
+    est4 = trace.deflate_oblique_coarse(op, inv4, P, ctrip, 6, ps4)
+    out["oblr_rank"] = 6
+    out["oblr_t0"] = est4.t0
+    out["oblr_samples"] = est4.samples
+    out["oblr_seed0"] = 90
     np.savez_compressed(os.path.join(HERE, "golden_4x4x4x4.npz"), **out)
     print("wrote golden_4x4x4x4.npz", {k: np.shape(v) for k, v in out.items()})
 

@@ -98,6 +98,54 @@ def test_full_coarse_deflation_matches_reference(gold, setup):
     assert abs(est.mean - complex(gold["obl_mean"])) / abs(complex(gold["obl_mean"])) < 1e-8 + 1e-10
 
 
+def test_coarse_bicgstab_solves(gold, setup):
+    M, MG, geo, op, A, Pg = setup
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    C = MG.build_coarse_operator(op, pro)
+    G = gold["C_dense"]
+    g5c = gold["coarse_gamma5"]
+    rng = np.random.default_rng(4)
+    bh = rng.normal(size=(3, C.dim)) + 1j * rng.normal(size=(3, C.dim))
+    b = pro.coarse_from_ref(torch.as_tensor(bh, device="cuda").reshape(3, pro.n_blocks, pro.nc))
+    for tau in (0.0, 0.3):
+        x, reps = MG.coarse_bicgstab(C, b, 1e-11, 500, tau)
+        assert all(r[2] for r in reps)
+        xr = pro.coarse_to_ref(x).reshape(3, -1).cpu().numpy()
+        for i in range(3):
+            exact = np.linalg.solve(G + 1j * tau * np.diag(g5c), bh[i])
+            assert np.linalg.norm(xr[i] - exact) / np.linalg.norm(exact) < 1e-9
+
+
+def test_coarse_davidson_and_rank_r_oblique_deflation(gold, setup):
+    M, MG, geo, op, A, Pg = setup
+    from paper_1909_12234_b200 import trace as TR
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    C = MG.build_coarse_operator(op, pro)
+    trip, res = TR.coarse_deflation_triplets(C, 8, tol=1e-6, inner_tol=1e-12)
+    assert res.converged.all()
+    exact = gold["ceig_exact"]
+    assert np.max(np.abs(res.lambdas - exact) / np.abs(exact)) < 1e-9
+    assert np.max(np.abs(res.lambdas - gold["ceig_lambdas"]) / np.abs(exact)) < 1e-9
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=1e-8))
+    probes = M.build_probe_set(geo, 12, 3, hp_count=1, dilution=False, kind="rademacher",
+                               seed=int(gold["oblr_seed0"]))
+    rank = int(gold["oblr_rank"])
+    # with the reference's own coarse triplets: same t0, samples within xi
+    class RefTrip:
+        left = gold["ctrip_left"]
+        count = gold["ctrip_left"].shape[1]
+    est = TR.deflate_oblique_coarse(op, inv, pro, RefTrip, rank, probes)
+    t0 = complex(gold["oblr_t0"])
+    assert abs(est.t0 - t0) < 1e-10 * abs(t0)
+    assert np.max(np.abs(est.samples - gold["oblr_samples"]) / np.abs(gold["oblr_samples"])) < 1e-7
+    # with the GPU triplets: the same deflation subspace up to the eigen tolerance
+    est2 = TR.deflate_oblique_coarse(op, inv, pro, trip, rank, probes)
+    assert abs(est2.t0 - t0) < 1e-6 * abs(t0)
+    assert np.max(np.abs(est2.samples - gold["oblr_samples"]) / np.abs(gold["oblr_samples"])) < 1e-6
+
+
 def test_config3_shape_against_oracle(cuda):
     """8^4, 4^4 aggregates, nv = 24 (the config-3 blocking at reduced volume):
     GPU null vectors + P + C against the oracle restatement."""
