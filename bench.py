@@ -272,6 +272,7 @@ def run_ours(args):
             probes3 = probes_config3(M, rank, world)
             if world == 1 and not args.skip_eigen:
                 probes4 = probes_config4(M, rank, world)
+    probes5 = probes_config5(M, rank, world) if args.config5 else None
 
     if rank == 0:
         line = {
@@ -300,6 +301,7 @@ def run_ours(args):
             "probes_per_sec": probes,
             "deflated_probes_per_sec": probes3,
             "eigen_deflated_probes_per_sec": probes4,
+            "full_box_deflated_probes_per_sec": probes5,
         }
         if world == 1 and not args.skip_cpu:
             try:
@@ -416,6 +418,42 @@ def probes_config4(M, rank, world, dims=(16, 16, 16, 16), s=128, k=64, tol=1e-8)
             "variance": float(est.variance) if world == 1 else None}
 
 
+def probes_config5(M, rank, world, dims=(32, 32, 32, 64), s=512, tol=1e-8, nv=24, r=64):
+    """BASELINE configs[4]: 32^3 x 64, eps 0.3, m0 0.05, 4^4 aggregates with
+    24 GCR(8)-relaxed null vectors (Nc = 393,216), Algorithm-2 deflation at
+    rank r from coarse Davidson triplets (a dense tr(C^-1) at this Nc would be
+    2.5 TB), s = 512 probes solved 4 per call.  Multi-GPU: probe sharding
+    with the lattice replicated per GPU (15 GB each)."""
+    import torch
+    from paper_1909_12234_b200 import multigrid as MG
+    from paper_1909_12234_b200 import trace as TR
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.3, seed=0), 0.05)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    nvs = MG.generate_null_vectors(op, nv, tol=1e-12, max_iter=8, seed=7)
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme((4, 4, 4, 4)), layout_op=op)
+    del nvs
+    coarse = MG.build_coarse_operator(op, pro)
+    torch.cuda.synchronize()
+    t_mg = time.perf_counter() - t0
+    trip, cres = TR.coarse_deflation_triplets(coarse, r, tol=1e-3, inner_tol=1e-3)
+    torch.cuda.synchronize()
+    setup = _max_over_ranks(time.perf_counter() - t0, world)
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
+    est, el = _sharded_estimate(
+        M, lambda p: TR.deflate_oblique_coarse(op, inv, pro, trip, r, p, coarse_op=coarse), geo, s, 300, rank,
+        world, reps=1)
+    return {"config": f"32^3x64 eps=0.3 m0=0.05, 4^4 aggregates, nv=24 GCR(8) null vectors (Nc={pro.coarse_dim}), "
+                      f"Algorithm 2 at rank {r} (coarse Davidson tol 1e-3), s={s} rademacher tol=1e-8, 4 rhs/solve "
+                      "(BASELINE configs[4])",
+            "value": s / el, "unit": "probes/s", "seconds": el, "setup_seconds": setup,
+            "setup_multigrid_seconds": t_mg, "coarse_eigen_inversions": int(cres.inversions),
+            "value_including_setup": s / (el + setup), "t0_re": float(est.t0.real),
+            "estimate_re": float(est.mean.real), "variance": float(est.variance),
+            "mean_iterations": inv.total_iterations / max(1, inv.n_solves)}
+
+
 def cpu_probes_sample(dims=(8, 8, 8, 8), n=4, tol=1e-8):
     """Reference path port (restated GCR(32) + Hutchinson, numpy/scipy, one
     process) on `n` config-1 probes."""
@@ -445,6 +483,7 @@ def main():
     ap.add_argument("--skip-probes", action="store_true")
     ap.add_argument("--skip-deflated", action="store_true")
     ap.add_argument("--skip-eigen", action="store_true")
+    ap.add_argument("--config5", action="store_true", help="also run BASELINE configs[4] (minutes)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
