@@ -77,6 +77,58 @@ def make_noise(n, kind="z4", seed=0):
     raise ValueError(f"unknown noise kind {kind!r}")
 
 
+def max_hp_level(geometry):
+    level = 0
+    while all(L % (2 ** (level + 1)) == 0 for L in geometry.dims):
+        level += 1
+    return level
+
+
+def _native_coords(geometry):
+    """(4, V) coordinates (x0..x3) of the native site order (t slowest)."""
+    L0, L1, L2, L3 = geometry.dims
+    s = torch.arange(geometry.site_count, device=device(), dtype=torch.int64)
+    x2 = s % L2
+    x1 = (s // L2) % L1
+    x0 = (s // (L2 * L1)) % L0
+    x3 = s // (L2 * L1 * L0)
+    return torch.stack([x0, x1, x2, x3])
+
+
+def hp_level(geometry, count):
+    """Level of the hierarchical-probing colouring for `count` vectors
+    (probing.py:64-77), with the reference's validation."""
+    if count < 1 or (count & (count - 1)) != 0:
+        raise ValueError(f"hp count must be a power of two, got {count}")
+    D = geometry.ndim
+    level = 0
+    while 2 ** (D * level) < count:
+        level += 1
+    if level > max_hp_level(geometry) or count > geometry.site_count:
+        raise ValueError(f"hp count {count} exceeds the closing colors of {geometry.dims}")
+    return level
+
+
+def hp_vectors_native(geometry, count):
+    """The first `count` hierarchical-probing vectors (+/-1 per site) in the
+    native site order, (count, V) float64 on the device: colour(x) = Morton
+    interleave of (x mod 2^level) bits (probing.py:45-61) and
+    h_j(x) = (-1)^popcount(j & colour(x)) (natural-order Hadamard, :78-84)."""
+    level = hp_level(geometry, count)
+    D = geometry.ndim
+    local = _native_coords(geometry) % (2 ** level)
+    colors = torch.zeros(geometry.site_count, dtype=torch.int64, device=device())
+    for b in range(level):
+        for d in range(D):
+            colors |= ((local[d] >> b) & 1) << (b * D + d)
+    j = torch.arange(count, device=device(), dtype=torch.int64)
+    anded = j[:, None] & colors[None, :]
+    bits = torch.zeros_like(anded)
+    for b in range(max(1, D * level)):
+        bits += (anded >> b) & 1
+    return torch.where(bits % 2 == 0, 1.0, -1.0).to(torch.float64)
+
+
 @dataclass
 class ProbeGroup:
     slots: object  # (n_slots, N) host array, materialised on demand
@@ -96,7 +148,7 @@ class ProbeSet:
     kind, seed0 + j) decomposed into `dilution_dim` spin-colour slots
     (hp_count = 1).  Slots are generated on the device on demand."""
 
-    def __init__(self, geometry, dof, n_noise, dilution=False, kind="rademacher", seed=0):
+    def __init__(self, geometry, dof, n_noise, dilution=False, kind="rademacher", seed=0, hp_count=1):
         if dof != 12:
             raise ValueError("the 4D SU(3) operator has dof = 12")
         self.geometry = geometry
@@ -105,7 +157,9 @@ class ProbeSet:
         self.dilution = bool(dilution)
         self.kind = kind
         self.seed = int(seed)
-        self.basis = ProbingBasis(geometry, dof if dilution else 1, 1)
+        self.hp_count = int(hp_count)
+        self._hp = hp_vectors_native(geometry, self.hp_count) if self.hp_count > 1 else None
+        self.basis = ProbingBasis(geometry, dof if dilution else 1, self.hp_count)
 
     @property
     def sample_count(self):
@@ -113,49 +167,62 @@ class ProbeSet:
 
     @property
     def slots_per_group(self):
-        return self.dof if self.dilution else 1
+        return self.hp_count * (self.dof if self.dilution else 1)
 
     @property
     def slot_count(self):
         return self.n_noise * self.slots_per_group
 
     def weights(self):
-        return np.ones(self.slots_per_group)
+        return np.full(self.slots_per_group, 1.0 / self.hp_count)
 
     def noise_native(self, j0, j1):
         """Noise fields of groups j0..j1-1, native layout."""
         return noise_native(self.geometry, [self.seed + j for j in range(j0, j1)], self.kind)
 
     def slots_native(self, j):
-        """All slots of group j, native layout (n_slots, 12, V)."""
-        z = self.noise_native(j, j + 1)
-        if not self.dilution:
-            return z
-        out = torch.zeros((self.dof,) + tuple(z.shape[1:]), dtype=z.dtype, device=z.device)
-        for p in range(self.dof):
-            out[p, p] = z[0, p]
-        return out
+        """All slots of group j in the reference's slot order (hp vector
+        outer, dilution pattern inner, probing.py:157-161), native layout
+        (n_slots, 12, V): slot = noise (.) kron(hp_h, dilution_p), multiplied
+        as complex x (mask + 0i) like numpy (signed zeros included)."""
+        z = self.noise_native(j, j + 1)[0]
+        V = self.geometry.site_count
+        hps = self._hp if self._hp is not None else torch.ones((1, V), dtype=torch.float64, device=z.device)
+        zr = torch.view_as_real(z)  # (12, V, 2)
+        out = torch.empty((self.slots_per_group, 12, V, 2), dtype=torch.float64, device=z.device)
+        s = 0
+        for h in range(hps.shape[0]):
+            for p in range(self.dof if self.dilution else 1):
+                # kron(hp_h, dilution_p) as numpy computes it: hp * pattern
+                # (so hp = -1 against a 0 of the pattern gives -0.0)
+                pat = torch.ones(12, dtype=torch.float64, device=z.device)
+                if self.dilution:
+                    pat = (torch.arange(12, device=z.device) == p).to(torch.float64)
+                m = hps[h][None, :] * pat[:, None]
+                zero = torch.zeros_like(m)
+                a, b = zr[..., 0], zr[..., 1]
+                out[s, ..., 0] = a * m - b * zero
+                out[s, ..., 1] = a * zero + b * m
+                s += 1
+        return torch.view_as_complex(out)
 
     @property
     def groups(self):
         """Reference-compatible host groups (materialises every slot)."""
         N = self.geometry.site_count * self.dof
+        from .multigrid import _LayoutOnly
+        lay = _LayoutOnly(self.geometry)
         out = []
         for j in range(self.n_noise):
             z = noise_ref(N, [self.seed + j], self.kind)[0].cpu().numpy()
-            if self.dilution:
-                slots = np.zeros((self.dof, N), dtype=np.complex128)
-                for p in range(self.dof):
-                    slots[p, p::self.dof] = z[p::self.dof]
-            else:
-                slots = z[None, :]
+            slots = lay.from_native(self.slots_native(j)).cpu().numpy()
             out.append(ProbeGroup(slots, self.weights(), NoiseVector(self.kind, self.seed + j, z)))
         return out
 
 
 def build_probe_set(geometry, dof, n_noise, hp_count=1, dilution=True, kind="z4", seed=0):
-    """Reference `build_probe_set` (probing.py:146-165) on the GPU.
-    Hierarchical probing (hp_count > 1) is SURVEY.md row f2, not built yet."""
-    if hp_count != 1:
-        raise NotImplementedError("hierarchical probing (hp_count > 1) is not in the GPU hot path yet")
-    return ProbeSet(geometry, dof, n_noise, dilution=dilution, kind=kind, seed=seed)
+    """Reference `build_probe_set` (probing.py:146-165) on the GPU: noise
+    j = make_noise(N, kind, seed + j) decomposed into hp_count hierarchical-
+    probing vectors x (dof if dilution else 1) spin-colour patterns, weights
+    1 / hp_count."""
+    return ProbeSet(geometry, dof, n_noise, dilution=dilution, kind=kind, seed=seed, hp_count=hp_count)

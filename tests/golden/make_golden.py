@@ -107,6 +107,18 @@ def main():
     out["orth_t0"] = est3.t0
     out["orth_samples"] = est3.samples
     out["orth_seed0"] = 70
+    # hierarchical probing + dilution slots (probing.py:146-165), 2 groups each
+    out["hp_seed"] = 21
+    for hp, dil, kind in [(1, True, "z4"), (16, False, "rademacher"), (16, True, "z4"), (256, False, "z4")]:
+        ps_hp = probing.build_probe_set(geo, 12, 2, hp_count=hp, dilution=dil, kind=kind, seed=21)
+        out[f"hp_{hp}_{int(dil)}_{kind}"] = np.stack([g.slots for g in ps_hp.groups])
+
+    ps_hp = probing.build_probe_set(geo, 12, 2, hp_count=16, dilution=False, kind="z4", seed=21)
+    inv_hp = krylov.TruncatedInverse(op, krylov.SolveConfig(tol=1e-8))
+    est_hp = trace.hutchinson(inv_hp, ps_hp)
+    out["hp16_samples"] = est_hp.samples
+    out["hp16_mean"] = est_hp.mean
+
     # Algorithm 2 at rank r: coarse Davidson triplets (experiments.py:65-74),
     # then the rank-r oblique deflation
     cconf = eigen.EigenConfig(k=8, tol=1e-6, inner=krylov.SolveConfig(tol=1e-12))

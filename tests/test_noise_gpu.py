@@ -50,6 +50,58 @@ def test_native_layout_probe_set(cuda):
     assert _bits_equal(groups[2].slots[0], P.rademacher_numpy(N, 44))
 
 
+@pytest.mark.parametrize("hp,dil,kind", [(1, True, "z4"), (16, False, "rademacher"), (16, True, "z4"),
+                                         (256, False, "z4")])
+def test_hierarchical_probing_slots_bitwise(cuda, hp, dil, kind):
+    """Slots vs the reference's build_probe_set (golden fixture made by the
+    reference: tests/golden/make_golden.py) -- bitwise incl. signed zeros."""
+    import os
+    import paper_1909_12234_b200 as M
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_4x4x4x4.npz"))
+    key = f"hp_{hp}_{int(dil)}_{kind}"
+    geo = M.LatticeGeometry(tuple(int(d) for d in g["dims"]), "antiperiodic")
+    ps = M.build_probe_set(geo, 12, 2, hp_count=hp, dilution=dil, kind=kind, seed=int(g["hp_seed"]))
+    groups = ps.groups
+    ref = g[key]  # (2 groups, n_slots, N)
+    assert len(groups) == 2 and groups[0].slots.shape == ref.shape[1:]
+    for j in range(2):
+        assert _bits_equal(groups[j].slots, ref[j])
+        assert np.array_equal(groups[j].weights, np.full(ref.shape[1], 1.0 / hp))
+
+
+def test_hutchinson_with_hierarchical_probing(cuda):
+    import os
+    import paper_1909_12234_b200 as M
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_4x4x4x4.npz"))
+    geo = M.LatticeGeometry(tuple(int(d) for d in g["dims"]), "antiperiodic")
+    op = M.build_wilson(M.gauge_from_array(geo, g["links"]), float(g["mass"]))
+    ps = M.build_probe_set(geo, 12, 2, hp_count=16, dilution=False, kind="z4", seed=int(g["hp_seed"]))
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=1e-8))
+    est = M.hutchinson(inv, ps)
+    assert inv.n_solves == 32 and est.inversions == 32
+    rel = np.abs(est.samples - g["hp16_samples"]) / np.abs(g["hp16_samples"])
+    assert rel.max() < 1e-8 + 1e-10
+
+
+def test_hp_vectors_match_reference_formula(cuda):
+    import paper_1909_12234_b200 as M
+    from paper_1909_12234_b200.probing import hp_vectors_native
+    from paper_1909_12234_b200.multigrid import _LayoutOnly
+    geo = M.LatticeGeometry((4, 4, 8, 8), "antiperiodic")
+    h = hp_vectors_native(geo, 16)  # native order
+    # native -> reference order through the layout kernel (12 identical comps)
+    lay = _LayoutOnly(geo)
+    f = h[:, None, :].expand(16, 12, geo.site_count).to(torch.complex128).contiguous()
+    ref_order = lay.from_native(f).cpu().numpy().reshape(16, geo.site_count, 12)[:, :, 0].real
+    coords = np.stack(np.unravel_index(np.arange(geo.site_count), geo.dims))
+    local = coords % 2
+    colors = sum(((local[d] >> 0) & 1) << d for d in range(4))
+    want = np.array([[(-1.0) ** bin(j & c).count("1") for c in colors] for j in range(16)])
+    assert np.array_equal(ref_order, want)
+    with pytest.raises(ValueError):
+        hp_vectors_native(geo, 3)
+
+
 def test_dilution_slots_sum_to_noise(cuda):
     import paper_1909_12234_b200 as M
     geo = M.LatticeGeometry((2, 2, 2, 4), "antiperiodic")
