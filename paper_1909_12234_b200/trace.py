@@ -340,7 +340,23 @@ def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probe
     if rank > coarse_triplets.count:
         raise ValueError(f"rank {rank} exceeds the {coarse_triplets.count} available triplets")
     # rank-r form (trace.py:220-233, :251-271)
+    fac, ubn, Y = _oblique_setup(op, inv_op, prolongator, coarse_triplets, rank)
+    minv = torch.as_tensor(fac.minv(), device=Y.device)
     pr = prolongator
+
+    def correction(j0, z, x):
+        g, h = _oblique_gh(pr, ubn, Y, z)
+        return torch.sum(h.conj() * (g @ minv.T), dim=1).cpu().numpy()
+
+    samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
+    _warn_flagged(flagged)
+    return finish(fac.t0, samples, inv_op.n_solves - before, flagged)
+
+
+def _oblique_setup(op, inv_op, pr, coarse_triplets, rank):
+    """oblique_factors (trace.py:220-233) + Y = A^-1_xi (A W Ubar) (:252):
+    returns (ObliqueFactors, Ubar as native coarse fields (r, nb, 2nv), Y)."""
+    import torch
     dev = pr.P.device
     left = coarse_triplets.left
     if isinstance(left, torch.Tensor):  # GPU triplets: native coarse fields (r, nb, 2nv)
@@ -358,19 +374,130 @@ def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probe
     g5c = pr.coarse_gamma5
     t_small = ubar.conj().T @ (g5c[:, None] * ubar)
     lam, uhat, t0 = factorize_small(s_small, t_small)
-    minv = torch.as_tensor(uhat @ np.diag(1.0 / lam) @ uhat.conj().T, device=dev)
     Y, _, _ = inv_op.solve_native(g_cols)
-    ubn_flat = ubn.reshape(rank, -1)
+    return ObliqueFactors(rank, lam, uhat, s_small, t_small, t0), ubn, Y
 
-    def correction(j0, z, x):
-        n = z.shape[0]
-        g = pr.restrict_native(z, gamma5_in=True).reshape(n, -1) @ ubn_flat.conj().T  # (n, r)
-        h = z.reshape(n, -1) @ Y.reshape(rank, -1).conj().T  # (n, r) = Y^H z
-        return torch.sum(h.conj() * (g @ minv.T), dim=1).cpu().numpy()
 
-    samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
-    _warn_flagged(flagged)
-    return finish(t0, samples, inv_op.n_solves - before, flagged)
+def _oblique_gh(pr, ubn, Y, z):
+    """Per slot g = Ubar^H (W^H (g5 z)) and h = Y^H z (trace.py:266-267), (n, r) each."""
+    n, r = z.shape[0], ubn.shape[0]
+    g = pr.restrict_native(z, gamma5_in=True).reshape(n, -1) @ ubn.reshape(r, -1).conj().T
+    h = z.reshape(n, -1) @ Y.reshape(r, -1).conj().T
+    return g, h
+
+
+@dataclass
+class PosteriorAnalysis:
+    """Small products of one expensive solve pass (trace.py:277-331): per
+    slot q = z^H A^-1 z, H = Y^H Z, G = Ubar^H W^H g5 Z and the k_max x k_max
+    small matrices; the deflated estimate at any rank <= k_max follows by
+    small dense algebra."""
+
+    rank_grid: list
+    k_max: int
+    weights: list
+    q: list
+    h: list
+    g: list
+    s_small: np.ndarray
+    t_small: np.ndarray
+    inversions: int
+    variances: dict = None
+    estimates: dict = None
+    errors: dict = None
+
+    def __post_init__(self):
+        self.variances = {} if self.variances is None else self.variances
+        self.estimates = {} if self.estimates is None else self.estimates
+        self.errors = {} if self.errors is None else self.errors
+
+    def storage_entries(self):
+        n = self.s_small.size + self.t_small.size
+        for qs, hs, gs, ws in zip(self.q, self.h, self.g, self.weights):
+            n += qs.size + hs.size + gs.size + ws.size
+        return n
+
+    def factors_at(self, rank):
+        lam, uhat, t0 = factorize_small(self.s_small[:rank, :rank], self.t_small[:rank, :rank])
+        return ObliqueFactors(rank, lam, uhat, self.s_small[:rank, :rank], self.t_small[:rank, :rank], t0)
+
+    def samples_at(self, rank):
+        minv = None if rank == 0 else self.factors_at(rank).minv()
+        out = np.empty(len(self.q), dtype=np.complex128)
+        for gi, (qs, hs, gs, ws) in enumerate(zip(self.q, self.h, self.g, self.weights)):
+            acc = 0.0 + 0.0j
+            for si in range(len(qs)):
+                if rank == 0:
+                    acc = acc + ws[si] * qs[si]
+                else:
+                    acc = acc + ws[si] * (qs[si] - np.vdot(hs[si, :rank], minv @ gs[si, :rank]))
+            out[gi] = acc
+        return out
+
+    def estimate_at(self, rank):
+        t0 = self.factors_at(rank).t0 if rank else 0.0 + 0.0j
+        return finish(t0, self.samples_at(rank), self.inversions)
+
+
+def posterior_rank_sweep(op, inv_op, prolongator, coarse_triplets, probes, rank_grid):
+    """One pass of expensive solves, then the deflated estimate at every rank
+    of rank_grid (trace.py:334-385)."""
+    rank_grid = sorted(set(int(r) for r in rank_grid))
+    if any(r < 0 for r in rank_grid):
+        raise ValueError("ranks must be >= 0")
+    k_max = max(rank_grid)
+    if k_max > coarse_triplets.count:
+        raise ValueError(f"rank grid up to {k_max} exceeds the {coarse_triplets.count} stored triplets")
+    before = getattr(inv_op, "n_solves", 0)
+    if k_max > 0:
+        fac, ubn, Y = _oblique_setup(op, inv_op, prolongator, coarse_triplets, k_max)
+        s_small, t_small = fac.s_small, fac.t_small
+    else:
+        s_small = t_small = np.zeros((0, 0), dtype=np.complex128)
+    store = {}
+
+    def collect(j0, z, x):
+        if k_max > 0:
+            g, h = _oblique_gh(prolongator, ubn, Y, z)
+            store[j0] = (h.cpu().numpy(), g.cpu().numpy())
+        return None
+
+    ns = probes.sample_count
+    w = probes.weights()
+    qs, hs, gs, ws = [], [], [], []
+    if probes.slots_per_group == 1:
+        batches = [(j0, min(ns, j0 + 4)) for j0 in range(0, ns, 4)]
+        results = _solve_batches_concurrently(inv_op, probes, batches, lambda j0, z, x: collect(j0, z, x) or 0.0,
+                                              default_streams(probes.geometry.site_count))
+        for (j0, j1), (reps, q) in zip(batches, results):
+            for rep in reps:
+                inv_op._account(rep)
+            for k in range(j1 - j0):
+                qs.append(np.array([q[k]]))
+                if k_max > 0:
+                    hs.append(store[j0][0][k:k + 1])
+                    gs.append(store[j0][1][k:k + 1])
+                else:
+                    hs.append(np.zeros((1, 0), dtype=np.complex128))
+                    gs.append(np.zeros((1, 0), dtype=np.complex128))
+                ws.append(np.array(w))
+    else:
+        for j in range(ns):
+            z = probes.slots_native(j)
+            x, reps, q = inv_op.solve_native(z, want_dot=True)
+            collect(j, z, x)
+            qs.append(np.asarray(q))
+            hs.append(store[j][0] if k_max > 0 else np.zeros((len(q), 0), dtype=np.complex128))
+            gs.append(store[j][1] if k_max > 0 else np.zeros((len(q), 0), dtype=np.complex128))
+            ws.append(np.array(w))
+    inversions = inv_op.n_solves - before
+    post = PosteriorAnalysis(rank_grid, k_max, ws, qs, hs, gs, s_small, t_small, inversions)
+    for r in rank_grid:
+        est = post.estimate_at(r)
+        post.variances[r] = est.variance
+        post.estimates[r] = est.mean
+        post.errors[r] = est.jackknife_err
+    return post
 
 
 def hutchinson(inv_op, probes):

@@ -135,6 +135,12 @@ def main():
     out["oblr_t0"] = est4.t0
     out["oblr_samples"] = est4.samples
     out["oblr_seed0"] = 90
+    inv5 = krylov.TruncatedInverse(op, krylov.SolveConfig(tol=1e-8))
+    post = trace.posterior_rank_sweep(op, inv5, P, ctrip, ps4, [0, 2, 4, 6])
+    out["post_grid"] = np.array([0, 2, 4, 6])
+    out["post_estimates"] = np.array([post.estimates[r] for r in (0, 2, 4, 6)])
+    out["post_variances"] = np.array([post.variances[r] for r in (0, 2, 4, 6)])
+    out["post_storage"] = post.storage_entries()
     np.savez_compressed(os.path.join(HERE, "golden_4x4x4x4.npz"), **out)
     print("wrote golden_4x4x4x4.npz", {k: np.shape(v) for k, v in out.items()})
 

@@ -146,6 +146,30 @@ def test_coarse_davidson_and_rank_r_oblique_deflation(gold, setup):
     assert np.max(np.abs(est2.samples - gold["oblr_samples"]) / np.abs(gold["oblr_samples"])) < 1e-6
 
 
+def test_posterior_rank_sweep_matches_reference(gold, setup):
+    M, MG, geo, op, A, Pg = setup
+    from paper_1909_12234_b200 import trace as TR
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+
+    class RefTrip:
+        left = gold["ctrip_left"]
+        count = gold["ctrip_left"].shape[1]
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=1e-8))
+    probes = M.build_probe_set(geo, 12, 3, hp_count=1, dilution=False, kind="rademacher",
+                               seed=int(gold["oblr_seed0"]))
+    post = TR.posterior_rank_sweep(op, inv, pro, RefTrip, probes, list(gold["post_grid"]))
+    est = np.array([post.estimates[int(r)] for r in gold["post_grid"]])
+    assert np.max(np.abs(est - gold["post_estimates"]) / np.abs(gold["post_estimates"])) < 1e-8
+    var = np.array([post.variances[int(r)] for r in gold["post_grid"]])
+    assert np.max(np.abs(var - gold["post_variances"]) / np.abs(gold["post_variances"])) < 1e-5
+    assert post.storage_entries() == int(gold["post_storage"])
+    # per-rank estimates equal a from-scratch deflate_oblique_coarse at that rank
+    inv2 = M.TruncatedInverse(op, M.SolveConfig(tol=1e-8))
+    e4 = TR.deflate_oblique_coarse(op, inv2, pro, RefTrip, 4, probes)
+    assert abs(e4.mean - post.estimates[4]) < 1e-12 * abs(e4.mean)
+
+
 def test_config3_shape_against_oracle(cuda):
     """8^4, 4^4 aggregates, nv = 24 (the config-3 blocking at reduced volume):
     GPU null vectors + P + C against the oracle restatement."""
