@@ -1,0 +1,139 @@
+"""Two-grid multigrid inverter on the GPU.
+
+Mirrors the reference's MG-preconditioned inverter:
+`krylov.Smoother` / `make_smoother` (`krylov.py:236-256`, fixed-iteration GCR
+from a zero start), `multigrid.two_grid_solve` (`multigrid.py:262-300`:
+coarse-grid correction, smoothing, explicit residual, divergence abort),
+`Hierarchy` / `build_hierarchy` (`:315-341`, two levels) and
+`MultigridSolver` (`:344-381`: coarsest level by LU or an iterative solve),
+wired as a `TruncatedInverse` solver plugin exactly like
+`experiments.build_inverter` (`experiments.py:50-62`).
+
+Everything runs on device fields: the smoother is the GPU GCR(m)
+(`mgt_gcr_solve`), restriction/prolongation are the P^H / P kernels, the
+coarsest solve is the cached dense C^-1 (LU on the device) or the coarse
+BiCGStab.  The fine prolongator kernels are specialised to the 12-component
+Wilson field, so hierarchies are two-level.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .krylov import SolveReport
+from .multigrid import (BlockingScheme, build_coarse_operator, build_prolongator, coarse_bicgstab,
+                        gcr_relax, generate_null_vectors)
+
+
+class Smoother:
+    """Fixed-iteration GCR from a zero start (krylov.py:236-252)."""
+
+    def __init__(self, op, n_iters):
+        if n_iters < 1:
+            raise ValueError("n_iters must be >= 1")
+        self.op = op
+        self.n_iters = n_iters
+        self.total_matvecs = 0
+
+    def __call__(self, b):
+        x, _, _, _, mv = gcr_relax(self.op, b, 1e-15, self.n_iters, self.n_iters)
+        self.total_matvecs += mv
+        return x
+
+
+def make_smoother(op, n_iters):
+    return Smoother(op, n_iters)
+
+
+def two_grid_solve(op, prolongator, coarse_solver, smoother, b, tol, max_cycles=100):
+    """multigrid.py:262-300 on native fields b (1, 12, V): returns
+    (x, SolveReport); matvecs count fine applications incl. the smoother's."""
+    bn = torch.linalg.vector_norm(b).item()
+    if bn == 0.0:
+        return torch.zeros_like(b), SolveReport(0, 0.0, True, 0)
+    x = torch.zeros_like(b)
+    r = b.clone()
+    matvecs = 0
+    sm_before = getattr(smoother, "total_matvecs", 0)
+    best = 1.0
+    relres = best
+
+    def report(cycle, ok, reason=""):
+        sm = getattr(smoother, "total_matvecs", sm_before) - sm_before
+        return SolveReport(cycle, relres, ok, matvecs + sm, reason)
+
+    for cycle in range(max_cycles):
+        if relres <= tol:
+            return x, report(cycle, True)
+        xc = coarse_solver(prolongator.restrict_native(r))
+        x = x + prolongator.prolong_native(xc)
+        r = b - op.apply_native(x)
+        matvecs += 1
+        x = x + smoother(r)
+        r = b - op.apply_native(x)
+        matvecs += 1
+        relres = torch.linalg.vector_norm(r).item() / bn
+        best = min(best, relres)
+        if relres > 10 * best:
+            return x, report(cycle + 1, False, "divergence")
+    ok = relres <= tol
+    return x, report(max_cycles, ok, "" if ok else "max_cycles")
+
+
+@dataclass
+class Hierarchy:
+    operators: list
+    prolongators: list
+
+    @property
+    def levels(self):
+        return len(self.operators)
+
+
+def build_hierarchy(op, blockings, null_counts, null_tol=1e-2, null_max_iter=200, seed=0):
+    """Two-level hierarchy by null-vector setup (multigrid.py:328-341)."""
+    if len(blockings) != len(null_counts):
+        from .multigrid import BlockingError
+        raise BlockingError("need one null-vector count per blocking level")
+    if len(blockings) != 1:
+        raise NotImplementedError("the GPU prolongator kernels are two-level (fine dof 12)")
+    nv = generate_null_vectors(op, null_counts[0], tol=null_tol, max_iter=null_max_iter, seed=seed)
+    P = build_prolongator(nv, BlockingScheme(tuple(blockings[0])), layout_op=op)
+    return Hierarchy([op, build_coarse_operator(op, P, level=1)], [P])
+
+
+class MultigridSolver:
+    """Two-grid cycles with a coarsest-level LU (dense C^-1 on the device) or
+    an iterative coarse BiCGStab (multigrid.py:344-381)."""
+
+    def __init__(self, hierarchy, smoother_iters=4, coarse_tol=1e-1, coarse_max_iter=200, coarsest="lu"):
+        self.hierarchy = hierarchy
+        self.smoothers = [make_smoother(o, smoother_iters) for o in hierarchy.operators[:-1]]
+        self.coarse_tol = coarse_tol
+        self.coarse_max_iter = coarse_max_iter
+        self.coarsest = coarsest
+        coarse = hierarchy.operators[-1]
+        if coarsest == "lu":
+            self._cinv = coarse.dense_inverse_native()
+            self._coarse = lambda rc: (rc.reshape(rc.shape[0], -1) @ self._cinv.T).reshape(rc.shape)
+        else:
+            self._coarse = lambda rc: coarse_bicgstab(coarse, rc, self.coarse_tol, self.coarse_max_iter)[0]
+
+    def solve_native(self, b, tol, max_cycles=100):
+        h = self.hierarchy
+        return two_grid_solve(h.operators[0], h.prolongators[0], self._coarse, self.smoothers[0], b, tol, max_cycles)
+
+    def solve(self, b, tol, max_cycles=100):
+        """Reference-layout vector in / out (numpy or CUDA tensor)."""
+        op = self.hierarchy.operators[0]
+        host = not isinstance(b, torch.Tensor)
+        bd = torch.as_tensor(np.asarray(b, dtype=np.complex128)).cuda() if host else b
+        x, rep = self.solve_native(op.to_native(bd.reshape(1, -1)), tol, max_cycles)
+        xr = op.from_native(x)[0]
+        return (xr.cpu().numpy() if host else xr), rep
+
+    def solver_plugin(self):
+        """callable(op, b, config) -> (x, SolveReport) for TruncatedInverse
+        (experiments.py:55-60)."""
+        return lambda _op, b, cfg: self.solve(b, cfg.tol, max_cycles=cfg.max_iter)

@@ -141,6 +141,13 @@ def main():
     out["post_estimates"] = np.array([post.estimates[r] for r in (0, 2, 4, 6)])
     out["post_variances"] = np.array([post.variances[r] for r in (0, 2, 4, 6)])
     out["post_storage"] = post.storage_entries()
+    # two-grid MG inverter (multigrid.py:262-381) with the golden hierarchy
+    hier = multigrid.Hierarchy([op, C], [P])
+    mg = multigrid.MultigridSolver(hier, smoother_iters=4, coarse_tol=1e-1)
+    xmg, repmg = mg.solve(out["probes"][0], 1e-10, max_cycles=100)
+    out["mg_x"] = xmg
+    out["mg_cycles"] = repmg.iterations
+    out["mg_matvecs"] = repmg.matvecs
     np.savez_compressed(os.path.join(HERE, "golden_4x4x4x4.npz"), **out)
     print("wrote golden_4x4x4x4.npz", {k: np.shape(v) for k, v in out.items()})
 

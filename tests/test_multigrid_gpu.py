@@ -170,6 +170,27 @@ def test_posterior_rank_sweep_matches_reference(gold, setup):
     assert abs(e4.mean - post.estimates[4]) < 1e-12 * abs(e4.mean)
 
 
+@pytest.mark.parametrize("coarsest", ["lu", "bicgstab"])
+def test_two_grid_inverter_matches_reference(gold, setup, coarsest):
+    M, MG, geo, op, A, Pg = setup
+    from paper_1909_12234_b200 import mgsolve
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    hier = mgsolve.Hierarchy([op, MG.build_coarse_operator(op, pro)], [pro])
+    mg = mgsolve.MultigridSolver(hier, smoother_iters=4, coarse_tol=1e-1, coarsest=coarsest)
+    x, rep = mg.solve(gold["probes"][0], 1e-10, max_cycles=100)
+    assert rep.converged and rep.final_relres <= 1e-10
+    xe = gold["mg_x"]
+    assert np.linalg.norm(x - xe) / np.linalg.norm(xe) < 1e-8
+    if coarsest == "lu":  # same cycle structure as the reference (exact coarse solve)
+        assert abs(rep.iterations - int(gold["mg_cycles"])) <= 1
+    # as a TruncatedInverse plugin (experiments.py:50-62)
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=1e-10, max_iter=100), solver=mg.solver_plugin())
+    y = inv(gold["probes"][1])
+    r = gold["probes"][1] - A @ y
+    assert np.linalg.norm(r) <= 1.01e-10 * np.linalg.norm(gold["probes"][1]) and inv.n_solves == 1
+
+
 def test_config3_shape_against_oracle(cuda):
     """8^4, 4^4 aggregates, nv = 24 (the config-3 blocking at reduced volume):
     GPU null vectors + P + C against the oracle restatement."""
