@@ -44,6 +44,10 @@ extern "C" {
 #define MGT_G5_IN 1  /* y = A (g5 x)          : a_gamma5()        lattice.py:244-247 */
 #define MGT_G5_OUT 2 /* y = g5 (A x)          : hermitian_form()  lattice.py:240-242 */
 #define MGT_DAGGER 4 /* y = A^dag x = g5 A g5 : apply_dagger()    lattice.py:219-222 */
+/* mgt_halo_pack only: the face pointers are peer-mapped receive windows of
+ * the neighbouring ranks (CUDA IPC over NVLink); the pack kernel stores the
+ * projected faces straight into them and fences system-wide. */
+#define MGT_HALO_PEER 8
 
 typedef struct mgt_wilson_s *mgt_wilson_t;
 
@@ -60,6 +64,13 @@ int mgt_spinor_from_ref(const int dims[4], int prec, const void *ref_dev,
                         void *native_dev, int n_rhs, void *stream);
 int mgt_spinor_to_ref(const int dims[4], int prec, const void *native_dev,
                       void *ref_dev, int n_rhs, void *stream);
+
+/* native (n_rhs, 12, V) <-> rhs-interleaved (12, V, n_rhs) (inverse = 1 goes
+ * interleaved -> native).  The interleaved layout is the multi-rhs form of
+ * the dilution / hierarchical-probing slot batches (probing.py:110-165,
+ * SURVEY 8(f) f2): the rhs of one site share every link load. */
+int mgt_rhs_interleave(int64_t volume, int prec, int n_rhs, int inverse,
+                       const void *in_dev, void *out_dev, void *stream);
 
 /* ---- gauge links --------------------------------------------------------- */
 /* SU(3) U = expm(i eps H) for `nsites` reference-order sites starting at
@@ -89,6 +100,12 @@ int mgt_wilson_info(mgt_wilson_t h, int dims[4], int *prec, int *recon,
  * (eigen.py:140-151). */
 int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs,
                      int flags, double tau, void *stream);
+
+/* The same operator on n_rhs rhs-interleaved fields ((comp*V + site)*n_rhs +
+ * rhs), n_rhs in {1, 2, 4, 8, 12}: one pass over the links for all rhs
+ * (LatticeOperator.apply on an (N, k) block, lattice.py:214-217). */
+int mgt_wilson_apply_il(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs,
+                        int flags, double tau, void *stream);
 
 /* Host-buffer apply: y_host = variant(A) x_host for n_rhs REFERENCE-layout
  * complex128 vectors in host memory (LatticeOperator.apply with numpy
@@ -122,6 +139,20 @@ int mgt_wilson_apply_slab(mgt_wilson_t h, const void *x_dev, void *y_dev,
                           const void *halo_next_dev, const void *halo_prev_dev,
                           int n_rhs, int flags, double tau, int part,
                           void *stream);
+
+/* Peer-memory transport for the slab halos (replaces the NCCL send/recv of
+ * the faces): every rank allocates one receive window with mgt_ipc_alloc,
+ * the 64-byte handles are all-gathered by the caller (torch.distributed),
+ * each rank maps its t neighbours' windows with mgt_ipc_open, and
+ * mgt_halo_pack(..., flags | MGT_HALO_PEER) writes the faces directly into
+ * them.  A stream-ordered barrier (one tiny NCCL all-reduce) then releases
+ * the boundary kernels; windows are double-buffered by apply parity so the
+ * next pack never overwrites a face a neighbour may still be reading. */
+#define MGT_IPC_HANDLE_BYTES 64
+int mgt_ipc_alloc(size_t bytes, void **dev_ptr, void *handle_out);
+int mgt_ipc_free(void *dev_ptr);
+int mgt_ipc_open(const void *handle, void **dev_ptr);
+int mgt_ipc_close(void *dev_ptr);
 
 /* ---- BLAS-1 on native fields (fp64) -------------------------------------- */
 /* out[r] = sum_i conj(a_i) b_i for each of n_rhs fields of `len` complex

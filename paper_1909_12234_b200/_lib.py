@@ -21,6 +21,8 @@ MGT_ERR_BLOCKING = 4
 G5_IN = 1
 G5_OUT = 2
 DAGGER = 4
+HALO_PEER = 8
+IPC_HANDLE_BYTES = 64
 
 _lock = threading.Lock()
 _lib = None
@@ -42,6 +44,12 @@ _SIGNATURES = {
     "mgt_wilson_destroy": (ct.c_int, [vp]),
     "mgt_wilson_info": (ct.c_int, [vp, c_int_p, c_int_p, c_int_p, c_i64_p]),
     "mgt_wilson_apply": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp]),
+    "mgt_wilson_apply_il": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp]),
+    "mgt_rhs_interleave": (ct.c_int, [ct.c_int64, ct.c_int, ct.c_int, ct.c_int, vp, vp, vp]),
+    "mgt_ipc_alloc": (ct.c_int, [ct.c_size_t, ct.POINTER(ct.c_void_p), vp]),
+    "mgt_ipc_free": (ct.c_int, [vp]),
+    "mgt_ipc_open": (ct.c_int, [vp, ct.POINTER(ct.c_void_p)]),
+    "mgt_ipc_close": (ct.c_int, [vp]),
     "mgt_wilson_apply_host": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, ct.c_int, vp]),
     "mgt_wilson_create_slab": (ct.c_int, [ct.POINTER(vp), c_int_p, ct.c_int, ct.c_int, ct.c_int, ct.c_double,
                                           ct.c_int, ct.c_int, vp, vp]),

@@ -75,7 +75,9 @@ struct LinkField {
 };
 
 // Accumulate one hop into acc[spin][colour] (without the -1/2).
-template <int MU, bool FWD, typename R, int RECON>
+// SS: site stride of the spinor field (1: native SoA; NR: rhs-interleaved
+// ((comp*V + site)*NR + rhs), `in` pre-offset by rhs).
+template <int MU, bool FWD, typename R, int RECON, int SS = 1>
 __device__ __forceinline__ void wilson_hop(const Geom &g, const cplx<R> *__restrict__ in,
                                            const LinkField<R, RECON> &links, int64_t site,
                                            const int (&x)[4], R g5in, bool antiperiodic,
@@ -96,10 +98,10 @@ __device__ __forceinline__ void wilson_hop(const Geom &g, const cplx<R> *__restr
   C<R> h[2][3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    C<R> p0 = ldc(in + (0 * 3 + c) * V + nb);
-    C<R> p1 = ldc(in + (1 * 3 + c) * V + nb);
-    C<R> p2 = g5in * ldc(in + (2 * 3 + c) * V + nb);
-    C<R> p3 = g5in * ldc(in + (3 * 3 + c) * V + nb);
+    C<R> p0 = ldc(in + ((0 * 3 + c) * V + nb) * SS);
+    C<R> p1 = ldc(in + ((1 * 3 + c) * V + nb) * SS);
+    C<R> p2 = g5in * ldc(in + ((2 * 3 + c) * V + nb) * SS);
+    C<R> p3 = g5in * ldc(in + ((3 * 3 + c) * V + nb) * SS);
     C<R> b0, b1;
     b_mul<MU>(p2, p3, b0, b1);
     if constexpr (FWD) {
@@ -211,7 +213,7 @@ __device__ __forceinline__ void wilson_thop_halo(const WilsonParams &P, const Li
 
 // y = G_out [ diag z - 1/2 hop(z) ],  z = G_in x.  Also returns the raw input
 // x at the site (xc, before G_in) for fused epilogues.
-template <typename R, int RECON>
+template <typename R, int RECON, int SS = 1>
 __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R> *__restrict__ in,
                                             const LinkField<R, RECON> &links, int64_t site,
                                             C<R> (&y)[4][3], C<R> (&xc)[4][3], int rhs = 0) {
@@ -231,24 +233,24 @@ __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R>
   if (P.slab && x[3] == P.g.L[3] - 1)
     wilson_thop_halo<true>(P, links, site, x, rhs, acc);
   else
-    wilson_hop<3, true>(P.g, in, links, site, x, g5in, ap, acc);
+    wilson_hop<3, true, R, RECON, SS>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
   if (P.slab && x[3] == 0)
     wilson_thop_halo<false>(P, links, site, x, rhs, acc);
   else
-    wilson_hop<3, false>(P.g, in, links, site, x, g5in, ap, acc);
+    wilson_hop<3, false, R, RECON, SS>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
-  wilson_hop<0, true>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<0, true, R, RECON, SS>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
-  wilson_hop<0, false>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<0, false, R, RECON, SS>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
-  wilson_hop<1, true>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<1, true, R, RECON, SS>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
-  wilson_hop<1, false>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<1, false, R, RECON, SS>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
-  wilson_hop<2, true>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<2, true, R, RECON, SS>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
-  wilson_hop<2, false>(P.g, in, links, site, x, g5in, ap, acc);
+  wilson_hop<2, false, R, RECON, SS>(P.g, in, links, site, x, g5in, ap, acc);
   MGT_HOP_FENCE;
 #undef MGT_HOP_FENCE
   const C<R> dup((R)P.diag_up_re, (R)P.diag_up_im);
@@ -259,7 +261,7 @@ __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R>
   for (int a = 0; a < 4; ++a) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      C<R> v = ldc(in + (a * 3 + c) * P.g.V + site);
+      C<R> v = ldc(in + ((a * 3 + c) * P.g.V + site) * SS);
       xc[a][c] = v;
       if (a >= 2) {
         v = g5in * v;

@@ -3,6 +3,23 @@
 
 namespace mgt {
 
+// native (n_rhs, 12, V)  <->  rhs-interleaved (12, V, n_rhs)
+template <typename R>
+__global__ void rhs_interleave_kernel(int64_t n12v, int n_rhs, int inverse, const cplx<R> *__restrict__ a,
+                                      cplx<R> *__restrict__ b) {
+  const int64_t n = n12v * n_rhs;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    // idx walks the interleaved order: e = idx / n_rhs, rhs = idx % n_rhs
+    const int64_t e = idx / n_rhs;
+    const int rhs = (int)(idx - e * n_rhs);
+    const int64_t nat = (int64_t)rhs * n12v + e;
+    if (inverse)
+      b[nat] = a[idx];
+    else
+      b[idx] = a[nat];
+  }
+}
+
 // ref (n_rhs, V_ref, 12) complex128  ->  native (n_rhs, 12, V_native)
 template <typename R>
 __global__ void spinor_from_ref_kernel(Geom g, int n_rhs, const double2 *__restrict__ ref, cplx<R> *__restrict__ nat) {
@@ -173,6 +190,24 @@ int mgt_su3_expm(double eps, const double *normals_dev, int64_t site_begin, int6
   su3_expm_kernel<<<grid, block, 0, as_stream(stream)>>>(eps, normals_dev, site_begin, nsites,
                                                           (double2 *)links_ref_dev);
   MGT_LAUNCH_CHECK("su3_expm_kernel");
+  return MGT_OK;
+}
+
+int mgt_rhs_interleave(int64_t V, int prec, int n_rhs, int inverse, const void *in_dev, void *out_dev,
+                       void *stream) {
+  if (!in_dev || !out_dev || n_rhs < 1 || V < 1 || in_dev == out_dev)
+    return fail(MGT_ERR_INVALID, "mgt_rhs_interleave: bad argument");
+  const int64_t n12v = 12 * V;
+  const int block = 256, grid = grid_for(n12v * n_rhs, block, 8);
+  if (prec == 64)
+    rhs_interleave_kernel<double><<<grid, block, 0, as_stream(stream)>>>(
+        n12v, n_rhs, inverse, (const cplx<double> *)in_dev, (cplx<double> *)out_dev);
+  else if (prec == 32)
+    rhs_interleave_kernel<float><<<grid, block, 0, as_stream(stream)>>>(
+        n12v, n_rhs, inverse, (const cplx<float> *)in_dev, (cplx<float> *)out_dev);
+  else
+    return fail(MGT_ERR_INVALID, "prec must be 64 or 32");
+  MGT_LAUNCH_CHECK("rhs_interleave_kernel");
   return MGT_OK;
 }
 

@@ -9,13 +9,16 @@
 // and the backward hop needs no link at all.  The antiperiodic sign is
 // applied by the receiver from its global t.  Interior sites (t in
 // 1 .. T_local-2) need no halo, so their kernel can overlap the exchange.
+#include <cstring>
+#include <string>
+
 #include "handle.cuh"
 
 namespace mgt {
 
 template <typename R, int RECON>
 __global__ void halo_pack_kernel(WilsonParams P, const cplx<R> *__restrict__ in, LinkField<R, RECON> links,
-                                 cplx<R> *__restrict__ to_prev, cplx<R> *__restrict__ to_next) {
+                                 cplx<R> *__restrict__ to_prev, cplx<R> *__restrict__ to_next, int peer) {
   const int64_t S3 = P.g.stride[3], V = P.g.V;
   const int rhs = blockIdx.y;
   const cplx<R> *x = in + (int64_t)rhs * 12 * V;
@@ -52,6 +55,10 @@ __global__ void halo_pack_kernel(WilsonParams P, const cplx<R> *__restrict__ in,
         stc(tn + (a * 3 + i) * S3, t);
       }
   }
+  // peer-mapped faces: the stores above went over NVLink straight into the
+  // neighbours' receive windows; make them visible system-wide before the
+  // stream-ordered barrier that releases the neighbours' boundary kernels
+  if (peer) __threadfence_system();
 }
 
 // part 0: every site; 1: interior slices 1 .. L3-2; 2: boundary slices
@@ -90,10 +97,11 @@ __global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4))
 
 template <typename R, int RECON>
 static int pack_t(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *to_prev, void *to_next,
-                  int n_rhs, cudaStream_t st) {
+                  int n_rhs, int peer, cudaStream_t st) {
   LinkField<R, RECON> lf{reinterpret_cast<const cplx<R> *>(h->links), h->g.V};
   dim3 grid(grid_for(h->g.stride[3], 128, 4), n_rhs);
-  halo_pack_kernel<R, RECON><<<grid, 128, 0, st>>>(P, (const cplx<R> *)x, lf, (cplx<R> *)to_prev, (cplx<R> *)to_next);
+  halo_pack_kernel<R, RECON><<<grid, 128, 0, st>>>(P, (const cplx<R> *)x, lf, (cplx<R> *)to_prev, (cplx<R> *)to_next,
+                                                    peer);
   MGT_LAUNCH_CHECK("halo_pack_kernel");
   return MGT_OK;
 }
@@ -136,13 +144,14 @@ int mgt_wilson_create_slab(mgt_wilson_t *out, const int dims_local[4], int t_beg
 int mgt_halo_pack(mgt_wilson_t h, const void *x_dev, void *to_prev_dev, void *to_next_dev, int n_rhs, int flags,
                   double tau, void *stream) {
   if (!h || !x_dev || !to_prev_dev || !to_next_dev || n_rhs < 1) return fail(MGT_ERR_INVALID, "mgt_halo_pack: bad argument");
-  WilsonParams P = make_params(h, flags, tau);
+  const int peer = (flags & MGT_HALO_PEER) ? 1 : 0;
+  WilsonParams P = make_params(h, flags & ~MGT_HALO_PEER, tau);
   cudaStream_t st = as_stream(stream);
   if (h->prec == 64)
-    return h->recon == 18 ? pack_t<double, 18>(h, P, x_dev, to_prev_dev, to_next_dev, n_rhs, st)
-                          : pack_t<double, 12>(h, P, x_dev, to_prev_dev, to_next_dev, n_rhs, st);
-  return h->recon == 18 ? pack_t<float, 18>(h, P, x_dev, to_prev_dev, to_next_dev, n_rhs, st)
-                        : pack_t<float, 12>(h, P, x_dev, to_prev_dev, to_next_dev, n_rhs, st);
+    return h->recon == 18 ? pack_t<double, 18>(h, P, x_dev, to_prev_dev, to_next_dev, n_rhs, peer, st)
+                          : pack_t<double, 12>(h, P, x_dev, to_prev_dev, to_next_dev, n_rhs, peer, st);
+  return h->recon == 18 ? pack_t<float, 18>(h, P, x_dev, to_prev_dev, to_next_dev, n_rhs, peer, st)
+                        : pack_t<float, 12>(h, P, x_dev, to_prev_dev, to_next_dev, n_rhs, peer, st);
 }
 
 int mgt_wilson_apply_slab(mgt_wilson_t h, const void *x_dev, void *y_dev, const void *halo_next_dev,
@@ -162,6 +171,49 @@ int mgt_wilson_apply_slab(mgt_wilson_t h, const void *x_dev, void *y_dev, const 
                           : slab_t<double, 12>(h, P, x_dev, y_dev, n_rhs, part, st);
   return h->recon == 18 ? slab_t<float, 18>(h, P, x_dev, y_dev, n_rhs, part, st)
                         : slab_t<float, 12>(h, P, x_dev, y_dev, n_rhs, part, st);
+}
+
+// ---- CUDA IPC windows (the peer-memory transport of the slab halos) -------
+int mgt_ipc_alloc(size_t bytes, void **dev_ptr, void *handle_out) {
+  if (!dev_ptr || !handle_out || bytes == 0) return fail(MGT_ERR_INVALID, "mgt_ipc_alloc: bad argument");
+  void *p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) return fail(MGT_ERR_CUDA, std::string("mgt_ipc_alloc: ") + cudaGetErrorString(e));
+  cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t hd;
+  e = cudaIpcGetMemHandle(&hd, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return fail(MGT_ERR_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == MGT_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &hd, sizeof(hd));
+  *dev_ptr = p;
+  return MGT_OK;
+}
+
+int mgt_ipc_free(void *dev_ptr) {
+  if (!dev_ptr) return MGT_OK;
+  cudaError_t e = cudaFree(dev_ptr);
+  return e == cudaSuccess ? MGT_OK : fail(MGT_ERR_CUDA, std::string("mgt_ipc_free: ") + cudaGetErrorString(e));
+}
+
+int mgt_ipc_open(const void *handle, void **dev_ptr) {
+  if (!handle || !dev_ptr) return fail(MGT_ERR_INVALID, "mgt_ipc_open: bad argument");
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof(hd));
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(MGT_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  }
+  return MGT_OK;
+}
+
+int mgt_ipc_close(void *dev_ptr) {
+  if (!dev_ptr) return MGT_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  return e == cudaSuccess ? MGT_OK : fail(MGT_ERR_CUDA, std::string("mgt_ipc_close: ") + cudaGetErrorString(e));
 }
 
 }  // extern "C"

@@ -140,6 +140,73 @@ static int launch_apply(const mgt_wilson_s *h, const WilsonParams &P, const void
   return MGT_OK;
 }
 
+// rhs-interleaved apply: fields at ((comp*V + site)*NR + rhs).  Thread
+// (site, rhs) = (tid / NR, tid % NR): the NR lanes of a site load the same
+// link address in one request (one sector set per NR rhs) and a warp's
+// spinor loads are 512 contiguous bytes, as for NR = 1.
+template <typename R, int RECON, int NR>
+__global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4))
+    wilson_apply_il_kernel(WilsonParams P, const cplx<R> *__restrict__ in, cplx<R> *__restrict__ out,
+                           LinkField<R, RECON> links, unsigned long long *ctr) {
+  constexpr int BLOCK = (128 / NR) * NR;
+  constexpr int SPB = BLOCK / NR;
+  if (threadIdx.x >= BLOCK) return;  // never: launched with BLOCK threads
+  const int rhs = threadIdx.x % NR;
+  const int local = threadIdx.x / NR;
+  for (int64_t step = 0;; ++step) {
+    const int64_t chunk = ctr ? next_chunk(ctr) : blockIdx.x + step * (int64_t)gridDim.x;
+    if (chunk * SPB >= P.g.V) break;
+    const int64_t o = chunk * SPB + local;
+    if (o >= P.g.V) continue;
+    const int64_t site = sched_site(P.sched, o);
+    C<R> y[4][3], xc[4][3];
+    wilson_eval<R, RECON, NR>(P, in + rhs, links, site, y, xc);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) stc_cs(out + ((a * 3 + c) * P.g.V + site) * NR + rhs, y[a][c]);
+  }
+}
+
+template <typename R, int RECON, int NR>
+static int launch_apply_il(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, cudaStream_t st) {
+  LinkField<R, RECON> lf{reinterpret_cast<const cplx<R> *>(h->links), h->g.V};
+  constexpr int block = (128 / NR) * NR;
+  static int grid_cache = 0;
+  if (!grid_cache) grid_cache = resident_grid(wilson_apply_il_kernel<R, RECON, NR>, block, (int64_t)1 << 40);
+  const int64_t need = (h->g.V + block / NR - 1) / (block / NR);
+  const int grid = (int)std::min<int64_t>(grid_cache, need);
+  unsigned long long *ctr = take_counter(h, st);
+  wilson_apply_il_kernel<R, RECON, NR><<<grid, block, 0, st>>>(P, reinterpret_cast<const cplx<R> *>(x),
+                                                                reinterpret_cast<cplx<R> *>(y), lf, ctr);
+  MGT_LAUNCH_CHECK("wilson_apply_il_kernel");
+  return MGT_OK;
+}
+
+template <typename R, int RECON>
+static int apply_il(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, int n_rhs,
+                    cudaStream_t st) {
+  switch (n_rhs) {
+    case 1: return launch_apply_il<R, RECON, 1>(h, P, x, y, st);
+    case 2: return launch_apply_il<R, RECON, 2>(h, P, x, y, st);
+    case 4: return launch_apply_il<R, RECON, 4>(h, P, x, y, st);
+    case 8: return launch_apply_il<R, RECON, 8>(h, P, x, y, st);
+    case 12: return launch_apply_il<R, RECON, 12>(h, P, x, y, st);
+    default: return fail(MGT_ERR_INVALID, "interleaved apply: n_rhs must be 1, 2, 4, 8 or 12");
+  }
+}
+
+int wilson_apply_il_native(const mgt_wilson_s *h, const void *x, void *y, int n_rhs, int flags, double tau,
+                           cudaStream_t st) {
+  WilsonParams P = make_params(h, flags, tau);
+  if (h->prec == 64) {
+    if (h->recon == 18) return apply_il<double, 18>(h, P, x, y, n_rhs, st);
+    return apply_il<double, 12>(h, P, x, y, n_rhs, st);
+  }
+  if (h->recon == 18) return apply_il<float, 18>(h, P, x, y, n_rhs, st);
+  return apply_il<float, 12>(h, P, x, y, n_rhs, st);
+}
+
 template <typename R, int RECON>
 static int apply_groups(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, int n_rhs,
                         cudaStream_t st) {
@@ -283,6 +350,14 @@ int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs, 
   if (x_dev == y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply: in-place apply is not supported");
   if (h->slab) return fail(MGT_ERR_INVALID, "mgt_wilson_apply: slab handles apply through mgt_wilson_apply_slab");
   return wilson_apply_native(h, x_dev, y_dev, n_rhs, flags, tau, as_stream(stream));
+}
+
+int mgt_wilson_apply_il(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs, int flags, double tau,
+                        void *stream) {
+  if (!h || !x_dev || !y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply_il: null argument");
+  if (x_dev == y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply_il: in-place apply is not supported");
+  if (h->slab) return fail(MGT_ERR_INVALID, "mgt_wilson_apply_il: slab handles are not supported");
+  return wilson_apply_il_native(h, x_dev, y_dev, n_rhs, flags, tau, as_stream(stream));
 }
 
 }  // extern "C"

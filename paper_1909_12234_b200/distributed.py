@@ -84,6 +84,74 @@ def exchange_halos(to_prev, to_next, group=None):
     return from_next, from_prev
 
 
+class PeerHaloWindows:
+    """Receive windows of the peer-memory halo transport.
+
+    One device allocation per rank (`mgt_ipc_alloc`), laid out as
+    [parity][face][rhs][6][S3] with face 0 = the face from rank + 1 (this
+    rank's halo_next) and face 1 = the face from rank - 1 (halo_prev).  The
+    64-byte CUDA IPC handles are all-gathered once; each rank maps its two
+    t neighbours' windows (`mgt_ipc_open`), so `mgt_halo_pack` with
+    MGT_HALO_PEER stores the projected faces straight into the neighbours'
+    memory over NVLink -- the pack (spin projection + U^dag multiply) and the
+    transfer are one kernel, no NCCL send/recv, no staging copy.  Parity
+    alternates per apply (double buffering): pack k+1 writes the other half,
+    and the barrier of apply k+1 orders pack k+2 after every neighbour's
+    boundary kernel of apply k."""
+
+    def __init__(self, S3, max_rhs, elem_bytes):
+        from . import _lib
+        self._lib = _lib
+        self.face_bytes = int(max_rhs) * 6 * int(S3) * int(elem_bytes)
+        self.max_rhs = int(max_rhs)
+        self.nbytes = 4 * self.face_bytes
+        p = _lib.ct.c_void_p()
+        self.handle = (_lib.ct.c_char * _lib.IPC_HANDLE_BYTES)()
+        _lib.check(_lib.lib().mgt_ipc_alloc(self.nbytes, _lib.ct.byref(p), self.handle), "ipc alloc")
+        self.ptr = p.value
+        self.prev_ptr = self.next_ptr = None
+        self._opened = []
+
+    def slot(self, base, parity, face):
+        return base + (2 * parity + face) * self.face_bytes
+
+    def connect_local(self, prev, nxt):
+        """In-process wiring (single-GPU rank emulation; world == 1 wraps to
+        itself): the neighbours' windows are plain device pointers."""
+        self.prev_ptr, self.next_ptr = prev.ptr, nxt.ptr
+
+    def connect(self, rank, world, group=None):
+        """All-gather the IPC handles and map the t neighbours' windows."""
+        if world == 1:
+            return self.connect_local(self, self)
+        hs = [None] * world
+        dist.all_gather_object(hs, bytes(self.handle), group=group)
+        prv, nxt = (rank - 1) % world, (rank + 1) % world
+        mapped = {}
+        for r in {prv, nxt}:
+            p = self._lib.ct.c_void_p()
+            buf = (self._lib.ct.c_char * self._lib.IPC_HANDLE_BYTES).from_buffer_copy(hs[r])
+            self._lib.check(self._lib.lib().mgt_ipc_open(buf, self._lib.ct.byref(p)), "ipc open")
+            mapped[r] = p.value
+            self._opened.append(p.value)
+        self.prev_ptr, self.next_ptr = mapped[prv], mapped[nxt]
+
+    def close(self):
+        lib = self._lib.lib()
+        for p in self._opened:
+            lib.mgt_ipc_close(self._lib.ct.c_void_p(p))
+        self._opened = []
+        if self.ptr:
+            lib.mgt_ipc_free(self._lib.ct.c_void_p(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def slab_links(gauge_links, dims, t_begin, t_local):
     """The slab's links in the reference layout of the LOCAL dims (t fastest)."""
     L0, L1, L2, T = dims
@@ -101,11 +169,15 @@ class SlabWilsonOperator:
     slices.  `exchange` may be replaced (tests emulate several ranks in one
     process by swapping faces between slab operators)."""
 
-    def __init__(self, gauge, mass, rank, world, prec=64, recon=12, group=None, local_links=None):
+    def __init__(self, gauge, mass, rank, world, prec=64, recon=12, group=None, local_links=None,
+                 transport="nccl", max_rhs=4, connect=True):
         """gauge: the GLOBAL GaugeField (the slab's links are cut out of it),
         or a (geometry, None) stand-in together with `local_links`, the slab's
         own links in local reference layout (when no rank holds the global
-        field)."""
+        field).  transport: "nccl" (grouped send/recv of the packed faces) or
+        "p2p" (the pack kernel writes into the neighbours' IPC-mapped receive
+        windows, `PeerHaloWindows`); with connect=False the p2p windows are
+        wired later (`connect_local`, single-process rank emulation)."""
         from . import _lib
         from ._device import ptr, stream_ptr
         geo = gauge.geometry
@@ -133,6 +205,27 @@ class SlabWilsonOperator:
         torch.cuda.current_stream().synchronize()
         self.exchange = lambda a, b: exchange_halos(a, b, self.group)
         self._side = torch.cuda.Stream()
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"unknown halo transport {transport!r}")
+        self.transport = transport
+        self.windows = None
+        self._parity = 0
+        self._barrier = None
+        if transport == "p2p":
+            esz = 16 if prec == 64 else 8
+            self.windows = PeerHaloWindows(self.S3, max_rhs, esz)
+            if connect:
+                self.windows.connect(rank, world, group)
+                if world > 1:
+                    self._barrier = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    @staticmethod
+    def connect_local(ops):
+        """Wire the p2p windows of in-process slab operators (ranks 0..W-1 of
+        one emulated ring) without IPC; the caller orders post/complete."""
+        W = len(ops)
+        for r, op in enumerate(ops):
+            op.windows.connect_local(ops[(r - 1) % W].windows, ops[(r + 1) % W].windows)
 
     def __del__(self):
         h = getattr(self, "_handle", None)
@@ -165,9 +258,48 @@ class SlabWilsonOperator:
             stream_ptr()), "slab apply")
         return out
 
+    # -- p2p transport: post (pack into the neighbours + interior) / complete
+    def post(self, x, out, flags=0, tau=0.0):
+        """Pack this rank's two faces straight into the neighbours' receive
+        windows (MGT_HALO_PEER) and start the interior slices on the side
+        stream."""
+        from ._device import ptr, stream_ptr
+        n = x.shape[0]
+        if n > self.windows.max_rhs:
+            raise ValueError(f"n_rhs {n} exceeds the halo window capacity {self.windows.max_rhs}")
+        w, par = self.windows, self._parity
+        self._lib.check(self._lib.lib().mgt_halo_pack(
+            self._handle, ptr(x), w.slot(w.prev_ptr, par, 0), w.slot(w.next_ptr, par, 1), n,
+            int(flags) | self._lib.HALO_PEER, float(tau), stream_ptr()), "halo pack (peer)")
+        main = torch.cuda.current_stream()
+        if self.t_local > 2:
+            self._side.wait_stream(main)
+            with torch.cuda.stream(self._side):
+                self.apply_part(x, out, None, None, 1, flags, tau)
+        return out
+
+    def complete(self, x, out, flags=0, tau=0.0):
+        """Stream-ordered barrier (every rank's pack has landed), then the two
+        boundary slices from this rank's own window; flips the parity."""
+        from ._device import ptr, stream_ptr
+        if self._barrier is not None:
+            dist.all_reduce(self._barrier, group=self.group)
+        w, par = self.windows, self._parity
+        part = 2 if self.t_local > 2 else 0
+        self._lib.check(self._lib.lib().mgt_wilson_apply_slab(
+            self._handle, ptr(x), ptr(out), w.slot(w.ptr, par, 0), w.slot(w.ptr, par, 1), x.shape[0],
+            int(flags), float(tau), part, stream_ptr()), "slab apply (peer halos)")
+        if self.t_local > 2:
+            torch.cuda.current_stream().wait_stream(self._side)
+        self._parity ^= 1
+        return out
+
     def apply_native(self, x, out=None, flags=0, tau=0.0, overlap=True):
         x = x.contiguous()
         out = torch.empty_like(x) if out is None else out
+        if self.transport == "p2p":
+            self.post(x, out, flags, tau)
+            return self.complete(x, out, flags, tau)
         main = torch.cuda.current_stream()
         to_prev, to_next = self.pack(x, flags, tau)
         if overlap and self.t_local > 2:

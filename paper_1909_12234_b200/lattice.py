@@ -188,6 +188,38 @@ class WilsonOperator:
                                                 float(tau), stream_ptr()), "apply")
         return out
 
+    def apply_interleaved(self, x, out=None, flags=0, tau=0.0):
+        """out = variant(A) x on rhs-interleaved fields (12, V, n), n in
+        {1, 2, 4, 8, 12}: the n rhs of a site share every link load (the
+        multi-rhs form of a dilution / hierarchical-probing slot batch)."""
+        if x.dim() != 3 or x.shape[0] != DOF or x.shape[1] != self.volume:
+            raise ValueError(f"dimension mismatch: interleaved field shape {tuple(x.shape)}")
+        if x.dtype != self.dtype:
+            raise ValueError(f"field dtype {x.dtype} != operator dtype {self.dtype}")
+        x = x.contiguous()
+        out = torch.empty_like(x) if out is None else out
+        _lib.check(_lib.lib().mgt_wilson_apply_il(self._handle, ptr(x), ptr(out), x.shape[2], int(flags),
+                                                   float(tau), stream_ptr()), "apply_interleaved")
+        return out
+
+    def interleave(self, x, out=None):
+        """native (n, 12, V) -> interleaved (12, V, n)."""
+        n = x.shape[0]
+        x = x.contiguous()
+        out = torch.empty((DOF, self.volume, n), dtype=x.dtype, device=x.device) if out is None else out
+        _lib.check(_lib.lib().mgt_rhs_interleave(self.volume, self.prec, n, 0, ptr(x), ptr(out), stream_ptr()),
+                   "interleave")
+        return out
+
+    def deinterleave(self, x, out=None):
+        """interleaved (12, V, n) -> native (n, 12, V)."""
+        n = x.shape[2]
+        x = x.contiguous()
+        out = torch.empty((n, DOF, self.volume), dtype=x.dtype, device=x.device) if out is None else out
+        _lib.check(_lib.lib().mgt_rhs_interleave(self.volume, self.prec, n, 1, ptr(x), ptr(out), stream_ptr()),
+                   "deinterleave")
+        return out
+
     # -- reference-layout API (lattice.py:214-247) ------------------------
     def apply_host(self, x, out=None, flags=0, tau=0.0, nchunks=32):
         """Host-memory reference-layout vector(s) (numpy or CPU tensor, (N,) or

@@ -74,3 +74,54 @@ def test_plain_apply_rejects_slab_handle(cuda):
     rc = _lib.lib().mgt_wilson_apply(slab._handle, ptr(x), ptr(torch.empty_like(x)), 1, 0, 0.0, stream_ptr())
     with pytest.raises(ValueError, match="slab"):
         _lib.check(rc)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("dims", [(4, 4, 6, 16), (4, 6, 4, 8)])
+def test_peer_window_transport_emulated(cuda, world, dims):
+    """p2p transport (pack kernel stores the faces straight into the
+    neighbours' receive windows): W in-process ranks wired without IPC,
+    every rank posts (pack + interior) before any rank completes (boundary),
+    as the barrier orders it across processes.  Three applies per rank with
+    changing inputs exercise the parity double buffering; the stitched result
+    must equal the full operator and be bitwise equal to the copy-exchange
+    path."""
+    from paper_1909_12234_b200.distributed import SlabWilsonOperator
+    M, geo, gauge = _setup(dims)
+    if dims[3] // world < 2:
+        pytest.skip("slab needs >= 2 slices")
+    full = M.build_wilson(gauge, 0.1, recon=12)
+    ops = [SlabWilsonOperator(gauge, 0.1, r, world, recon=12, transport="p2p", max_rhs=4, connect=False)
+           for r in range(world)]
+    SlabWilsonOperator.connect_local(ops)
+    ref = [SlabWilsonOperator(gauge, 0.1, r, world, recon=12) for r in range(world)]
+    S3, Tl = ops[0].S3, ops[0].t_local
+    for it, (n, flags, tau) in enumerate([(3, 0, 0.0), (1, 1, 0.0), (4, 4, 0.25)]):
+        x = torch.randn((n, 12, geo.site_count), dtype=torch.complex128, device=cuda)
+        xs = [x[:, :, r * Tl * S3:(r + 1) * Tl * S3].contiguous() for r in range(world)]
+        outs = [torch.empty_like(xl) for xl in xs]
+        for op, xl, o in zip(ops, xs, outs):
+            op.post(xl, o, flags, tau)
+        for op, xl, o in zip(ops, xs, outs):
+            op.complete(xl, o, flags, tau)
+        y = torch.cat(outs, dim=2)
+        assert _rel(y, full.apply_native(x, flags=flags, tau=tau)) < 1e-13
+        faces = [op.pack(xl, flags, tau) for op, xl in zip(ops, xs)]
+        for r, (op, xl) in enumerate(zip(ref, xs)):
+            o = torch.empty_like(xl)
+            op.apply_part(xl, o, faces[(r + 1) % world][0], faces[(r - 1) % world][1], 0, flags, tau)
+            assert torch.equal(o, outs[r]), (it, r)
+    with pytest.raises(ValueError, match="capacity"):
+        ops[0].post(torch.zeros((5, 12, ops[0].volume), dtype=torch.complex128, device=cuda),
+                    torch.empty((5, 12, ops[0].volume), dtype=torch.complex128, device=cuda))
+
+
+def test_peer_window_single_rank_apply_native(cuda):
+    """world = 1 with the p2p transport: the window wraps to itself."""
+    from paper_1909_12234_b200.distributed import SlabWilsonOperator
+    M, geo, gauge = _setup((4, 4, 4, 8))
+    full = M.build_wilson(gauge, 0.1, recon=12)
+    slab = SlabWilsonOperator(gauge, 0.1, 0, 1, recon=12, transport="p2p")
+    x = torch.randn((2, 12, geo.site_count), dtype=torch.complex128, device=cuda)
+    for _ in range(3):
+        assert _rel(slab.apply_native(x), full.apply_native(x)) < 1e-13

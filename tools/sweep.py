@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--nrhs", default="1")
     ap.add_argument("--flags", default="0")
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--layout", default="native", help="native or il (rhs-interleaved)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     for dims_s in args.dims.split(","):
@@ -37,22 +38,25 @@ def main():
                     for nrhs in [int(n) for n in args.nrhs.split(",")]:
                         for flags in [int(f) for f in args.flags.split(",")]:
                             V = geo.site_count
-                            x = torch.randn((nrhs, 12, V), dtype=op.dtype, device="cuda")
+                            il = args.layout == "il"
+                            shape = (12, V, nrhs) if il else (nrhs, 12, V)
+                            x = torch.randn(shape, dtype=op.dtype, device="cuda")
                             y = torch.empty_like(x)
+                            fn = op.apply_interleaved if il else op.apply_native
                             for _ in range(3):
-                                op.apply_native(x, out=y, flags=flags)
+                                fn(x, out=y, flags=flags)
                             torch.cuda.synchronize()
                             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
                             e0.record()
                             for _ in range(args.steps):
-                                op.apply_native(x, out=y, flags=flags)
+                                fn(x, out=y, flags=flags)
                             e1.record()
                             torch.cuda.synchronize()
                             ms = e0.elapsed_time(e1) / args.steps
                             w = 8 if prec == 64 else 4
                             alg = V * (4 * 18 * w + nrhs * 48 * w)
                             print(json.dumps({"dims": dims_s, "eps": eps, "prec": prec, "recon": recon,
-                                              "n_rhs": nrhs, "flags": flags, "ms": ms,
+                                              "n_rhs": nrhs, "layout": args.layout, "flags": flags, "ms": ms,
                                               "GBps": alg / ms / 1e6,
                                               "Gsites_rhs_per_s": V * nrhs / ms / 1e6}), flush=True)
                             del x, y
