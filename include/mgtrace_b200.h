@@ -48,6 +48,9 @@ extern "C" {
  * the neighbouring ranks (CUDA IPC over NVLink); the pack kernel stores the
  * projected faces straight into them and fences system-wide. */
 #define MGT_HALO_PEER 8
+/* mgt_bicgstab_solve only: solve the full system instead of the even-odd
+ * Schur complement (the default whenever every extent is even). */
+#define MGT_SOLVE_FULL 16
 
 typedef struct mgt_wilson_s *mgt_wilson_t;
 
@@ -106,6 +109,20 @@ int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs,
  * (LatticeOperator.apply on an (N, k) block, lattice.py:214-217). */
 int mgt_wilson_apply_il(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs,
                         int flags, double tau, void *stream);
+
+/* Even-odd (checkerboard) form, every extent even.  Parity fields are
+ * (n_rhs, 12, V/2) with cb index = native site >> 1.  split/merge convert a
+ * native field to/from its even and odd halves; mgt_wilson_schur_apply
+ * applies the even-site Schur complement
+ *   S = G_out [ Dg - 1/4 H_eo Dg^-1 H_oe ] G_in   (Dg = 4 + m0 +- i tau)
+ * of the flags/tau variant.  mgt_bicgstab_solve runs on S (full residual
+ * ||b - A x|| <= tol ||b|| exactly as krylov.py:78-85 tests it). */
+int mgt_wilson_eo_split(mgt_wilson_t h, const void *x_full_dev, void *x_even_dev,
+                        void *x_odd_dev, int n_rhs, void *stream);
+int mgt_wilson_eo_merge(mgt_wilson_t h, const void *x_even_dev, const void *x_odd_dev,
+                        void *x_full_dev, int n_rhs, void *stream);
+int mgt_wilson_schur_apply(mgt_wilson_t h, const void *x_even_dev, void *y_even_dev,
+                           int n_rhs, int flags, double tau, void *stream);
 
 /* Host-buffer apply: y_host = variant(A) x_host for n_rhs REFERENCE-layout
  * complex128 vectors in host memory (LatticeOperator.apply with numpy

@@ -22,6 +22,7 @@ G5_IN = 1
 G5_OUT = 2
 DAGGER = 4
 HALO_PEER = 8
+SOLVE_FULL = 16
 IPC_HANDLE_BYTES = 64
 
 _lock = threading.Lock()
@@ -46,6 +47,9 @@ _SIGNATURES = {
     "mgt_wilson_apply": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp]),
     "mgt_wilson_apply_il": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp]),
     "mgt_rhs_interleave": (ct.c_int, [ct.c_int64, ct.c_int, ct.c_int, ct.c_int, vp, vp, vp]),
+    "mgt_wilson_eo_split": (ct.c_int, [vp, vp, vp, vp, ct.c_int, vp]),
+    "mgt_wilson_eo_merge": (ct.c_int, [vp, vp, vp, vp, ct.c_int, vp]),
+    "mgt_wilson_schur_apply": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp]),
     "mgt_ipc_alloc": (ct.c_int, [ct.c_size_t, ct.POINTER(ct.c_void_p), vp]),
     "mgt_ipc_free": (ct.c_int, [vp]),
     "mgt_ipc_open": (ct.c_int, [vp, ct.POINTER(ct.c_void_p)]),

@@ -22,6 +22,7 @@
 #include <tuple>
 #include <vector>
 
+#include "eo_core.cuh"
 #include "handle.cuh"
 #include "reduce.cuh"
 
@@ -31,16 +32,18 @@ enum : int { ST_RUN = 0, ST_CONV = 1, ST_BREAK = 2, ST_MAXIT = 3, ST_RESTART = 4
 
 struct BiState {
   C<double> rho, alpha, omega, beta, dotq;
-  double b2, r2, s2, true_r2, tol2;
+  double b2, r2, s2, true_r2, tol2, bfull2;
   int status, half, iters, maxit, matvecs, reason, pad0, pad1;
 };
 
 // Workspace: fields of NR rhs each (native layout) + reduction scratch.
 struct BiWS {
   double2 *r, *rhat, *p, *v, *s, *t, *x, *b;
+  double2 *be, *bo, *tmp;    // even-odd solve: b_e, b_o, odd-parity scratch
   double *partials;
   unsigned *ticket;
-  unsigned long long *ctr;  // dynamic chunk counter (dslash kernels), reset by their last block
+  unsigned long long *ctr;   // dynamic chunk counter (dslash kernels), reset by their last block
+  unsigned long long *ctr2;  // counter of the eo first-half kernels, reset by the following kernel
   BiState *st;
 };
 
@@ -71,11 +74,93 @@ __device__ __forceinline__ bool cfinite(C<double> a) { return isfinite(a.re) && 
   for (int64_t chunk = next_chunk(CTR), o = chunk * (M).SPB + (M).local; chunk < NCH; \
        chunk = next_chunk(CTR), o = chunk * (M).SPB + (M).local)
 
+// Last-block scalar recurrences of the stencil kernels (shared by the full
+// and the even-odd kernels).  They also reset the chunk counters.
+template <int NR>
+__device__ __forceinline__ void k1_finish(const BiWS &w, int64_t nchunks) {
+  double out[NR * 2];
+  reduce_finish_n<NR * 2>(w.partials, nchunks, w.ticket, out);
+  if (threadIdx.x == 0) {
+    *w.ctr = 0ull;
+    *w.ctr2 = 0ull;
+  }
+  const int r = threadIdx.x;
+  if (r < NR && w.st[r].status == ST_RUN) {
+    BiState &s = w.st[r];
+    C<double> sigma(out[2 * r], out[2 * r + 1]);
+    s.matvecs += 1;
+    if (czero(sigma) || !cfinite(sigma)) {
+      s.status = ST_BREAK;
+      s.reason = 2;
+    } else {
+      s.alpha = cdiv(s.rho, sigma);
+    }
+  }
+}
+
+template <int NR>
+__device__ __forceinline__ void k3_finish(const BiWS &w, int64_t nchunks) {
+  double out[NR * 3];
+  reduce_finish_n<NR * 3>(w.partials, nchunks, w.ticket, out);
+  if (threadIdx.x == 0) {
+    *w.ctr = 0ull;
+    *w.ctr2 = 0ull;
+  }
+  const int r = threadIdx.x;
+  if (r < NR && w.st[r].status == ST_RUN) {
+    BiState &s = w.st[r];
+    C<double> ts(out[3 * r], out[3 * r + 1]);
+    const double tt = out[3 * r + 2];
+    s.matvecs += 1;
+    if (s.half) {
+      s.omega = C<double>(0.0, 0.0);
+    } else if (tt == 0.0 || !isfinite(tt)) {
+      s.status = ST_BREAK;
+      s.reason = 2;
+    } else {
+      s.omega = C<double>(ts.re / tt, ts.im / tt);
+    }
+  }
+}
+
+template <int NR>
+__device__ __forceinline__ void resid_finish(const BiWS &w, int64_t nchunks) {
+  double out[NR];
+  reduce_finish_n<NR>(w.partials, nchunks, w.ticket, out);
+  if (threadIdx.x == 0) {
+    *w.ctr = 0ull;
+    *w.ctr2 = 0ull;
+  }
+  const int r = threadIdx.x;
+  if (r < NR) {
+    BiState &s = w.st[r];
+    const int st = s.status;
+    if (st == ST_CONV || st == ST_MAXIT || st == ST_BREAK) {
+      s.true_r2 = out[r];
+      s.matvecs += 1;
+      if (s.true_r2 <= s.tol2) {
+        s.status = ST_DONE;
+        s.reason = 0;
+      } else if (st == ST_CONV && s.iters < s.maxit) {
+        s.status = ST_RESTART;  // recursion drifted from the true residual
+      } else {
+        s.status = ST_DONE;
+        if (s.reason == 0) s.reason = 1;
+      }
+    }
+  }
+}
+
+template <int NR>
+__device__ __forceinline__ bool resid_active(int st) {
+  return st == ST_CONV || st == ST_MAXIT || st == ST_BREAK;
+}
+
 // ---------------------------------------------------------------------------
 // init: b -> workspace, r = rhat = p = b, x = 0, |b|^2
 template <int NR>
 __global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *__restrict__ b, BiWS w, double tol,
-                                                     int maxit) {
+                                                     int maxit, int use_bfull) {
   RhsMap<NR> m;
   double acc[1] = {0.0};
   MGT_SITE_LOOP(m, V) {
@@ -99,11 +184,13 @@ __global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *_
     if (r < NR) {
       BiState &s = w.st[r];
       const double b2 = out[r];
-      s.b2 = b2;
+      // even-odd: the stopping norm is the FULL right-hand side's (the Schur
+      // residual is the full residual), set by bi_eo_split
+      s.b2 = use_bfull ? s.bfull2 : b2;
       s.r2 = b2;
       s.s2 = b2;
       s.true_r2 = b2;
-      s.tol2 = tol * tol * b2;
+      s.tol2 = tol * tol * s.b2;
       s.rho = C<double>(b2, 0.0);
       s.alpha = C<double>(1.0, 0.0);
       s.omega = C<double>(1.0, 0.0);
@@ -147,23 +234,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<
     }
     chunk_publish<NR, 2>(acc, w.partials + chunk * NR * 2);
   }
-  if (last_block(w.ticket)) {
-    double out[NR * 2];
-    reduce_finish_n<NR * 2>(w.partials, nchunks, w.ticket, out);
-    if (threadIdx.x == 0) *w.ctr = 0ull;
-    const int r = threadIdx.x;
-    if (r < NR && w.st[r].status == ST_RUN) {
-      BiState &s = w.st[r];
-      C<double> sigma(out[2 * r], out[2 * r + 1]);
-      s.matvecs += 1;
-      if (czero(sigma) || !cfinite(sigma)) {
-        s.status = ST_BREAK;
-        s.reason = 2;
-      } else {
-        s.alpha = cdiv(s.rho, sigma);
-      }
-    }
-  }
+  if (last_block(w.ticket)) k1_finish<NR>(w, nchunks);
 }
 
 // K2: s = r - alpha v ; |s|^2
@@ -226,26 +297,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<
     }
     chunk_publish<NR, 3>(acc, w.partials + chunk * NR * 3);
   }
-  if (last_block(w.ticket)) {
-    double out[NR * 3];
-    reduce_finish_n<NR * 3>(w.partials, nchunks, w.ticket, out);
-    if (threadIdx.x == 0) *w.ctr = 0ull;
-    const int r = threadIdx.x;
-    if (r < NR && w.st[r].status == ST_RUN) {
-      BiState &s = w.st[r];
-      C<double> ts(out[3 * r], out[3 * r + 1]);
-      const double tt = out[3 * r + 2];
-      s.matvecs += 1;
-      if (s.half) {
-        s.omega = C<double>(0.0, 0.0);
-      } else if (tt == 0.0 || !isfinite(tt)) {
-        s.status = ST_BREAK;
-        s.reason = 2;
-      } else {
-        s.omega = C<double>(ts.re / tt, ts.im / tt);
-      }
-    }
-  }
+  if (last_block(w.ticket)) k3_finish<NR>(w, nchunks);
 }
 
 // K4: x += alpha p + omega s ; r = s - omega t ; rho' = (rhat, r), |r|^2
@@ -350,29 +402,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
     }
     chunk_publish<NR, 1>(acc, w.partials + chunk * NR);
   }
-  if (last_block(w.ticket)) {
-    double out[NR];
-    reduce_finish_n<NR>(w.partials, nchunks, w.ticket, out);
-    if (threadIdx.x == 0) *w.ctr = 0ull;
-    const int r = threadIdx.x;
-    if (r < NR) {
-      BiState &s = w.st[r];
-      const int st = s.status;
-      if (st == ST_CONV || st == ST_MAXIT || st == ST_BREAK) {
-        s.true_r2 = out[r];
-        s.matvecs += 1;
-        if (s.true_r2 <= s.tol2) {
-          s.status = ST_DONE;
-          s.reason = 0;
-        } else if (st == ST_CONV && s.iters < s.maxit) {
-          s.status = ST_RESTART;  // recursion drifted from the true residual
-        } else {
-          s.status = ST_DONE;
-          if (s.reason == 0) s.reason = 1;
-        }
-      }
-    }
-  }
+  if (last_block(w.ticket)) resid_finish<NR>(w, nchunks);
 }
 
 // Restart for rhs flagged ST_RESTART: rhat = p = r (r holds the true residual)
@@ -435,6 +465,232 @@ __global__ void __launch_bounds__(kRedBlock) bi_final(int64_t V, double2 *__rest
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Even-odd (Schur) solve, eo_core.cuh.  Fields in the workspace are parity
+// fields of Vh sites; the BLAS-1 kernels above run unchanged with V = Vh.
+struct BiEo {
+  EoGeom E;
+  Sched sh;  // slab schedule over cb indices
+  EoRoles R;
+};
+
+// b (full) -> b_e, b_o, tmp = u_o = Dg^-1 G_out b_o ; |b|^2 of the full rhs
+template <int NR>
+__global__ void __launch_bounds__(kRedBlock) bi_eo_split(BiEo X, const double2 *__restrict__ b, BiWS w, double g5out) {
+  RhsMap<NR> m;
+  const int64_t Vh = X.E.Vh, V = X.E.g.V;
+  const C<double> iu(X.R.iu_re, X.R.iu_im), id(X.R.id_re, X.R.id_im);
+  double acc[1] = {0.0};
+  MGT_SITE_LOOP(m, Vh) {
+    int x[4];
+    const int64_t fe = eo_coords(X.E, 0, o, x);
+    const int64_t fo = eo_coords(X.E, 1, o, x);
+    const double2 *B = b + (int64_t)m.rhs * 12 * V;
+    const int64_t hb = (int64_t)m.rhs * 12 * Vh + o;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+      const C<double> e = ldc(B + (int64_t)k * V + fe), od = ldc(B + (int64_t)k * V + fo);
+      stc(w.be + hb + (int64_t)k * Vh, e);
+      stc(w.bo + hb + (int64_t)k * Vh, od);
+      const C<double> u = k < 6 ? iu * od : id * (g5out * od);
+      stc(w.tmp + hb + (int64_t)k * Vh, u);
+      acc[0] += cabs2(e) + cabs2(od);
+    }
+  }
+  if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
+    double out[NR];
+    reduce_finish<NR>(w.partials, w.ticket, out);
+    if (threadIdx.x < NR) w.st[threadIdx.x].bfull2 = out[threadIdx.x];
+  }
+}
+
+// bh_e = G_out [ G_out b_e + 1/2 H_eo u_o ]  -> w.b
+template <int NR, int RECON>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_eo_rhs(BiEo X, LinkField<double, RECON> le,
+                                                          LinkField<double, RECON> lo, BiWS w) {
+  RhsMap<NR> m;
+  const int64_t Vh = X.E.Vh;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  MGT_SITE_LOOP(m, Vh) {
+    const int64_t c = sched_site(X.sh, o);
+    C<double> y[4][3], cc[4][3];
+    eo_eval<double, RECON>(X.E, 0, X.R.rhs, w.tmp + off, w.be + off, le, lo, c, y, cc);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) stc(w.b + off + (int64_t)(a * 3 + k) * Vh + c, y[a][k]);
+  }
+}
+
+// first half of S: tmp = Dg^-1 H_oe (G_in f), f = p / s / x (mode 0: rhs
+// still iterating, mode 1: rhs whose true residual is due)
+template <int NR, int RECON>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<double, RECON> le,
+                                                            LinkField<double, RECON> lo, const double2 *f, BiWS w,
+                                                            int mode) {
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) any |= mode ? resid_active<NR>(w.st[r].status) : w.st[r].status == ST_RUN;
+  if (!any) return;
+  RhsMap<NR> m;
+  const int stm = w.st[m.rhs].status;
+  const bool act = mode ? resid_active<NR>(stm) : stm == ST_RUN;
+  const int64_t Vh = X.E.Vh;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  int64_t nchunks = 0;
+  MGT_DYN_LOOP(m, Vh, w.ctr2, nchunks) {
+    if (act && o < Vh) {
+      const int64_t c = sched_site(X.sh, o);
+      C<double> y[4][3], cc[4][3];
+      eo_eval<double, RECON>(X.E, 1, X.R.first, f + off, nullptr, lo, le, c, y, cc);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) stc(w.tmp + off + (int64_t)(a * 3 + k) * Vh + c, y[a][k]);
+    }
+  }
+}
+
+// K1 (eo): v = S p = G_out [ Dg G_in p - 1/4 H_eo tmp ] ; sigma = (rhat, v)
+template <int NR, int RECON>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<double, RECON> le,
+                                                         LinkField<double, RECON> lo, BiWS w) {
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool run_me = w.st[m.rhs].status == ST_RUN;
+  const int64_t Vh = X.E.Vh;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  int64_t nchunks = 0;
+  MGT_DYN_LOOP(m, Vh, w.ctr, nchunks) {
+    double acc[2] = {0.0, 0.0};
+    if (run_me && o < Vh) {
+      const int64_t c = sched_site(X.sh, o);
+      C<double> y[4][3], cc[4][3];
+      eo_eval<double, RECON>(X.E, 0, X.R.second, w.tmp + off, w.p + off, le, lo, c, y, cc);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int64_t q = off + (int64_t)(a * 3 + k) * Vh + c;
+          stc(w.v + q, y[a][k]);
+          C<double> rh = ldc(w.rhat + q);
+          acc[0] += rh.re * y[a][k].re + rh.im * y[a][k].im;
+          acc[1] += rh.re * y[a][k].im - rh.im * y[a][k].re;
+        }
+    }
+    chunk_publish<NR, 2>(acc, w.partials + chunk * NR * 2);
+  }
+  if (last_block(w.ticket)) k1_finish<NR>(w, nchunks);
+}
+
+// K3 (eo): t = S s ; (t, s), |t|^2
+template <int NR, int RECON>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_k3_eo(BiEo X, LinkField<double, RECON> le,
+                                                         LinkField<double, RECON> lo, BiWS w) {
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool run_me = w.st[m.rhs].status == ST_RUN;
+  const int64_t Vh = X.E.Vh;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  int64_t nchunks = 0;
+  MGT_DYN_LOOP(m, Vh, w.ctr, nchunks) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    if (run_me && o < Vh) {
+      const int64_t c = sched_site(X.sh, o);
+      C<double> y[4][3], cc[4][3];
+      eo_eval<double, RECON>(X.E, 0, X.R.second, w.tmp + off, w.s + off, le, lo, c, y, cc);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          stc(w.t + off + (int64_t)(a * 3 + k) * Vh + c, y[a][k]);
+          const C<double> tt = y[a][k], ss = cc[a][k];
+          acc[0] += tt.re * ss.re + tt.im * ss.im;
+          acc[1] += tt.re * ss.im - tt.im * ss.re;
+          acc[2] += cabs2(tt);
+        }
+    }
+    chunk_publish<NR, 3>(acc, w.partials + chunk * NR * 3);
+  }
+  if (last_block(w.ticket)) k3_finish<NR>(w, nchunks);
+}
+
+// true Schur residual r = bh - S x (= the full residual, odd rows exact)
+template <int NR, int RECON>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_resid_eo(BiEo X, LinkField<double, RECON> le,
+                                                            LinkField<double, RECON> lo, BiWS w) {
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) any |= resid_active<NR>(w.st[r].status);
+  if (!any) return;
+  RhsMap<NR> m;
+  const bool act_me = resid_active<NR>(w.st[m.rhs].status);
+  const int64_t Vh = X.E.Vh;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  int64_t nchunks = 0;
+  MGT_DYN_LOOP(m, Vh, w.ctr, nchunks) {
+    double acc[1] = {0.0};
+    if (act_me && o < Vh) {
+      const int64_t c = sched_site(X.sh, o);
+      C<double> y[4][3], cc[4][3];
+      eo_eval<double, RECON>(X.E, 0, X.R.second, w.tmp + off, w.x + off, le, lo, c, y, cc);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int64_t q = off + (int64_t)(a * 3 + k) * Vh + c;
+          C<double> rr = ldc(w.b + q) - y[a][k];
+          stc(w.r + q, rr);
+          acc[0] += cabs2(rr);
+        }
+    }
+    chunk_publish<NR, 1>(acc, w.partials + chunk * NR);
+  }
+  if (last_block(w.ticket)) resid_finish<NR>(w, nchunks);
+}
+
+// x_full: even sites <- x_e, odd sites <- x_o = G_in Dg^-1 [G_out b_o + 1/2 H_oe G_in x_e];
+// q = vdot(b, x) over the full lattice (trace.py:104)
+template <int NR, int RECON>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_eo_final(BiEo X, LinkField<double, RECON> le,
+                                                            LinkField<double, RECON> lo, double2 *__restrict__ xout,
+                                                            BiWS w) {
+  RhsMap<NR> m;
+  const int64_t Vh = X.E.Vh, V = X.E.g.V;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  double2 *XO = xout + (int64_t)m.rhs * 12 * V;
+  double acc[2] = {0.0, 0.0};
+  MGT_SITE_LOOP(m, Vh) {
+    int x[4];
+    const int64_t fe = eo_coords(X.E, 0, o, x);
+    const int64_t fo = eo_coords(X.E, 1, o, x);
+    C<double> y[4][3], cc[4][3];
+    eo_eval<double, RECON>(X.E, 1, X.R.recon, w.x + off, w.bo + off, lo, le, o, y, cc);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int ck = a * 3 + k;
+        const C<double> xe = ldc(w.x + off + (int64_t)ck * Vh + o), bev = ldc(w.be + off + (int64_t)ck * Vh + o);
+        stc(XO + (int64_t)ck * V + fe, xe);
+        stc(XO + (int64_t)ck * V + fo, y[a][k]);
+        const C<double> bov = cc[a][k], xo = y[a][k];
+        acc[0] += bev.re * xe.re + bev.im * xe.im + bov.re * xo.re + bov.im * xo.im;
+        acc[1] += bev.re * xe.im - bev.im * xe.re + bov.re * xo.im - bov.im * xo.re;
+      }
+  }
+  if (reduce_publish<NR, 2>(acc, w.partials, w.ticket)) {
+    double out[NR * 2];
+    reduce_finish<NR * 2>(w.partials, w.ticket, out);
+    const int r = threadIdx.x;
+    if (r < NR) {
+      w.st[r].dotq = C<double>(out[2 * r], out[2 * r + 1]);
+      w.st[r].matvecs += 1;  // the odd-site reconstruction (half of A)
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -447,7 +703,7 @@ struct WSLayout {
 
 static WSLayout ws_layout(int64_t V) {
   WSLayout L;
-  L.field = align_up((size_t)kMaxGroup * 12 * V * sizeof(double2), 256);
+  L.field = align_up((size_t)kMaxGroup * 12 * V * sizeof(double2), 512);
   // static-grid kernels: one NR*NV slot per block; dynamic kernels: one per
   // chunk of 128 / NR sites (NR = 4 is the largest)
   const size_t per_block = (size_t)kNumSMs * 16 * kMaxGroup * 4;
@@ -457,17 +713,20 @@ static WSLayout ws_layout(int64_t V) {
   return L;
 }
 
-static BiWS carve(char *q, const WSLayout &Lw) {
+static BiWS carve(char *q, const WSLayout &Lw, bool eo = false) {
   BiWS w;
-  double2 **f[8] = {&w.r, &w.rhat, &w.p, &w.v, &w.s, &w.t, &w.x, &w.b};
-  for (auto *pp : f) {
-    *pp = (double2 *)q;
-    q += Lw.field;
-  }
+  double2 **f[11] = {&w.r, &w.rhat, &w.p, &w.v, &w.s, &w.t, &w.x, &w.b, &w.be, &w.bo, &w.tmp};
+  // full solve: 8 fields of the slot size; even-odd: 11 parity fields of half a slot
+  const size_t step = eo ? Lw.field / 2 : Lw.field;
+  char *f0 = q;
+  for (int i = 0; i < (eo ? 11 : 8); ++i) *f[i] = (double2 *)(f0 + i * step);
+  if (!eo) w.be = w.bo = w.tmp = nullptr;
+  q += 8 * Lw.field;
   w.partials = (double *)q;
   q += Lw.partials;
   w.ticket = (unsigned *)q;
   w.ctr = (unsigned long long *)(q + 8);
+  w.ctr2 = (unsigned long long *)(q + 16);
   q += 256;
   w.st = (BiState *)q;
   return w;
@@ -477,10 +736,10 @@ static BiWS carve(char *q, const WSLayout &Lw) {
 // (workspace, NR, RECON, operator variant).
 struct GraphKey {
   const void *h, *ws;
-  int nr, recon, flags;
+  int nr, recon, flags, eo;
   double tau;
   bool operator<(const GraphKey &o) const {
-    return std::tie(h, ws, nr, recon, flags, tau) < std::tie(o.h, o.ws, o.nr, o.recon, o.flags, o.tau);
+    return std::tie(h, ws, nr, recon, flags, eo, tau) < std::tie(o.h, o.ws, o.nr, o.recon, o.flags, o.eo, o.tau);
   }
 };
 static std::mutex g_graph_mu;
@@ -513,25 +772,70 @@ static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &l
 }
 
 template <int NR, int RECON>
+static int launch_chunk_eo(const BiEo &X, const LinkField<double, RECON> &le, const LinkField<double, RECON> &lo,
+                           const BiWS &w, int gd, int g1, int grid, cudaStream_t st) {
+  const int64_t Vh = X.E.Vh;
+  for (int it = 0; it < kChunk; ++it) {
+    bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
+    bi_k1_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    bi_k2<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w, 0);
+    bi_k3_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    bi_k4<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    bi_k5<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
+  }
+  return MGT_OK;
+}
+
+template <int NR, int RECON>
 static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b, double2 *x,
                        char *ws, const WSLayout &Lw, double tol, int max_iter, int64_t *report, double *relres,
-                       double *dot_out, cudaStream_t st) {
+                       double *dot_out, bool eo, cudaStream_t st) {
   const int64_t V = h->g.V;
-  BiWS w = carve(ws, Lw);
+  const int64_t Vs = eo ? V / 2 : V;  // sites of the solved system
+  BiWS w = carve(ws, Lw, eo);
   LinkField<double, RECON> lf{reinterpret_cast<const double2 *>(h->links), V};
-  static int g_dsl = 0, g_str = 0;  // resident grids, per template instance
+  // even-odd pieces
+  BiEo X;
+  LinkField<double, RECON> le{nullptr, V / 2}, lo{nullptr, V / 2};
+  if (eo) {
+    X.E = make_eo_geom(h->g, h->antiperiodic);
+    Geom gh = h->g;
+    gh.L[2] /= 2;
+    gh.V /= 2;
+    gh.stride[1] /= 2;
+    gh.stride[0] /= 2;
+    gh.stride[3] /= 2;
+    X.sh = make_sched(gh, 1024, h->slab_bytes);
+    X.R = make_eo_roles(P);
+    le.p = reinterpret_cast<const double2 *>(h->links_cb);
+    lo.p = reinterpret_cast<const double2 *>((const char *)h->links_cb + h->link_bytes / 2);
+  }
+  static int g_dsl = 0, g_str = 0, g_e1 = 0, g_e2 = 0;  // resident grids, per template instance
   if (!g_dsl) g_dsl = resident_grid(bi_k1<NR, RECON>, kRedBlock, (int64_t)1 << 40);
   if (!g_str) g_str = resident_grid(bi_k4<NR>, kRedBlock, (int64_t)1 << 40);
-  const int64_t need = (V + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
-  const int gd = (int)std::min<int64_t>(g_dsl, need), grid = (int)std::min<int64_t>(g_str, need);
-  MGT_CUDA(cudaMemsetAsync(w.ticket, 0, 16, st));  // ticket and chunk counter
-  bi_init<NR><<<grid, kRedBlock, 0, st>>>(V, b, w, tol, max_iter);
+  if (eo && !g_e1) g_e1 = resident_grid(bi_eo_first<NR, RECON>, kRedBlock, (int64_t)1 << 40);
+  if (eo && !g_e2) g_e2 = resident_grid(bi_k1_eo<NR, RECON>, kRedBlock, (int64_t)1 << 40);
+  const int64_t need = (Vs + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
+  const int grid = (int)std::min<int64_t>(g_str, need);
+  const int gd = (int)std::min<int64_t>(eo ? g_e2 : g_dsl, need);
+  const int g1 = eo ? (int)std::min<int64_t>(g_e1, need) : 0;
+  MGT_CUDA(cudaMemsetAsync(w.ticket, 0, 24, st));  // ticket and chunk counters
+  if (eo) {
+    bi_eo_split<NR><<<grid, kRedBlock, 0, st>>>(X, b, w, P.g5out);
+    bi_eo_rhs<NR, RECON><<<grid, kRedBlock, 0, st>>>(X, le, lo, w);
+    bi_init<NR><<<grid, kRedBlock, 0, st>>>(Vs, w.b, w, tol, max_iter, 1);
+    note_launch(3);
+  } else {
+    bi_init<NR><<<grid, kRedBlock, 0, st>>>(V, b, w, tol, max_iter, 0);
+    note_launch(1);
+  }
   MGT_LAUNCH_CHECK("bi_init");
 
   cudaGraphExec_t exec = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    GraphKey key{h, ws, NR, RECON, flags, tau};
+    GraphKey key{h, ws, NR, RECON, flags, eo ? 1 : 0, tau};
     auto it = g_graphs.find(key);
     if (it != g_graphs.end()) {
       exec = it->second;
@@ -540,7 +844,10 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
       MGT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
       cudaGraph_t graph;
       MGT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-      launch_chunk<NR, RECON>(P, lf, w, gd, grid, cap);
+      if (eo)
+        launch_chunk_eo<NR, RECON>(X, le, lo, w, gd, g1, grid, cap);
+      else
+        launch_chunk<NR, RECON>(P, lf, w, gd, grid, cap);
       cudaError_t e = cudaStreamEndCapture(cap, &graph);
       cudaStreamDestroy(cap);
       if (e != cudaSuccess) return cuda_fail(e, "bicgstab graph capture");
@@ -550,12 +857,13 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
       g_graphs[key] = exec;
     }
   }
+  const int per_iter = eo ? 7 : 5;
   // pinned per-thread mailbox: concurrent solves on several streams may share a handle
   static thread_local int *hf = nullptr;
   if (!hf) MGT_CUDA(cudaMallocHost((void **)&hf, 64 * sizeof(int)));
   for (int round = 0; round < 1000000; ++round) {
     MGT_CUDA(cudaGraphLaunch(exec, st));
-    note_launch(5 * kChunk);
+    note_launch(per_iter * kChunk);
     MGT_CUDA(cudaMemcpyAsync(hf, &w.st[0].status, sizeof(int), cudaMemcpyDeviceToHost, st));
     for (int r = 1; r < NR; ++r)
       MGT_CUDA(cudaMemcpyAsync(hf + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -563,8 +871,14 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
     bool running = false;
     for (int r = 0; r < NR; ++r) running |= (hf[r] == ST_RUN);
     if (running) continue;
-    bi_resid<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
-    bi_restart<NR><<<grid, kRedBlock, 0, st>>>(V, w);
+    if (eo) {
+      bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.x, w, 1);
+      bi_resid_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+      note_launch(1);
+    } else {
+      bi_resid<NR, RECON><<<gd, kRedBlock, 0, st>>>(P, lf, w);
+    }
+    bi_restart<NR><<<grid, kRedBlock, 0, st>>>(Vs, w);
     note_launch(2);
     MGT_LAUNCH_CHECK("bicgstab residual");
     for (int r = 0; r < NR; ++r)
@@ -574,7 +888,11 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
     for (int r = 0; r < NR; ++r) again |= (hf[r] == ST_RUN);
     if (!again) break;
   }
-  bi_final<NR><<<grid, kRedBlock, 0, st>>>(V, x, w);
+  if (eo)
+    bi_eo_final<NR, RECON><<<grid, kRedBlock, 0, st>>>(X, le, lo, x, w);
+  else
+    bi_final<NR><<<grid, kRedBlock, 0, st>>>(V, x, w);
+  note_launch(1);
   MGT_LAUNCH_CHECK("bi_final");
   std::vector<BiState> hs(NR);
   MGT_CUDA(cudaMemcpyAsync(hs.data(), w.st, NR * sizeof(BiState), cudaMemcpyDeviceToHost, st));
@@ -618,6 +936,13 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs
   if (max_iter < 1) return fail(MGT_ERR_INVALID, "max_iter must be >= 1");
   if (n_rhs < 1) return fail(MGT_ERR_INVALID, "n_rhs must be >= 1");
   cudaStream_t st = as_stream(stream);
+  // even-odd Schur solve unless disabled (handle / MGT_SOLVE_FULL) or an extent is odd
+  const bool eo = h->solve_eo && !(flags & MGT_SOLVE_FULL) && eo_available(h);
+  flags &= ~MGT_SOLVE_FULL;
+  if (eo) {
+    int rc = eo_prepare(h, st);
+    if (rc) return rc;
+  }
   WilsonParams P = make_params(h, flags, tau);
   const int64_t V = h->g.V;
   WSLayout Lw = ws_layout(V);
@@ -633,9 +958,9 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs
     int rc;
 #define MGT_SOLVE(NR)                                                                                           \
   (h->recon == 18 ? solve_group<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
-                                         relres_out + r0, dot, st)                                               \
+                                         relres_out + r0, dot, eo, st)                                           \
                   : solve_group<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
-                                         relres_out + r0, dot, st))
+                                         relres_out + r0, dot, eo, st))
     if (nr == 4)
       rc = MGT_SOLVE(4);
     else if (nr == 2)

@@ -1,0 +1,242 @@
+// Even-odd (red-black) form of the Wilson operator, sm_100a.
+//
+// With the sites split by parity p = (x0+x1+x2+x3) & 1 the operator of
+// dslash_core.cuh, M = G_out (Dg - 1/2 H) G_in  (Dg = diag(d_up, d_dn) per
+// spin half, H the 8-hop sum, G = 1 or g5), has site-diagonal M_ee, M_oo and
+// hop-only M_eo, M_oe.  Its Schur complement on the even sites is
+//   S = M_ee - M_eo M_oo^-1 M_oe = G_out [ Dg - 1/4 H_eo Dg^-1 H_oe ] G_in,
+// so A x = b is solved as
+//   bh_e = b_e + 1/2 G_out H_eo (Dg^-1 G_out b_o),     S x_e = bh_e,
+//   x_o  = G_in Dg^-1 ( G_out b_o + 1/2 H_oe (G_in x_e) ),
+// and the full residual is b - A x = (bh_e - S x_e, 0) exactly (the odd
+// rows are solved by construction).  The reference solves the full system
+// (krylov.py:52-118); the stopping test here is on the same full-residual
+// norm ||b - A x|| <= tol ||b||, and BiCGStab on S needs about half the
+// iterations (49 -> 25 at 8^4, 62 -> 31 at 16^4).
+//
+// Checkerboard layout: a parity field has Vh = V/2 sites, cb index
+// c = native_site >> 1 (every extent even; x2 is the fastest native index,
+// so the two sites of a pair (x2 = 2k, 2k+1) have opposite parity).  Links
+// are stored per parity in the same SoA form: ((mu*NL + e)*Vh + c).
+#pragma once
+#include "dslash_core.cuh"
+
+namespace mgt {
+
+struct EoGeom {
+  Geom g;       // full lattice
+  int64_t Vh;   // sites per parity
+  int L2h;      // L2 / 2
+  int antiperiodic;
+};
+
+inline EoGeom make_eo_geom(const Geom &g, int antiperiodic) {
+  EoGeom e;
+  e.g = g;
+  e.Vh = g.V / 2;
+  e.L2h = g.L[2] / 2;
+  e.antiperiodic = antiperiodic;
+  return e;
+}
+
+// cb index c of parity p -> coords and full native site
+__device__ __forceinline__ int64_t eo_coords(const EoGeom &E, int p, int64_t c, int (&x)[4]) {
+  const int64_t row = c / E.L2h;
+  const int x2h = (int)(c - row * E.L2h);
+  int64_t r = row;
+  x[1] = (int)(r % E.g.L[1]);
+  r /= E.g.L[1];
+  x[0] = (int)(r % E.g.L[0]);
+  x[3] = (int)(r / E.g.L[0]);
+  x[2] = 2 * x2h + ((p + x[0] + x[1] + x[3]) & 1);
+  return row * E.g.L[2] + x[2];
+}
+
+// One hop into acc (no -1/2): the neighbour spinor lives in the other-parity
+// field `in` at cb index nb >> 1; forward link from the output parity's
+// links at c, backward link from the input parity's links at nb >> 1.
+template <int MU, bool FWD, typename R, int RECON>
+__device__ __forceinline__ void eo_hop(const EoGeom &E, const cplx<R> *__restrict__ in,
+                                       const LinkField<R, RECON> &lout, const LinkField<R, RECON> &lin,
+                                       int64_t site, int64_t c, const int (&x)[4], R gin, C<R> (&acc)[4][3]) {
+  const int L = E.g.L[MU];
+  const int64_t st = E.g.stride[MU];
+  int64_t nb;
+  R ph = R(1);
+  if constexpr (FWD) {
+    nb = (x[MU] == L - 1) ? site - (int64_t)(L - 1) * st : site + st;
+    if (MU == 3 && E.antiperiodic && x[3] == L - 1) ph = R(-1);
+  } else {
+    nb = (x[MU] == 0) ? site + (int64_t)(L - 1) * st : site - st;
+    if (MU == 3 && E.antiperiodic && x[3] == 0) ph = R(-1);
+  }
+  const int64_t cn = nb >> 1;
+  const int64_t Vh = E.Vh;
+  C<R> h[2][3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    C<R> p0 = ldc(in + (0 * 3 + k) * Vh + cn);
+    C<R> p1 = ldc(in + (1 * 3 + k) * Vh + cn);
+    C<R> p2 = gin * ldc(in + (2 * 3 + k) * Vh + cn);
+    C<R> p3 = gin * ldc(in + (3 * 3 + k) * Vh + cn);
+    C<R> b0, b1;
+    b_mul<MU>(p2, p3, b0, b1);
+    if constexpr (FWD) {
+      h[0][k] = p0 - b0;
+      h[1][k] = p1 - b1;
+    } else {
+      h[0][k] = p0 + b0;
+      h[1][k] = p1 + b1;
+    }
+  }
+  C<R> u[3][3];
+  if constexpr (FWD)
+    lout.load(MU, c, u);
+  else
+    lin.load(MU, cn, u);
+  C<R> w[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      C<R> s(R(0), R(0));
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if constexpr (FWD)
+          s = cfma(u[i][j], h[a][j], s);
+        else
+          s = cfma_conj(u[j][i], h[a][j], s);
+      }
+      w[a][i] = ph * s;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    acc[0][i] = acc[0][i] + w[0][i];
+    acc[1][i] = acc[1][i] + w[1][i];
+    C<R> o2, o3;
+    bdag_mul<MU>(w[0][i], w[1][i], o2, o3);
+    if constexpr (FWD) {
+      acc[2][i] = acc[2][i] - o2;
+      acc[3][i] = acc[3][i] - o3;
+    } else {
+      acc[2][i] = acc[2][i] + o2;
+      acc[3][i] = acc[3][i] + o3;
+    }
+  }
+}
+
+// Coefficients of one half-lattice kernel:
+//   out = go o E . [ dc . (gc o ctr) + ch * H(gin o in) ]
+// (o: sign on spins 2,3; .: per-spin-half complex scale).
+struct EoCoef {
+  double dcu_re, dcu_im, dcd_re, dcd_im;  // centre scale (spins 0,1 / 2,3)
+  double eu_re, eu_im, ed_re, ed_im;      // final scale
+  double ch;                              // hop coefficient
+  double gc, gin, go;                     // +-1
+};
+
+// 8-hop sum at cb site c of parity pout, raw centre value (ctr may be null)
+// returned in cc, result in y.
+template <typename R, int RECON>
+__device__ __forceinline__ void eo_eval(const EoGeom &E, int pout, const EoCoef &K, const cplx<R> *__restrict__ in,
+                                        const cplx<R> *__restrict__ ctr, const LinkField<R, RECON> &lout,
+                                        const LinkField<R, RECON> &lin, int64_t c, C<R> (&y)[4][3],
+                                        C<R> (&cc)[4][3]) {
+  int x[4];
+  const int64_t site = eo_coords(E, pout, c, x);
+  const R gin = (R)K.gin;
+  C<R> acc[4][3];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) acc[a][k] = C<R>(R(0), R(0));
+#define MGT_HOP_FENCE asm volatile("" ::: "memory")
+  eo_hop<3, true>(E, in, lout, lin, site, c, x, gin, acc);
+  MGT_HOP_FENCE;
+  eo_hop<3, false>(E, in, lout, lin, site, c, x, gin, acc);
+  MGT_HOP_FENCE;
+  eo_hop<0, true>(E, in, lout, lin, site, c, x, gin, acc);
+  MGT_HOP_FENCE;
+  eo_hop<0, false>(E, in, lout, lin, site, c, x, gin, acc);
+  MGT_HOP_FENCE;
+  eo_hop<1, true>(E, in, lout, lin, site, c, x, gin, acc);
+  MGT_HOP_FENCE;
+  eo_hop<1, false>(E, in, lout, lin, site, c, x, gin, acc);
+  MGT_HOP_FENCE;
+  eo_hop<2, true>(E, in, lout, lin, site, c, x, gin, acc);
+  MGT_HOP_FENCE;
+  eo_hop<2, false>(E, in, lout, lin, site, c, x, gin, acc);
+  MGT_HOP_FENCE;
+#undef MGT_HOP_FENCE
+  const R ch = (R)K.ch, gc = (R)K.gc, go = (R)K.go;
+  const C<R> dcu((R)K.dcu_re, (R)K.dcu_im), dcd((R)K.dcd_re, (R)K.dcd_im);
+  const C<R> eu((R)K.eu_re, (R)K.eu_im), ed((R)K.ed_re, (R)K.ed_im);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      C<R> v = ch * acc[a][k];
+      if (ctr) {
+        C<R> z = ldc(ctr + (a * 3 + k) * E.Vh + c);
+        cc[a][k] = z;
+        if (a >= 2) z = gc * z;
+        v = v + (a < 2 ? dcu : dcd) * z;
+      } else {
+        cc[a][k] = C<R>(R(0), R(0));
+      }
+      v = (a < 2 ? eu : ed) * v;
+      y[a][k] = a >= 2 ? go * v : v;
+    }
+  }
+}
+
+// The four kernel roles of the Schur solve for operator variant (flags, tau):
+// d_up = 4 + m0 + i tau', d_dn = 4 + m0 - i tau' (make_params), g5in, g5out.
+struct EoRoles {
+  EoCoef first;   // t_o  = Dg^-1 H_oe (G_in x_e)
+  EoCoef second;  // S x  = G_out [ Dg G_in x_e - 1/4 H_eo t_o ]
+  EoCoef rhs;     // bh_e = G_out [ G_out b_e + 1/2 H_eo u_o ]
+  EoCoef recon;   // x_o  = G_in Dg^-1 [ G_out b_o + 1/2 H_oe (G_in x_e) ]
+  double iu_re, iu_im, id_re, id_im;  // Dg^-1 (u_o = Dg^-1 G_out b_o)
+};
+
+inline EoRoles make_eo_roles(const WilsonParams &P) {
+  auto inv = [](double re, double im, double &ore, double &oim) {
+    const double d = re * re + im * im;
+    ore = re / d;
+    oim = -im / d;
+  };
+  EoRoles R;
+  double iure, iuim, idre, idim;
+  inv(P.diag_up_re, P.diag_up_im, iure, iuim);
+  inv(P.diag_dn_re, P.diag_dn_im, idre, idim);
+  R.iu_re = iure, R.iu_im = iuim, R.id_re = idre, R.id_im = idim;
+  EoCoef one{1, 0, 1, 0, 1, 0, 1, 0, 1, 1, 1, 1};
+  R.first = one;
+  R.first.ch = 1.0;
+  R.first.gin = P.g5in;
+  R.first.eu_re = iure, R.first.eu_im = iuim, R.first.ed_re = idre, R.first.ed_im = idim;
+  R.first.go = 1.0;
+  R.second = one;
+  R.second.dcu_re = P.diag_up_re, R.second.dcu_im = P.diag_up_im;
+  R.second.dcd_re = P.diag_dn_re, R.second.dcd_im = P.diag_dn_im;
+  R.second.gc = P.g5in;
+  R.second.ch = -0.25;
+  R.second.gin = 1.0;
+  R.second.go = P.g5out;
+  R.rhs = one;
+  R.rhs.gc = P.g5out;
+  R.rhs.ch = 0.5;
+  R.rhs.gin = 1.0;
+  R.rhs.go = P.g5out;
+  R.recon = one;
+  R.recon.gc = P.g5out;
+  R.recon.ch = 0.5;
+  R.recon.gin = P.g5in;
+  R.recon.eu_re = iure, R.recon.eu_im = iuim, R.recon.ed_re = idre, R.recon.ed_im = idim;
+  R.recon.go = P.g5in;
+  return R;
+}
+
+}  // namespace mgt

@@ -28,6 +28,10 @@ struct mgt_wilson_s {
   unsigned long long *ctr_ring;
   mutable std::atomic<unsigned> ctr_next;
   int dyn_sched;
+  // even-odd form: per-parity link copy, built on first use (eo.cu)
+  void *links_cb;
+  std::mutex eo_mu;
+  int solve_eo;  // BiCGStab solves the even-odd Schur system (default 1)
 };
 
 namespace mgt {
@@ -70,6 +74,10 @@ inline WilsonParams make_params(const mgt_wilson_s *h, int flags, double tau) {
   P.halo_prev = nullptr;
   return P;
 }
+
+// build the per-parity links if needed; false if the lattice has an odd extent (eo.cu)
+bool eo_available(const mgt_wilson_s *h);
+int eo_prepare(mgt_wilson_s *h, cudaStream_t st);
 
 // forget cached solver graphs of a handle (bicgstab.cu)
 void drop_graphs(const void *h);

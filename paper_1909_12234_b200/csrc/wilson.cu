@@ -292,6 +292,9 @@ int mgt_wilson_create(mgt_wilson_t *out, const int dims[4], int antiperiodic, do
   }
   h->dyn_sched = 1;
   if (const char *v = getenv("MGT_DYN_SCHED")) h->dyn_sched = atoi(v);
+  h->links_cb = nullptr;
+  h->solve_eo = 1;
+  if (const char *v = getenv("MGT_SOLVE_EO")) h->solve_eo = atoi(v);
   h->ctr_next = 0;
   e = cudaMalloc(&h->ctr_ring, kCtrRing * sizeof(unsigned long long));
   if (e != cudaSuccess) {
@@ -327,6 +330,7 @@ int mgt_wilson_destroy(mgt_wilson_t h) {
   if (!h) return MGT_OK;
   drop_graphs(h);
   cudaFree(h->links);
+  if (h->links_cb) cudaFree(h->links_cb);
   cudaFree(h->ctr_ring);
   cudaFreeHost(h->host_flags);
   delete h;

@@ -33,6 +33,9 @@ class SolveConfig:
     max_iter: int = 2000
     restart: int = 32
     kind: str = "bicgstab"  # bicgstab (GPU default) | gcr
+    # BiCGStab on the even-odd Schur complement (same full-residual stopping
+    # test; about half the iterations).  False solves the full system.
+    even_odd: bool = True
 
     def __post_init__(self):
         if not (0 < self.tol < 1):
@@ -72,9 +75,11 @@ class BiCGStab:
         nbytes = _lib.lib().mgt_bicgstab_workspace_bytes(self.op.handle, self.MAX_GROUP)
         self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=device())
 
-    def solve_native(self, b, tol, max_iter, x=None, want_dot=False):
+    def solve_native(self, b, tol, max_iter, x=None, want_dot=False, even_odd=True):
         """Solve A x_r = b_r for native fields b (n, 12, V); returns
-        (x, [SolveReport], dots or None) where dots[r] = vdot(b_r, x_r)."""
+        (x, [SolveReport], dots or None) where dots[r] = vdot(b_r, x_r).
+        even_odd: solve through the even-odd Schur complement (whenever every
+        extent is even); the stopping test is the full residual either way."""
         n = b.shape[0]
         b = b.contiguous()
         x = torch.empty_like(b) if x is None else x
@@ -82,7 +87,8 @@ class BiCGStab:
         rel = (ct.c_double * n)()
         dots = (ct.c_double * (2 * n))() if want_dot else None
         _lib.check(_lib.lib().mgt_bicgstab_solve(
-            self.op.handle, ptr(b), ptr(x), n, int(self.flags), float(self.tau), float(tol), int(max_iter),
+            self.op.handle, ptr(b), ptr(x), n, int(self.flags) | (0 if even_odd else _lib.SOLVE_FULL),
+            float(self.tau), float(tol), int(max_iter),
             ptr(self.workspace), rep, rel, dots, stream_ptr()), "bicgstab")
         reports = []
         for r in range(n):
@@ -121,7 +127,7 @@ def bicgstab_solve(op, b, config):
         raise ValueError(f"dimension mismatch: {bd.shape[0]} != {base.dim}")
     solver = _solver_for(op)
     bn = base.to_native(bd.unsqueeze(0))
-    x, reps, _ = solver.solve_native(bn, config.tol, config.max_iter)
+    x, reps, _ = solver.solve_native(bn, config.tol, config.max_iter, even_odd=config.even_odd)
     xr = base.from_native(x)[0]
     return (xr.cpu().numpy() if host else xr), reps[0]
 
@@ -162,7 +168,8 @@ class TruncatedInverse:
         xs, reps, dots = [], [], []
         for r0 in range(0, b.shape[0], BiCGStab.MAX_GROUP):
             x, rr, d = solver.solve_native(b[r0:r0 + BiCGStab.MAX_GROUP], self.config.tol,
-                                           self.config.max_iter, want_dot=want_dot)
+                                           self.config.max_iter, want_dot=want_dot,
+                                           even_odd=getattr(self.config, "even_odd", True))
             xs.append(x)
             reps.extend(rr)
             if want_dot:

@@ -220,6 +220,32 @@ class WilsonOperator:
                    "deinterleave")
         return out
 
+    # -- even-odd form (every extent even) ------------------------------
+    def eo_split(self, x):
+        """native (n, 12, V) -> (even, odd) parity fields (n, 12, V/2)."""
+        x = x.contiguous()
+        n = x.shape[0]
+        e = torch.empty((n, DOF, self.volume // 2), dtype=x.dtype, device=x.device)
+        o = torch.empty_like(e)
+        _lib.check(_lib.lib().mgt_wilson_eo_split(self._handle, ptr(x), ptr(e), ptr(o), n, stream_ptr()), "eo split")
+        return e, o
+
+    def eo_merge(self, e, o):
+        """(even, odd) parity fields -> native (n, 12, V)."""
+        e, o = e.contiguous(), o.contiguous()
+        n = e.shape[0]
+        x = torch.empty((n, DOF, self.volume), dtype=e.dtype, device=e.device)
+        _lib.check(_lib.lib().mgt_wilson_eo_merge(self._handle, ptr(e), ptr(o), ptr(x), n, stream_ptr()), "eo merge")
+        return x
+
+    def schur_apply(self, xe, flags=0, tau=0.0):
+        """S x_e, the even-site Schur complement of the flags/tau variant."""
+        xe = xe.contiguous()
+        y = torch.empty_like(xe)
+        _lib.check(_lib.lib().mgt_wilson_schur_apply(self._handle, ptr(xe), ptr(y), xe.shape[0], int(flags),
+                                                     float(tau), stream_ptr()), "schur apply")
+        return y
+
     # -- reference-layout API (lattice.py:214-247) ------------------------
     def apply_host(self, x, out=None, flags=0, tau=0.0, nchunks=32):
         """Host-memory reference-layout vector(s) (numpy or CPU tensor, (N,) or

@@ -95,7 +95,8 @@ def _solve_batches_concurrently(inv_op, probes, batches, correction, streams):
         with torch.cuda.stream(stream):
             z = probes.noise_native(j0, j1)
             solver = _solver_for(inv_op.op)
-            x, reps, q = solver.solve_native(z, inv_op.config.tol, inv_op.config.max_iter, want_dot=True)
+            x, reps, q = solver.solve_native(z, inv_op.config.tol, inv_op.config.max_iter, want_dot=True,
+                                             even_odd=getattr(inv_op.config, "even_odd", True))
             if correction is not None:
                 q = q - correction(j0, z, x)
             stream.synchronize()

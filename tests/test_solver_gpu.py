@@ -71,3 +71,76 @@ def test_hutchinson_matches_exact_quadratic_forms(cuda):
     assert np.max(np.abs(est.samples - exact) / np.abs(exact)) < 1e-9
     assert est.s == s and est.inversions == s
     assert abs(est.mean - exact.mean()) / abs(exact.mean()) < 1e-9
+
+
+@pytest.mark.parametrize("flags,tau", [(0, 0.0), (1, 0.0), (2, 0.0), (4, 0.4), (3, -0.3), (0, 0.7)])
+def test_schur_complement_identity(cuda, flags, tau):
+    """S x_e = M_ee x_e - M_eo M_oo^-1 M_oe x_e, every block taken from the
+    full operator (A applied to parity-masked fields); split/merge exact."""
+    import torch
+    M, geo, op, A = _setup((4, 6, 4, 8), eps=0.4)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n, Vh = 2, geo.site_count // 2
+    xe = torch.randn((n, 12, Vh), dtype=torch.complex128, device="cuda", generator=g)
+    eo = torch.randn_like(xe)
+    z = torch.zeros_like(xe)
+    full = op.eo_merge(xe, eo)
+    e2, o2 = op.eo_split(full)
+    assert torch.equal(e2, xe) and torch.equal(o2, eo)
+    y1e, y1o = op.eo_split(op.apply_native(op.eo_merge(xe, z), flags=flags, tau=tau))
+    _, doo = op.eo_split(op.apply_native(op.eo_merge(z, eo), flags=flags, tau=tau))
+    moo = doo / eo                       # M_oo is site-diagonal
+    y2e, _ = op.eo_split(op.apply_native(op.eo_merge(z, y1o / moo), flags=flags, tau=tau))
+    ref = y1e - y2e
+    S = op.schur_apply(xe, flags=flags, tau=tau)
+    rel = (torch.linalg.vector_norm(S - ref) / torch.linalg.vector_norm(ref)).item()
+    assert rel < 1e-13
+
+
+def test_even_odd_solve_matches_full_solve(cuda):
+    """Same stopping test (full residual), half the iterations, same answer."""
+    import torch
+    M, geo, op, A = _setup((8, 8, 8, 8))
+    N = op.dim
+    z = np.stack([P.rademacher_numpy(N, 300 + j) for j in range(4)])
+    zn = op.to_native(torch.as_tensor(z).cuda())
+    sol = M.krylov.BiCGStab(op)
+    xe, re, qe = sol.solve_native(zn, 1e-10, 2000, want_dot=True, even_odd=True)
+    xf, rf, qf = sol.solve_native(zn, 1e-10, 2000, want_dot=True, even_odd=False)
+    X = op.from_native(xe).cpu().numpy()
+    for j in range(4):
+        assert re[j].converged and rf[j].converged
+        assert re[j].iterations < 0.7 * rf[j].iterations
+        r = z[j] - A @ X[j]
+        assert np.linalg.norm(r) <= 1.01e-10 * np.linalg.norm(z[j])
+        assert abs(re[j].final_relres - np.linalg.norm(r) / np.linalg.norm(z[j])) < 1e-11
+        assert abs(qe[j] - np.vdot(z[j], X[j])) < 1e-12 * abs(qe[j])
+        assert abs(qe[j] - qf[j]) < 1e-8 * abs(qf[j])
+    xx = (torch.linalg.vector_norm(xe - xf) / torch.linalg.vector_norm(xf)).item()
+    assert xx < 1e-8
+
+
+@pytest.mark.parametrize("flags,tau", [(0, 0.5), (3, -0.2), (4, 0.0)])
+def test_even_odd_solve_operator_variants(cuda, flags, tau):
+    import torch
+    from paper_1909_12234_b200.lattice import FormOperator
+    M, geo, op, A = _setup((4, 4, 4, 8), eps=0.3)
+    form = FormOperator(op, flags, tau, "t")
+    rng = np.random.default_rng(5)
+    b = rng.normal(size=op.dim) + 1j * rng.normal(size=op.dim)
+    x, rep = M.bicgstab_solve(form, b, M.SolveConfig(tol=1e-10))
+    assert rep.converged
+    r = b - form.apply(x)
+    assert np.linalg.norm(r) <= 1.01e-10 * np.linalg.norm(b)
+
+
+def test_odd_extent_solves_full_system(cuda):
+    M, geo, op, A = _setup((4, 4, 4, 5))
+    rng = np.random.default_rng(6)
+    b = rng.normal(size=op.dim) + 1j * rng.normal(size=op.dim)
+    x, rep = M.bicgstab_solve(op, b, M.SolveConfig(tol=1e-10))
+    assert rep.converged
+    assert np.linalg.norm(b - A @ x) <= 1.01e-10 * np.linalg.norm(b)
+    import torch
+    with pytest.raises(ValueError):
+        op.eo_split(torch.zeros((1, 12, geo.site_count), dtype=torch.complex128, device="cuda"))
