@@ -389,7 +389,7 @@ def probes_config1(M, rank, world, dims=(8, 8, 8, 8), s=32, tol=1e-8):
     its = inv.total_iterations / max(1, inv.n_solves)
     return {"config": "8x8x8x8 eps=0.2 m0=0.1 s=32 rademacher tol=1e-8 (BASELINE configs[0])",
             "value": s / el, "unit": "probes/s", "seconds": el, "mean_iterations": its,
-            "solver": "BiCGStab, 4 rhs per solve, 8 concurrent solves",
+            "solver": "BiCGStab on the even-odd Schur complement (stopping test on the full residual), 4 rhs per solve, 8 concurrent solves",
             "estimate_re": float(est.mean.real) if world == 1 else None}
 
 

@@ -129,7 +129,7 @@ def test_estimator_statistics_match_reference_formulas():
 
 def test_default_streams_rule():
     from paper_1909_12234_b200.trace import default_streams
-    assert default_streams(8 ** 4) == 7
-    assert default_streams(12 ** 4) == 2
-    assert default_streams(16 ** 4) == 1
+    assert default_streams(8 ** 4) == 8
+    assert default_streams(12 ** 4) == 8
+    assert default_streams(16 ** 4) == 4
     assert default_streams(32 ** 4) == 1

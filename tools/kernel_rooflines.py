@@ -115,16 +115,20 @@ def main():
         o2 = M.build_wilson(M.generate_gauge(g2, "su3", eps=0.2, seed=0), 0.1)
         z = M.build_probe_set(g2, 12, 4, dilution=False, kind="rademacher", seed=0).noise_native(0, 4)
         solver = K.BiCGStab(o2)
-        solver.solve_native(z, 1e-8, 2000)
-        torch.cuda.synchronize()
         import time
-        t0 = time.perf_counter()
-        _, reps, _ = solver.solve_native(z, 1e-8, 2000)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        its = sum(r.iterations for r in reps) / 4
-        emit("BiCGStab iteration (4 rhs, whole solve / iterations)", "x".join(map(str, dims)), el / its,
-             4608 * g2.site_count * 4)
+        # full system: 4608 B/site/rhs per iteration; even-odd Schur system:
+        # 2 x (first half 480 + second half 576) + 15 parity-field streams x 96
+        # = 3552 B per full site per rhs
+        for eo, model, name in [(False, 4608, "full"), (True, 3552, "even-odd Schur")]:
+            solver.solve_native(z, 1e-8, 2000, even_odd=eo)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, reps, _ = solver.solve_native(z, 1e-8, 2000, even_odd=eo)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            its = sum(r.iterations for r in reps) / 4
+            emit(f"BiCGStab iteration, {name} (4 rhs, whole solve / {its:g} iterations)", "x".join(map(str, dims)),
+                 el / its, model * g2.site_count * 4)
 
 
 if __name__ == "__main__":
