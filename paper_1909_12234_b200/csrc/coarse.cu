@@ -122,28 +122,72 @@ __global__ void scatter_column_kernel(int64_t nb, int nc, int col, const double2
   }
 }
 
-// y[b] = sum_dir C[b][dir] x[nbr(b, dir)] ; CTA per (b, rhs), thread per row
-__global__ void __launch_bounds__(128) coarse_apply_kernel(CoarseGeom cg, const double2 *__restrict__ Cm,
+// y[b] = sum_dir C[b][dir] x[nbr(b, dir)] for NR rhs at once; CTA per b.
+// Thread (row, group g) accumulates the dirs g, g+G, .. of its row for every
+// rhs, so each C entry is read once for all rhs (coalesced: a column of a
+// block is contiguous in rows); the neighbour vectors are staged in shared
+// memory and read as broadcasts.  The G group partials are summed in group
+// order (fixed, deterministic).
+template <int NR>
+__global__ void __launch_bounds__(256) coarse_apply_kernel(CoarseGeom cg, int G, const double2 *__restrict__ Cm,
                                                            const double2 *__restrict__ x, double2 *__restrict__ y) {
-  extern __shared__ double2 sx[];  // 9 * nc
-  const int64_t b = blockIdx.x;
-  const int rhs = blockIdx.y;
+  extern __shared__ double2 sm[];
   const int nc = cg.nc;
-  const double2 *xr = x + (int64_t)rhs * cg.nb * nc;
-  for (int i = threadIdx.x; i < 9 * nc; i += blockDim.x) {
-    const int dir = i / nc, col = i % nc;
-    sx[i] = xr[coarse_nbr(cg, b, dir) * nc + col];
+  double2 *sx = sm;                    // [9][nc][NR]
+  double2 *part = sm + 9 * nc * NR;    // [G][NR][nc]
+  const int64_t b = blockIdx.x;
+  for (int i = threadIdx.x; i < 9 * nc * NR; i += blockDim.x) {
+    const int r = i % NR, q = i / NR;
+    const int dir = q / nc, col = q % nc;
+    sx[i] = x[((int64_t)r * cg.nb + coarse_nbr(cg, b, dir)) * nc + col];
   }
   __syncthreads();
-  for (int row = threadIdx.x; row < nc; row += blockDim.x) {
-    C<double> acc(0.0, 0.0);
-    for (int dir = 0; dir < 9; ++dir) {
+  const int row = threadIdx.x % nc, grp = threadIdx.x / nc;
+  if (grp < G) {
+    C<double> acc[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[r] = C<double>(0.0, 0.0);
+    for (int dir = grp; dir < 9; dir += G) {
       const double2 *Cb = Cm + (b * 9 + dir) * (int64_t)nc * nc + row;
-      for (int col = 0; col < nc; ++col)
-        acc = cfma(ldc(Cb + (int64_t)col * nc), C<double>(sx[dir * nc + col].x, sx[dir * nc + col].y), acc);
+      const double2 *xs = sx + dir * nc * NR;
+#pragma unroll 4
+      for (int col = 0; col < nc; ++col) {
+        const C<double> cv = ldc(Cb + (int64_t)col * nc);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[r] = cfma(cv, C<double>(xs[col * NR + r].x, xs[col * NR + r].y), acc[r]);
+      }
     }
-    y[((int64_t)rhs * cg.nb + b) * nc + row] = make_double2(acc.re, acc.im);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) part[(grp * NR + r) * nc + row] = make_double2(acc[r].re, acc[r].im);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NR * nc; i += blockDim.x) {
+    const int r = i / nc, rw = i % nc;
+    C<double> t(0.0, 0.0);
+    for (int g = 0; g < G; ++g) {
+      const double2 v = part[(g * NR + r) * nc + rw];
+      t = t + C<double>(v.x, v.y);
+    }
+    y[((int64_t)r * cg.nb + b) * nc + rw] = make_double2(t.re, t.im);
+  }
+}
+
+template <int NR>
+static int launch_coarse_apply(const CoarseGeom &cg, const double2 *C, const double2 *x, double2 *y,
+                               cudaStream_t st) {
+  const int G = std::max(1, std::min(9, 256 / cg.nc));
+  const int block = ((G * cg.nc + 31) / 32) * 32;
+  const size_t smem = (size_t)(9 * cg.nc * NR + G * NR * cg.nc) * sizeof(double2);
+  if (smem > 48 * 1024) {
+    static size_t set = 0;
+    if (smem > set) {
+      MGT_CUDA(cudaFuncSetAttribute(coarse_apply_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      set = smem;
+    }
+  }
+  coarse_apply_kernel<NR><<<(unsigned)cg.nb, block, smem, st>>>(cg, G, C, x, y);
+  MGT_LAUNCH_CHECK("coarse_apply_kernel");
+  return MGT_OK;
 }
 
 static int make_cg(const int dims[4], const int block[4], int nv, CoarseGeom &cg) {
@@ -215,11 +259,20 @@ int mgt_coarse_apply(const int dims[4], const int block[4], int nv, const void *
   CoarseGeom cg;
   int rc = make_cg(dims, block, nv, cg);
   if (rc) return rc;
-  dim3 grid((unsigned)cg.nb, (unsigned)n_rhs);
-  const size_t smem = (size_t)9 * cg.nc * sizeof(double2);
-  coarse_apply_kernel<<<grid, 128, smem, as_stream(stream)>>>(cg, (const double2 *)C_dev, (const double2 *)xc_dev,
-                                                              (double2 *)yc_dev);
-  MGT_LAUNCH_CHECK("coarse_apply_kernel");
+  cudaStream_t st = as_stream(stream);
+  const double2 *Cp = (const double2 *)C_dev, *xp = (const double2 *)xc_dev;
+  double2 *yp = (double2 *)yc_dev;
+  const int64_t stride = cg.nb * cg.nc;
+  int r = 0;
+  while (r < n_rhs) {
+    const int left = n_rhs - r;
+    const int nr = left >= 4 ? 4 : (left >= 2 ? 2 : 1);
+    rc = nr == 4 ? launch_coarse_apply<4>(cg, Cp, xp + r * stride, yp + r * stride, st)
+                 : (nr == 2 ? launch_coarse_apply<2>(cg, Cp, xp + r * stride, yp + r * stride, st)
+                            : launch_coarse_apply<1>(cg, Cp, xp + r * stride, yp + r * stride, st));
+    if (rc) return rc;
+    r += nr;
+  }
   return MGT_OK;
 }
 

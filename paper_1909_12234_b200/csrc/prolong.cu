@@ -141,11 +141,12 @@ __global__ void __launch_bounds__(256) prolong_mgs_kernel(Agg a, double2 *__rest
 }
 
 // x (native fine) = P xc ; one CTA per (b, c, rhs)
-__global__ void __launch_bounds__(256) prolong_kernel(Agg a, const double2 *__restrict__ P,
+__global__ void __launch_bounds__(256) prolong_kernel(Agg a, int n_rhs, const double2 *__restrict__ P,
                                                      const double2 *__restrict__ xc, double2 *__restrict__ x) {
+  // rhs fastest in the grid: the CTAs that read one P block run together (L2 reuse)
   __shared__ double2 sx[64];
-  const int64_t grp = blockIdx.x;
-  const int rhs = blockIdx.y;
+  const int64_t grp = blockIdx.x / n_rhs;
+  const int rhs = (int)(blockIdx.x - grp * n_rhs);
   const int64_t b = grp >> 1;
   const int c = (int)(grp & 1);
   const int nc = 2 * a.nv;
@@ -163,50 +164,110 @@ __global__ void __launch_bounds__(256) prolong_kernel(Agg a, const double2 *__re
   }
 }
 
-// xc = P^H (g5? x) ; one CTA per (b, c, rhs); nv outputs per CTA reduced by
-// warp shuffles then across warps in fixed order.
-template <int NVMAX>
-__global__ void __launch_bounds__(256) restrict_kernel(Agg a, const double2 *__restrict__ P,
-                                                      const double2 *__restrict__ x, double2 *__restrict__ xc,
-                                                      int gamma5_in) {
-  __shared__ double2 part[8][64];
+// xc = P^H (g5? x) for NR rhs at once; one CTA per (b, c).  The CTA stages
+// the x block of its aggregate/chirality (all NR rhs, tiles of JT entries)
+// in shared memory; warp w owns columns k = w, w+8, .., so every P entry is
+// read from HBM once for all rhs and every staged x entry feeds CPW columns.
+// Fixed reduction order: per-lane partial sums, then a shuffle-xor tree.
+constexpr int kRestrictJT = 1024;
+
+template <int CPW, int NR>
+__global__ void __launch_bounds__(256) restrict_mrhs_kernel(Agg a, const double2 *__restrict__ P,
+                                                           const double2 *__restrict__ x,
+                                                           double2 *__restrict__ xc, int gamma5_in) {
+  extern __shared__ double2 sx[];  // [NR][kRestrictJT]
   const int64_t grp = blockIdx.x;
-  const int rhs = blockIdx.y;
   const int64_t b = grp >> 1;
   const int c = (int)(grp & 1);
   const int nc = 2 * a.nv;
-  const double2 *xr = x + (int64_t)rhs * 12 * a.g.V;
-  const double2 *G = P + grp * a.nv * (int64_t)a.bs;
   const double sign = (gamma5_in && c == 1) ? -1.0 : 1.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  C<double> acc[NVMAX];
+  const double2 *G = P + grp * a.nv * (int64_t)a.bs;
+  C<double> acc[CPW][NR];
 #pragma unroll
-  for (int k = 0; k < NVMAX; ++k) acc[k] = C<double>(0.0, 0.0);
-  for (int j = threadIdx.x; j < a.bs; j += blockDim.x) {
-    const int q = j / a.S, s = j % a.S;
-    const int comp = (2 * c + q / 3) * 3 + q % 3;
-    C<double> xv = sign * ldc(xr + (int64_t)comp * a.g.V + agg_site(a, b, s));
+  for (int i = 0; i < CPW; ++i)
 #pragma unroll
-    for (int k = 0; k < NVMAX; ++k)
-      if (k < a.nv) acc[k] = cfma_conj(ldc(G + (int64_t)k * a.bs + j), xv, acc[k]);
-  }
-#pragma unroll
-  for (int k = 0; k < NVMAX; ++k) {
-    if (k >= a.nv) break;
-    C<double> v = acc[k];
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      v.re += __shfl_xor_sync(0xffffffffu, v.re, off);
-      v.im += __shfl_xor_sync(0xffffffffu, v.im, off);
+    for (int r = 0; r < NR; ++r) acc[i][r] = C<double>(0.0, 0.0);
+  for (int j0 = 0; j0 < a.bs; j0 += kRestrictJT) {
+    const int jn = min(kRestrictJT, a.bs - j0);
+    __syncthreads();
+#pragma unroll 4
+    for (int t = threadIdx.x; t < jn * NR; t += blockDim.x) {
+      const int r = t / jn, jj = t - r * jn, j = j0 + jj;
+      const int q = j / a.S, s = j % a.S;
+      const int comp = (2 * c + q / 3) * 3 + q % 3;
+      const double2 v = x[((int64_t)r * 12 + comp) * a.g.V + agg_site(a, b, s)];
+      sx[r * kRestrictJT + jj] = make_double2(sign * v.x, sign * v.y);
     }
-    if (lane == 0) part[warp][k] = make_double2(v.re, v.im);
+    __syncthreads();
+#pragma unroll 4
+    for (int jj = lane; jj < jn; jj += 32) {
+      C<double> xv[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) xv[r] = C<double>(sx[r * kRestrictJT + jj].x, sx[r * kRestrictJT + jj].y);
+#pragma unroll
+      for (int i = 0; i < CPW; ++i) {
+        const int k = warp + 8 * i;
+        if (k < a.nv) {
+          const C<double> pk = ldc(G + (int64_t)k * a.bs + j0 + jj);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) acc[i][r] = cfma_conj(pk, xv[r], acc[i][r]);
+        }
+      }
+    }
   }
-  __syncthreads();
-  if (threadIdx.x < a.nv) {
-    C<double> t(0.0, 0.0);
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = t + C<double>(part[w][threadIdx.x].x, part[w][threadIdx.x].y);
-    xc[(int64_t)rhs * a.nb * nc + b * nc + c * a.nv + threadIdx.x] = make_double2(t.re, t.im);
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    const int k = warp + 8 * i;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      C<double> v = acc[i][r];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        v.re += __shfl_xor_sync(0xffffffffu, v.re, off);
+        v.im += __shfl_xor_sync(0xffffffffu, v.im, off);
+      }
+      if (lane == 0 && k < a.nv) xc[(int64_t)r * a.nb * nc + b * nc + c * a.nv + k] = make_double2(v.re, v.im);
+    }
   }
+}
+
+template <int CPW, int NR>
+static int launch_restrict_mrhs(const Agg &a, const double2 *P, const double2 *x, double2 *xc, int g5,
+                                cudaStream_t st) {
+  const size_t smem = (size_t)NR * kRestrictJT * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    MGT_CUDA(cudaFuncSetAttribute(restrict_mrhs_kernel<CPW, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = true;
+  }
+  restrict_mrhs_kernel<CPW, NR><<<(unsigned)(a.nb * 2), 256, smem, st>>>(a, P, x, xc, g5);
+  MGT_LAUNCH_CHECK("restrict_mrhs_kernel");
+  return MGT_OK;
+}
+
+template <int CPW>
+static int restrict_groups(const Agg &a, const double2 *P, const double2 *x, double2 *xc, int n_rhs, int g5,
+                           cudaStream_t st) {
+  const int64_t fstride = (int64_t)12 * a.g.V, cstride = a.nb * 2 * a.nv;
+  int r = 0;
+  while (r < n_rhs) {
+    const int left = n_rhs - r;
+    int rc;
+    if (left >= 4) {
+      rc = launch_restrict_mrhs<CPW, 4>(a, P, x + r * fstride, xc + r * cstride, g5, st);
+      r += 4;
+    } else if (left >= 2) {
+      rc = launch_restrict_mrhs<CPW, 2>(a, P, x + r * fstride, xc + r * cstride, g5, st);
+      r += 2;
+    } else {
+      rc = launch_restrict_mrhs<CPW, 1>(a, P, x + r * fstride, xc + r * cstride, g5, st);
+      r += 1;
+    }
+    if (rc) return rc;
+  }
+  return MGT_OK;
 }
 
 // coarse vectors: reference order (b_ref lexicographic, last coarse dim
@@ -271,9 +332,8 @@ int mgt_prolong(const int dims[4], const int block[4], int nv, const void *P_dev
   Agg a;
   int rc = make_agg(dims, block, nv, a);
   if (rc) return rc;
-  dim3 grid((unsigned)(a.nb * 2), (unsigned)n_rhs);
-  prolong_kernel<<<grid, 256, 0, as_stream(stream)>>>(a, (const double2 *)P_dev, (const double2 *)xc_dev,
-                                                       (double2 *)x_native_dev);
+  prolong_kernel<<<(unsigned)(a.nb * 2 * n_rhs), 256, 0, as_stream(stream)>>>(
+      a, n_rhs, (const double2 *)P_dev, (const double2 *)xc_dev, (double2 *)x_native_dev);
   MGT_LAUNCH_CHECK("prolong_kernel");
   return MGT_OK;
 }
@@ -285,20 +345,13 @@ int mgt_restrict(const int dims[4], const int block[4], int nv, const void *P_de
   Agg a;
   int rc = make_agg(dims, block, nv, a);
   if (rc) return rc;
-  dim3 grid((unsigned)(a.nb * 2), (unsigned)n_rhs);
   cudaStream_t st = as_stream(stream);
   const double2 *Pp = (const double2 *)P_dev, *xp = (const double2 *)x_native_dev;
   double2 *cp = (double2 *)xc_dev;
-  if (nv <= 8)
-    restrict_kernel<8><<<grid, 256, 0, st>>>(a, Pp, xp, cp, gamma5_in);
-  else if (nv <= 24)
-    restrict_kernel<24><<<grid, 256, 0, st>>>(a, Pp, xp, cp, gamma5_in);
-  else if (nv <= 32)
-    restrict_kernel<32><<<grid, 256, 0, st>>>(a, Pp, xp, cp, gamma5_in);
-  else
-    restrict_kernel<64><<<grid, 256, 0, st>>>(a, Pp, xp, cp, gamma5_in);
-  MGT_LAUNCH_CHECK("restrict_kernel");
-  return MGT_OK;
+  if (nv <= 8) return restrict_groups<1>(a, Pp, xp, cp, n_rhs, gamma5_in, st);
+  if (nv <= 24) return restrict_groups<3>(a, Pp, xp, cp, n_rhs, gamma5_in, st);
+  if (nv <= 32) return restrict_groups<4>(a, Pp, xp, cp, n_rhs, gamma5_in, st);
+  return restrict_groups<8>(a, Pp, xp, cp, n_rhs, gamma5_in, st);
 }
 
 int mgt_coarse_perm(const int dims[4], const int block[4], int nc, int n_rhs, const void *in_dev, void *out_dev,
