@@ -20,6 +20,8 @@ from .lattice import (
 from .gauge import GaugeField, gauge_from_array, generate_gauge
 from .krylov import SolveConfig, SolveReport, TruncatedInverse, bicgstab_solve, truncated_inverse
 from .probing import NoiseVector, ProbeGroup, ProbeSet, build_probe_set, make_noise
-from .trace import TraceEstimate, hutchinson, jackknife
+from .trace import TraceEstimate, hutchinson, jackknife, tsm_correction
+from .mgsolve import Hierarchy, MultigridSolver, build_hierarchy, dump_hierarchy, load_hierarchy
+from . import experiments
 
 __version__ = "0.1.0"

@@ -103,6 +103,67 @@ def build_hierarchy(op, blockings, null_counts, null_tol=1e-2, null_max_iter=200
     return Hierarchy([op, build_coarse_operator(op, P, level=1)], [P])
 
 
+def dump_hierarchy(hierarchy, outdir):
+    """Portable dump in the reference's format (multigrid.py:384-407):
+    hierarchy_manifest.csv (level, dims, block_dims, coarse_dim, fine_dof,
+    columns_file) and one columns CSV per level with rows (col, site, spin,
+    re, im) ordered by column then fine row, values with 17 significant
+    digits (exact round trip)."""
+    import csv
+    import os
+
+    from .multigrid import prolongator_entries
+    os.makedirs(outdir, exist_ok=True)
+    manifest = os.path.join(outdir, "hierarchy_manifest.csv")
+    with open(manifest, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["level", "dims", "block_dims", "coarse_dim", "fine_dof", "columns_file"])
+        for lvl, P in enumerate(hierarchy.prolongators):
+            fname = f"level{lvl}_columns.csv"
+            col, site, comp, val = prolongator_entries(P)
+            w.writerow([lvl, "x".join(map(str, P.geometry.dims)), "x".join(map(str, P.blocking.block_dims)),
+                        int(col.max()) + 1 if len(col) else 0, P.fine_dof, fname])
+            with open(os.path.join(outdir, fname), "w", newline="") as g:
+                cw = csv.writer(g)
+                cw.writerow(["col", "site", "spin", "re", "im"])
+                cw.writerows([int(c), int(si), int(sp), f"{v.real:.17g}", f"{v.imag:.17g}"]
+                             for c, si, sp, v in zip(col, site, comp, val))
+    return manifest
+
+
+def load_hierarchy(fine_op, outdir):
+    """Rebuild a hierarchy from a dump (multigrid.py:409-435): the
+    prolongator is placed back into the device block layout and the Galerkin
+    operator recomputed on the GPU."""
+    import csv
+    import os
+
+    from .multigrid import prolongator_from_entries
+    with open(os.path.join(outdir, "hierarchy_manifest.csv"), newline="") as f:
+        recs = list(csv.DictReader(f))
+    if len(recs) != 1:
+        raise NotImplementedError("the GPU prolongator kernels are two-level (fine dof 12)")
+    rec = recs[0]
+    block = tuple(int(v) for v in rec["block_dims"].split("x"))
+    dims = tuple(int(v) for v in rec["dims"].split("x"))
+    if dims != tuple(fine_op.geometry.dims):
+        raise ValueError(f"dump is for lattice {dims}, operator is {fine_op.geometry.dims}")
+    blocking = BlockingScheme(block)
+    nc = int(rec["coarse_dim"])
+    nv = nc // (2 * blocking.block_count(fine_op.geometry))
+    cols, sites, spins, vals = [], [], [], []
+    with open(os.path.join(outdir, rec["columns_file"]), newline="") as g:
+        for line in csv.DictReader(g):
+            cols.append(int(line["col"]))
+            sites.append(int(line["site"]))
+            spins.append(int(line["spin"]))
+            vals.append(complex(float(line["re"]), float(line["im"])))
+    P = prolongator_from_entries(fine_op.geometry, blocking, nv, np.array(cols), np.array(sites), np.array(spins),
+                                 np.array(vals, dtype=np.complex128), layout_op=fine_op,
+                                 fine_dof=int(rec["fine_dof"]))
+    return Hierarchy([fine_op, build_coarse_operator(fine_op, P, level=1)], [P])
+
+
 class MultigridSolver:
     """Two-grid cycles with a coarsest-level LU (dense C^-1 on the device) or
     an iterative coarse BiCGStab (multigrid.py:344-381)."""

@@ -159,6 +159,7 @@ class Prolongator:
         self.per_block_counts = keep.sum(axis=2)
         self.dropped = int(keep.size - keep.sum())
         self.coarse_gamma5 = np.tile(np.concatenate([np.ones(nv), -np.ones(nv)]), m)
+        self.keep = np.asarray(keep).reshape(-1).astype(np.int32)
 
     @property
     def uniform(self):
@@ -243,6 +244,97 @@ class Prolongator:
         nat = self.coarse_from_ref(eye.reshape(self.coarse_dim, self.n_blocks, self.nc))
         cols = self._layout.from_native(self.prolong_native(nat))
         return cols.T.cpu().numpy()
+
+
+def _block_maps(geo, blocking):
+    """(b_native -> b_ref, (b_native, s) -> reference fine site) for the
+    dense block layout of `Prolongator.P` (csrc/prolong.cu agg_site)."""
+    L = np.array(geo.dims)
+    B = np.array(blocking.block_dims)
+    Cd = L // B
+    m = int(np.prod(Cd))
+    S = int(np.prod(B))
+    bn = np.arange(m)
+    c2 = bn % Cd[2]
+    c1 = (bn // Cd[2]) % Cd[1]
+    c0 = (bn // (Cd[2] * Cd[1])) % Cd[0]
+    c3 = bn // (Cd[2] * Cd[1] * Cd[0])
+    b_ref = ((c0 * Cd[1] + c1) * Cd[2] + c2) * Cd[3] + c3
+    sl = np.arange(S)
+    l2 = sl % B[2]
+    l1 = (sl // B[2]) % B[1]
+    l0 = (sl // (B[2] * B[1])) % B[0]
+    l3 = sl // (B[2] * B[1] * B[0])
+    x0 = c0[:, None] * B[0] + l0[None, :]
+    x1 = c1[:, None] * B[1] + l1[None, :]
+    x2 = c2[:, None] * B[2] + l2[None, :]
+    x3 = c3[:, None] * B[3] + l3[None, :]
+    site_ref = ((x0 * L[1] + x1) * L[2] + x2) * L[3] + x3
+    return b_ref, site_ref
+
+
+def prolongator_entries(pro):
+    """Every stored entry of P in the reference's CSR terms: (col, fine row
+    site, fine component, value), ordered by column then row like the
+    reference's dump (multigrid.py:384-407).  Dropped columns are skipped and
+    the surviving ones renumbered in the reference's column order."""
+    geo, nv = pro.geometry, pro.nv
+    m = pro.n_blocks
+    S = int(np.prod(pro.blocking.block_dims))
+    Ph = pro.P.reshape(m, 2, nv, 6, S).cpu().numpy()
+    b_ref, site_ref = _block_maps(geo, pro.blocking)
+    keep = pro.keep.reshape(m, 2, nv).astype(bool)
+    order_b = np.argsort(b_ref)                      # native blocks in reference order
+    cols, sites, comps, vals = [], [], [], []
+    col = 0
+    q = np.arange(6)
+    for bn in order_b:
+        for c in range(2):
+            comp = (2 * c + q // 3) * 3 + q % 3      # (6,)
+            row = site_ref[bn][None, :] * pro.fine_dof + comp[:, None]   # (6, S)
+            ordr = np.argsort(row, axis=None)
+            for k in range(nv):
+                if not keep[bn, c, k]:
+                    continue
+                cols.append(np.full(6 * S, col))
+                sites.append((row.reshape(-1)[ordr]) // pro.fine_dof)
+                comps.append((row.reshape(-1)[ordr]) % pro.fine_dof)
+                vals.append(Ph[bn, c, k].reshape(-1)[ordr])
+                col += 1
+    return np.concatenate(cols), np.concatenate(sites), np.concatenate(comps), np.concatenate(vals)
+
+
+def prolongator_from_entries(geo, blocking, nv, col, site, comp, val, layout_op=None, fine_dof=12):
+    """Inverse of `prolongator_entries` for a uniform P (every block and
+    chirality keeps nv columns): the loader of multigrid.py:409-435."""
+    blocking.validate(geo)
+    m = blocking.block_count(geo)
+    S = int(np.prod(blocking.block_dims))
+    if int(np.max(col)) + 1 != 2 * nv * m:
+        raise BlockingError("prolongator dump is not uniform (dropped columns); cannot place it")
+    b_ref, site_ref = _block_maps(geo, blocking)
+    ref_to_native_b = np.empty(m, dtype=np.int64)
+    ref_to_native_b[b_ref] = np.arange(m)
+    # fine reference site -> (native block, local s)
+    where = np.empty((geo.site_count, 2), dtype=np.int64)
+    where[site_ref.reshape(-1), 0] = np.repeat(np.arange(m), S)
+    where[site_ref.reshape(-1), 1] = np.tile(np.arange(S), m)
+    br = col // (2 * nv)
+    c = (col % (2 * nv)) // nv
+    k = col % nv
+    bn = ref_to_native_b[br]
+    if np.any(where[site, 0] != bn):
+        raise BlockingError("prolongator dump: an entry lies outside its column's aggregate")
+    spin = comp // 3
+    if np.any(spin // 2 != c):
+        raise BlockingError("prolongator dump: an entry has the wrong chirality for its column")
+    q = (spin - 2 * c) * 3 + comp % 3
+    Ph = np.zeros((m, 2, nv, 6, S), dtype=np.complex128)
+    Ph[bn, c, k, q, where[site, 1]] = val
+    P = torch.as_tensor(Ph.reshape(-1)).to(device())
+    pro = Prolongator(P, geo, blocking, nv, fine_dof, np.ones(m * 2 * nv, dtype=np.int32))
+    pro._layout = layout_op if layout_op is not None else _LayoutOnly(geo)
+    return pro
 
 
 def build_prolongator(null_vectors, blocking, layout_op=None):

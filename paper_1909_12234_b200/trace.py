@@ -518,3 +518,30 @@ def hutchinson(inv_op, probes):
     _warn_flagged(flagged)
     inversions = inv_op.n_solves - before if before is not None else probes.slot_count
     return finish(0.0, samples, inversions, flagged)
+
+
+def tsm_correction(op, xi_low, xi_high, s_corr, seed, kind="z4", solver=None, max_iter=5000):
+    """Truncated-solver bias correction (trace.py:388-407): the mean over
+    s_corr noise vectors (seeds seed .. seed+s_corr-1) of
+    z^H (A^-1_{xi_high} z - A^-1_{xi_low} z).  Both solves run on the GPU in
+    batches with the quadratic forms fused into the solver; the solver is
+    deterministic, so xi_high == xi_low returns exactly 0."""
+    if xi_high > xi_low:
+        raise ValueError("expected xi_high <= xi_low (xi_high is the tighter tolerance)")
+    from .krylov import SolveConfig
+    from .probing import build_probe_set
+    if solver is not None:
+        raise NotImplementedError("tsm_correction runs the GPU BiCGStab; custom solver plugins are not supported")
+    inv_hi = TruncatedInverse(op, SolveConfig(tol=xi_high, max_iter=max_iter))
+    inv_lo = TruncatedInverse(op, SolveConfig(tol=xi_low, max_iter=max_iter))
+    probes = build_probe_set(op.geometry, 12, s_corr, hp_count=1, dilution=False, kind=kind, seed=seed)
+    qs = []
+    for j0 in range(0, s_corr, 4):
+        j1 = min(s_corr, j0 + 4)
+        z = probes.noise_native(j0, j1)
+        _, _, q_hi = inv_hi.solve_native(z, want_dot=True)
+        _, _, q_lo = inv_lo.solve_native(z, want_dot=True)
+        qs.append(np.asarray(q_hi) - np.asarray(q_lo))
+    samples = np.concatenate(qs) if qs else np.zeros(0, dtype=np.complex128)
+    return finish(0.0, samples, inv_hi.n_solves + inv_lo.n_solves).mean
+

@@ -214,3 +214,70 @@ def test_config3_shape_against_oracle(cuda):
     C = MG.build_coarse_operator(op, pro)
     Co = OMG.coarse_operator(A, Po, g5c).toarray()
     assert np.abs(C.dense() - Co).max() < 1e-11 * np.abs(Co).max()
+
+
+GOLD_IO = os.path.join(os.path.dirname(__file__), "golden", "golden_io.npz")
+
+
+def test_hierarchy_load_dump_reference_format(gold, setup, tmp_path):
+    """load_hierarchy reads the REFERENCE's dump of the golden hierarchy
+    (multigrid.py:409-435): P exactly, C recomputed on the GPU; dumping the
+    loaded hierarchy reproduces the reference's files byte for byte."""
+    M, MG, geo, op, A, Pg = setup
+    g = np.load(GOLD_IO)
+    src = tmp_path / "ref"
+    src.mkdir()
+    (src / "hierarchy_manifest.csv").write_bytes(g["hier_manifest"].tobytes())
+    (src / "level0_columns.csv").write_bytes(g["hier_columns"].tobytes())
+    hier = M.load_hierarchy(op, str(src))
+    P = hier.prolongators[0]
+    assert np.array_equal(P.dense(), Pg.toarray())
+    C = hier.operators[1].dense()
+    assert np.abs(C - gold["C_dense"]).max() <= 1e-12 * np.abs(gold["C_dense"]).max()
+    out = tmp_path / "ours"
+    M.dump_hierarchy(hier, str(out))
+    assert (out / "hierarchy_manifest.csv").read_bytes() == g["hier_manifest"].tobytes()
+    assert (out / "level0_columns.csv").read_bytes() == g["hier_columns"].tobytes()
+
+
+def test_hierarchy_dump_of_gpu_prolongator(gold, setup, tmp_path):
+    """A GPU-built P dumps with the reference's (col, site, spin) sequence
+    and values within the P tolerance; the dump loads back exactly."""
+    import csv
+    M, MG, geo, op, A, Pg = setup
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    hier = M.Hierarchy([op, MG.build_coarse_operator(op, pro)], [pro])
+    M.dump_hierarchy(hier, str(tmp_path))
+    with open(tmp_path / "level0_columns.csv", newline="") as f:
+        ours = list(csv.reader(f))
+    ref = list(csv.reader(np.load(GOLD_IO)["hier_columns"].tobytes().decode().splitlines()))
+    assert ours[0] == ref[0] and len(ours) == len(ref)
+    assert [r[:3] for r in ours] == [r[:3] for r in ref]
+    a = np.array([[float(r[3]), float(r[4])] for r in ours[1:]])
+    b = np.array([[float(r[3]), float(r[4])] for r in ref[1:]])
+    assert np.abs(a - b).max() < 1e-12
+    back = M.load_hierarchy(op, str(tmp_path))
+    assert np.array_equal(back.prolongators[0].dense(), pro.dense())
+
+
+def test_tsm_correction(gold, setup):
+    """trace.py:388-407: exactly 0 for equal tolerances (deterministic
+    solver); otherwise the mean of z^H (A^-1_hi z - A^-1_lo z), small
+    against the trace and equal to an independent evaluation."""
+    M, MG, geo, op, A, Pg = setup
+    assert M.tsm_correction(op, 1e-6, 1e-6, 5, seed=3) == 0.0
+    with pytest.raises(ValueError):
+        M.tsm_correction(op, 1e-8, 1e-6, 2, seed=3)
+    c = M.tsm_correction(op, 1e-3, 1e-10, 6, seed=3, kind="rademacher")
+    ps = M.build_probe_set(geo, 12, 6, hp_count=1, dilution=False, kind="rademacher", seed=3)
+    acc = []
+    for j0, j1 in ((0, 4), (4, 6)):
+        z = ps.noise_native(j0, j1)
+        _, _, qh = M.TruncatedInverse(op, M.SolveConfig(tol=1e-10)).solve_native(z, want_dot=True)
+        _, _, ql = M.TruncatedInverse(op, M.SolveConfig(tol=1e-3)).solve_native(z, want_dot=True)
+        acc.extend(qh - ql)
+    assert c == np.mean(np.array(acc))
+    z0 = P.rademacher_numpy(op.dim, 3)
+    xe = np.vdot(z0, np.linalg.solve(A.toarray(), z0))
+    assert 0 < abs(c) < 1e-2 * abs(xe)
