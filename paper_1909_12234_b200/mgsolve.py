@@ -92,15 +92,25 @@ class Hierarchy:
 
 
 def build_hierarchy(op, blockings, null_counts, null_tol=1e-2, null_max_iter=200, seed=0):
-    """Two-level hierarchy by null-vector setup (multigrid.py:328-341)."""
+    """2- or 3-level hierarchy by recursive null-vector setup
+    (multigrid.py:328-341; level l uses seed + 7 l).  Level 0 -> 1 runs on
+    the fine kernels; level 1 -> 2 on the coarse-level pieces (mglevel.py)."""
+    from .multigrid import BlockingError
     if len(blockings) != len(null_counts):
-        from .multigrid import BlockingError
         raise BlockingError("need one null-vector count per blocking level")
-    if len(blockings) != 1:
-        raise NotImplementedError("the GPU prolongator kernels are two-level (fine dof 12)")
+    if len(blockings) not in (1, 2):
+        raise NotImplementedError("hierarchies of 2 or 3 levels are supported")
     nv = generate_null_vectors(op, null_counts[0], tol=null_tol, max_iter=null_max_iter, seed=seed)
     P = build_prolongator(nv, BlockingScheme(tuple(blockings[0])), layout_op=op)
-    return Hierarchy([op, build_coarse_operator(op, P, level=1)], [P])
+    ops, prols = [op, build_coarse_operator(op, P, level=1)], [P]
+    if len(blockings) == 2:
+        from .mglevel import build_level_coarse_operator, build_level_prolongator, generate_null_vectors_coarse
+        nv1 = generate_null_vectors_coarse(ops[1], null_counts[1], tol=null_tol, max_iter=null_max_iter,
+                                           seed=seed + 7)
+        P1 = build_level_prolongator(nv1, BlockingScheme(tuple(blockings[1])))
+        ops.append(build_level_coarse_operator(ops[1], P1, level=2))
+        prols.append(P1)
+    return Hierarchy(ops, prols)
 
 
 def dump_hierarchy(hierarchy, outdir):
@@ -120,7 +130,7 @@ def dump_hierarchy(hierarchy, outdir):
         w.writerow(["level", "dims", "block_dims", "coarse_dim", "fine_dof", "columns_file"])
         for lvl, P in enumerate(hierarchy.prolongators):
             fname = f"level{lvl}_columns.csv"
-            col, site, comp, val = prolongator_entries(P)
+            col, site, comp, val = prolongator_entries(P) if lvl == 0 else _level_entries(P)
             w.writerow([lvl, "x".join(map(str, P.geometry.dims)), "x".join(map(str, P.blocking.block_dims)),
                         int(col.max()) + 1 if len(col) else 0, P.fine_dof, fname])
             with open(os.path.join(outdir, fname), "w", newline="") as g:
@@ -141,8 +151,8 @@ def load_hierarchy(fine_op, outdir):
     from .multigrid import prolongator_from_entries
     with open(os.path.join(outdir, "hierarchy_manifest.csv"), newline="") as f:
         recs = list(csv.DictReader(f))
-    if len(recs) != 1:
-        raise NotImplementedError("the GPU prolongator kernels are two-level (fine dof 12)")
+    if len(recs) not in (1, 2):
+        raise NotImplementedError("hierarchies of 2 or 3 levels are supported")
     rec = recs[0]
     block = tuple(int(v) for v in rec["block_dims"].split("x"))
     dims = tuple(int(v) for v in rec["dims"].split("x"))
@@ -161,25 +171,100 @@ def load_hierarchy(fine_op, outdir):
     P = prolongator_from_entries(fine_op.geometry, blocking, nv, np.array(cols), np.array(sites), np.array(spins),
                                  np.array(vals, dtype=np.complex128), layout_op=fine_op,
                                  fine_dof=int(rec["fine_dof"]))
-    return Hierarchy([fine_op, build_coarse_operator(fine_op, P, level=1)], [P])
+    ops, prols = [fine_op, build_coarse_operator(fine_op, P, level=1)], [P]
+    if len(recs) == 2:
+        from .mglevel import build_level_coarse_operator
+        rec = recs[1]
+        cols, sites, spins, vals = _read_columns(os.path.join(outdir, rec["columns_file"]))
+        P1 = _level_from_entries(ops[1], BlockingScheme(tuple(int(v) for v in rec["block_dims"].split("x"))),
+                                 int(rec["coarse_dim"]), int(rec["fine_dof"]), cols, sites, spins, vals)
+        ops.append(build_level_coarse_operator(ops[1], P1, level=2))
+        prols.append(P1)
+    return Hierarchy(ops, prols)
+
+
+def _read_columns(path):
+    import csv
+    cols, sites, spins, vals = [], [], [], []
+    with open(path, newline="") as g:
+        for line in csv.DictReader(g):
+            cols.append(int(line["col"]))
+            sites.append(int(line["site"]))
+            spins.append(int(line["spin"]))
+            vals.append(complex(float(line["re"]), float(line["im"])))
+    return np.array(cols), np.array(sites), np.array(spins), np.array(vals, dtype=np.complex128)
+
+
+def _level_entries(P):
+    """(col, site, spin, value) of a coarse-level prolongator, column then row order."""
+    m, nv, L = P.n_blocks, P.nv, P.G.shape[-1]
+    G = P.G.cpu().numpy()
+    idx = P.idx.cpu().numpy()
+    cols, rows, vals = [], [], []
+    for b in range(m):
+        for c in range(2):
+            order = np.argsort(idx[b, c])
+            for k in range(nv):
+                cols.append(np.full(L, (b * 2 + c) * nv + k))
+                rows.append(idx[b, c][order])
+                vals.append(G[b, c, k][order])
+    rows = np.concatenate(rows)
+    return np.concatenate(cols), rows // P.fine_dof, rows % P.fine_dof, np.concatenate(vals)
+
+
+def _level_from_entries(op, blocking, nc, dof, cols, sites, spins, vals):
+    from .mglevel import LevelProlongator
+    from ._device import device
+    m = blocking.block_count(op.geometry)
+    nv = nc // (2 * m)
+    L = len(cols) // nc
+    order = np.lexsort((sites * dof + spins, cols))
+    rows = (sites * dof + spins)[order].reshape(m, 2, nv, L)
+    if np.any(rows != rows[:, :, :1, :]):
+        raise ValueError("columns of one (block, chirality) group must share their support")
+    G = torch.as_tensor(vals[order].reshape(m, 2, nv, L)).to(device())
+    idx = torch.as_tensor(rows[:, :, 0, :]).to(device())
+    return LevelProlongator(G, idx, op.geometry, blocking, dof, nv, op.dim)
 
 
 class MultigridSolver:
-    """Two-grid cycles with a coarsest-level LU (dense C^-1 on the device) or
-    an iterative coarse BiCGStab (multigrid.py:344-381)."""
+    """Two-grid cycles recursing through an intermediate level for 3-level
+    hierarchies (multigrid.py:344-381).  Coarsest level: dense LU on the
+    device ("lu"), or iterative -- coarse BiCGStab for a level-1 coarsest
+    ("bicgstab"), GCR(32) for a level-2 coarsest ("gcr", as the reference)."""
 
     def __init__(self, hierarchy, smoother_iters=4, coarse_tol=1e-1, coarse_max_iter=200, coarsest="lu"):
+        from .mglevel import CoarseSmoother
         self.hierarchy = hierarchy
-        self.smoothers = [make_smoother(o, smoother_iters) for o in hierarchy.operators[:-1]]
+        ops = hierarchy.operators
+        self.smoothers = [make_smoother(ops[0], smoother_iters)] + [CoarseSmoother(o, smoother_iters)
+                                                                     for o in ops[1:-1]]
         self.coarse_tol = coarse_tol
         self.coarse_max_iter = coarse_max_iter
         self.coarsest = coarsest
-        coarse = hierarchy.operators[-1]
-        if coarsest == "lu":
-            self._cinv = coarse.dense_inverse_native()
-            self._coarse = lambda rc: (rc.reshape(rc.shape[0], -1) @ self._cinv.T).reshape(rc.shape)
+        coarse = ops[-1]
+        if hierarchy.levels == 2:
+            if coarsest == "lu":
+                self._cinv = coarse.dense_inverse_native()
+                self._coarse = lambda rc: (rc.reshape(rc.shape[0], -1) @ self._cinv.T).reshape(rc.shape)
+            else:
+                self._coarse = lambda rc: coarse_bicgstab(coarse, rc, self.coarse_tol, self.coarse_max_iter)[0]
         else:
-            self._coarse = lambda rc: coarse_bicgstab(coarse, rc, self.coarse_tol, self.coarse_max_iter)[0]
+            from .mglevel import gcr_torch, two_grid_solve_ref
+            if coarsest == "lu":
+                inner = coarse.solve
+            else:
+                inner = lambda rc: gcr_torch(coarse.apply, rc, self.coarse_tol, self.coarse_max_iter, 32)[0]  # noqa: E731
+            op1, P0, P1, sm1 = ops[1], hierarchy.prolongators[0], hierarchy.prolongators[1], self.smoothers[1]
+
+            def level1(rc):  # native coarse (n, nb, nc) -> reference order, recurse, back
+                ref = P0.coarse_to_ref(rc)
+                out = torch.empty_like(ref)
+                for j in range(ref.shape[0]):
+                    out[j] = two_grid_solve_ref(op1, P1, inner, sm1, ref[j].reshape(-1), self.coarse_tol,
+                                                max_cycles=self.coarse_max_iter)[0].reshape(ref[j].shape)
+                return P0.coarse_from_ref(out)
+            self._coarse = level1
 
     def solve_native(self, b, tol, max_cycles=100):
         h = self.hierarchy
