@@ -337,6 +337,20 @@ def prolongator_from_entries(geo, blocking, nv, col, site, comp, val, layout_op=
     return pro
 
 
+def subspace_angles(prolongator, vectors):
+    """sin of the principal angle between range(V) and each unit vector,
+    sqrt(max(0, 1 - ||V^H v||^2)) (multigrid.py:303-313); vectors:
+    reference-layout (n, N) or (N,), numpy or CUDA tensor."""
+    V = torch.as_tensor(np.atleast_2d(np.asarray(vectors, dtype=np.complex128))).to(device()) \
+        if not isinstance(vectors, torch.Tensor) else torch.atleast_2d(vectors)
+    if hasattr(prolongator, "restrict_native"):
+        c = prolongator.restrict_native(prolongator._layout.to_native(V.contiguous()))
+        c2 = torch.linalg.vector_norm(c.reshape(c.shape[0], -1), dim=1) ** 2
+    else:
+        c2 = torch.linalg.vector_norm(prolongator.restrict(V), dim=-1) ** 2
+    return np.sqrt(np.maximum(0.0, 1.0 - c2.cpu().numpy()))
+
+
 def build_prolongator(null_vectors, blocking, layout_op=None):
     """Reference build_prolongator (multigrid.py:163-225) on the GPU."""
     geo = null_vectors.geometry

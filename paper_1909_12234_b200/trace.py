@@ -545,3 +545,65 @@ def tsm_correction(op, xi_low, xi_high, s_corr, seed, kind="z4", solver=None, ma
     samples = np.concatenate(qs) if qs else np.zeros(0, dtype=np.complex128)
     return finish(0.0, samples, inv_hi.n_solves + inv_lo.n_solves).mean
 
+
+def orthogonal_rank_sweep(inv_op, U, lefts_inv, probes, rank_grid, op=None):
+    """Per-rank orthogonally deflated estimates from ONE set of undeflated
+    probe solves (experiments.py:205-243): U (k columns, ascending singular
+    value) and lefts_inv = A^-1_xi U as reference-layout (N, k) arrays or
+    native (k, 12, V) tensors.  Per slot the GPU solve returns q = z^H A^-1 z
+    (fused), and a = U^H z, ybar = lefts^H z come from the projection kernel;
+    rank r uses q - sum_{i<r} conj(ybar_i) a_i and t0 = sum_{i<r} u_i^H l_i.
+    Returns {rank: TraceEstimate}."""
+    import torch
+    from .linalg import vhx
+    base = op if op is not None else inv_op.op
+    rank_grid = sorted(set(int(r) for r in rank_grid))
+    k_max = max(rank_grid)
+
+    def native(M):
+        if isinstance(M, torch.Tensor) and M.dim() == 3:
+            return M
+        Mt = torch.as_tensor(np.ascontiguousarray(np.asarray(M).T)) if not isinstance(M, torch.Tensor) \
+            else M.transpose(0, 1).contiguous()
+        return base.to_native(Mt.to(torch.complex128).cuda())
+
+    U, L = native(U), native(lefts_inv)
+    if k_max > U.shape[0]:
+        raise ValueError("rank grid exceeds available vectors")
+    U, L = U[:k_max], L[:k_max]
+    t0_terms = torch.diagonal(vhx(U, L)).cpu().numpy() if k_max else np.zeros(0, dtype=np.complex128)
+    per_group = []
+    w = probes.weights()
+
+    def collect(z, n_groups):
+        _, _, q = inv_op.solve_native(z, want_dot=True)
+        a = vhx(U, z).cpu().numpy() if k_max else np.zeros((0, z.shape[0]), dtype=np.complex128)
+        yb = vhx(L, z).cpu().numpy() if k_max else np.zeros((0, z.shape[0]), dtype=np.complex128)
+        per = z.shape[0] // n_groups
+        for gidx in range(n_groups):
+            sl = slice(gidx * per, (gidx + 1) * per)
+            per_group.append((np.asarray(q)[sl], a[:, sl].T, yb[:, sl].T))
+
+    ns = probes.sample_count
+    if probes.slots_per_group == 1:
+        for j0 in range(0, ns, 4):
+            j1 = min(ns, j0 + 4)
+            collect(probes.noise_native(j0, j1), j1 - j0)
+    else:
+        for j in range(ns):
+            collect(probes.slots_native(j), 1)
+    out = {}
+    for r in rank_grid:
+        samples = np.empty(len(per_group), dtype=np.complex128)
+        for gi, (q, a, yb) in enumerate(per_group):
+            acc = 0.0 + 0.0j
+            for si in range(len(q)):
+                if r == 0:
+                    acc = acc + w[si] * q[si]
+                else:
+                    acc = acc + w[si] * (q[si] - np.sum(np.conj(yb[si, :r]) * a[si, :r]))
+            samples[gi] = acc
+        t0 = complex(np.sum(t0_terms[:r])) if r else 0.0 + 0.0j
+        out[r] = finish(t0, samples, probes.slot_count + r)
+    return out
+

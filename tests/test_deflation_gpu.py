@@ -76,3 +76,41 @@ def test_davidson_eigenpairs_match_reference(gold, setup):
     assert np.abs(G - np.eye(6)).max() < 1e-10
     trip = E.to_singular_triplets(res)
     assert np.all(np.diff(trip.sigmas) >= 0)
+
+
+GOLD_SWEEP = os.path.join(os.path.dirname(__file__), "golden", "golden_sweep.npz")
+
+
+def test_orthogonal_rank_sweep_matches_reference(cuda, gold, setup):
+    """experiments.py:205-243 (the reference's golden run, tol 1e-10 solves):
+    per-rank mean, t0, variance and inversion counts; rank r of the sweep
+    equals deflate_orthogonal with the first r vectors on the same probes."""
+    M, geo, op = setup
+    from paper_1909_12234_b200 import trace as TR
+    g = np.load(GOLD_SWEEP)
+    U = gold["eig_vectors"]
+    Un = op.to_native(torch.as_tensor(np.ascontiguousarray(U.T)).cuda())
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=1e-10))
+    lefts, _, _ = inv.solve_native(Un)
+    ps = M.build_probe_set(geo, 12, int(g["sweep_s"]), hp_count=1, dilution=False, kind="rademacher",
+                           seed=int(g["sweep_seed"]))
+    grid = [int(r) for r in g["sweep_grid"]]
+    res = TR.orthogonal_rank_sweep(M.TruncatedInverse(op, M.SolveConfig(tol=1e-10)), Un, lefts, ps, grid)
+    for i, r in enumerate(grid):
+        assert abs(res[r].mean - g["sweep_mean"][i]) < 1e-8 * abs(g["sweep_mean"][i])
+        assert abs(res[r].t0 - g["sweep_t0"][i]) < 1e-8 * max(abs(g["sweep_t0"][i]), 1.0)
+        assert abs(res[r].variance - g["sweep_var"][i]) < 1e-6 * g["sweep_var"][i]
+        assert res[r].inversions == int(g["sweep_inv"][i])
+    r = 3
+    est = TR.deflate_orthogonal(M.TruncatedInverse(op, M.SolveConfig(tol=1e-10)), Un[:r], ps)
+    assert abs(est.mean - res[r].mean) < 1e-9 * abs(est.mean)
+
+
+def test_subspace_angles_match_reference(cuda, gold, setup):
+    M, geo, op = setup
+    from paper_1909_12234_b200 import multigrid as MG
+    g = np.load(GOLD_SWEEP)
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    ang = MG.subspace_angles(pro, g["angles_vectors"])
+    assert np.abs(ang - g["angles"]).max() < 1e-7
