@@ -247,7 +247,7 @@ class WilsonOperator:
         return y
 
     # -- reference-layout API (lattice.py:214-247) ------------------------
-    def apply_host(self, x, out=None, flags=0, tau=0.0, nchunks=32):
+    def apply_host(self, x, out=None, flags=0, tau=0.0, nchunks=64):
         """Host-memory reference-layout vector(s) (numpy or CPU tensor, (N,) or
         (n, N) rows) -> host result through the pipelined C-ABI path
         `mgt_wilson_apply_host` (PCIe copies overlapped with the layout

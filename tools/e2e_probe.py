@@ -23,3 +23,28 @@ for nch in (1, 4, 8, 16, 24, 48):
 y2 = op.apply(np.asarray(xh.numpy()))
 assert np.array_equal(y2, ref.numpy())
 print("numpy path ok")
+
+# raw PCIe ceilings with the same pinned buffers
+dev = torch.empty(op.dim, dtype=torch.complex128, device="cuda")
+dev2 = torch.empty_like(dev)
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+nb = op.dim * 16
+for name, fn in [("H2D", lambda: dev.copy_(xh, non_blocking=True)),
+                 ("D2H", lambda: yh.copy_(dev2, non_blocking=True))]:
+    fn(); torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    el = (time.perf_counter() - t0) / 3
+    print(f"{name} alone: {el*1e3:7.2f} ms  {nb/el/1e9:6.1f} GB/s", flush=True)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(3):
+    with torch.cuda.stream(s1):
+        dev.copy_(xh, non_blocking=True)
+    with torch.cuda.stream(s2):
+        yh.copy_(dev2, non_blocking=True)
+torch.cuda.synchronize()
+el = (time.perf_counter() - t0) / 3
+print(f"H2D || D2H: {el*1e3:7.2f} ms  {2*nb/el/1e9:6.1f} GB/s total", flush=True)
