@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                 "-Xptxas", "-v", "--expt-relaxed-constexpr",
-                "-I" + os.path.join(ROOT, "include")]
+                "-I" + os.path.join(ROOT, "include")] + os.environ.get("MGT_NVCC_EXTRA", "").split()
 
 
 def _headers():
