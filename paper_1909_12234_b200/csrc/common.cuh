@@ -91,6 +91,15 @@ __device__ __forceinline__ C<float> ldc(const float2 *p) {
   float2 v = __ldg(p);
   return {v.x, v.y};
 }
+// L2-only (L1-bypassing) loads
+__device__ __forceinline__ C<double> ldc_cg(const double2 *p) {
+  double2 v = __ldcg(p);
+  return {v.x, v.y};
+}
+__device__ __forceinline__ C<float> ldc_cg(const float2 *p) {
+  float2 v = __ldcg(p);
+  return {v.x, v.y};
+}
 __device__ __forceinline__ void stc(double2 *p, C<double> v) { *p = make_double2(v.re, v.im); }
 __device__ __forceinline__ void stc(float2 *p, C<float> v) { *p = make_float2(v.re, v.im); }
 // streaming store (evict-first): output fields are not re-read by this kernel

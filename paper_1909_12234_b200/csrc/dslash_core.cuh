@@ -74,6 +74,11 @@ struct LinkField {
   }
 };
 
+// neighbour-spinor load of the hops (experiment hook: ldc_cg bypasses L1)
+#ifndef MGT_SPINOR_LD
+#define MGT_SPINOR_LD ldc
+#endif
+
 // Accumulate one hop into acc[spin][colour] (without the -1/2).
 // SS: site stride of the spinor field (1: native SoA; NR: rhs-interleaved
 // ((comp*V + site)*NR + rhs), `in` pre-offset by rhs).
@@ -98,10 +103,10 @@ __device__ __forceinline__ void wilson_hop(const Geom &g, const cplx<R> *__restr
   C<R> h[2][3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    C<R> p0 = ldc(in + ((0 * 3 + c) * V + nb) * SS);
-    C<R> p1 = ldc(in + ((1 * 3 + c) * V + nb) * SS);
-    C<R> p2 = g5in * ldc(in + ((2 * 3 + c) * V + nb) * SS);
-    C<R> p3 = g5in * ldc(in + ((3 * 3 + c) * V + nb) * SS);
+    C<R> p0 = MGT_SPINOR_LD(in + ((0 * 3 + c) * V + nb) * SS);
+    C<R> p1 = MGT_SPINOR_LD(in + ((1 * 3 + c) * V + nb) * SS);
+    C<R> p2 = g5in * MGT_SPINOR_LD(in + ((2 * 3 + c) * V + nb) * SS);
+    C<R> p3 = g5in * MGT_SPINOR_LD(in + ((3 * 3 + c) * V + nb) * SS);
     C<R> b0, b1;
     b_mul<MU>(p2, p3, b0, b1);
     if constexpr (FWD) {
