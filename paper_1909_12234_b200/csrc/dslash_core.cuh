@@ -56,15 +56,42 @@ __device__ __forceinline__ void bdag_mul(C<R> w0, C<R> w1, C<R> &o2, C<R> &o3) {
 
 // Native link storage: element e of link (mu, site) at ((mu*NL + e)*V + site),
 // NL = 9 (full 3x3, row-major) or 6 (rows 0 and 1; row 2 = conj(r0 x r1)).
+#ifndef MGT_LINK_PAIRS
+#define MGT_LINK_PAIRS 1
+#endif
+// With MGT_LINK_PAIRS the 12-real links are stored as 3 element pairs per
+// (mu, site), ((mu*3 + e/2)*V + site)*2 + (e & 1): one 256-bit (fp64) /
+// 128-bit (fp32) load per pair.
+template <typename R> struct alignas(2 * sizeof(cplx<R>)) cpair {
+  cplx<R> a, b;
+};
+template <int RECON>
+__host__ __device__ __forceinline__ int64_t link_index(int mu, int e, int64_t site, int64_t V) {
+  if constexpr (RECON == 12 && MGT_LINK_PAIRS)
+    return (((int64_t)mu * 3 + e / 2) * V + site) * 2 + (e & 1);
+  else
+    return ((int64_t)mu * (RECON / 2) + e) * V + site;
+}
+
 template <typename R, int RECON>
 struct LinkField {
   static constexpr int NL = RECON / 2;
   const cplx<R> *__restrict__ p;
   int64_t V;
   __device__ __forceinline__ void load(int mu, int64_t site, C<R> (&u)[3][3]) const {
-    const cplx<R> *q = p + (int64_t)mu * NL * V + site;
+    if constexpr (RECON == 12 && MGT_LINK_PAIRS) {
+      const cpair<R> *q = reinterpret_cast<const cpair<R> *>(p) + (int64_t)mu * 3 * V + site;
 #pragma unroll
-    for (int e = 0; e < NL; ++e) u[e / 3][e % 3] = ldc(q + e * V);
+      for (int pp = 0; pp < 3; ++pp) {
+        const cpair<R> v = q[pp * V];
+        u[(2 * pp) / 3][(2 * pp) % 3] = C<R>(v.a.x, v.a.y);
+        u[(2 * pp + 1) / 3][(2 * pp + 1) % 3] = C<R>(v.b.x, v.b.y);
+      }
+    } else {
+      const cplx<R> *q = p + (int64_t)mu * NL * V + site;
+#pragma unroll
+      for (int e = 0; e < NL; ++e) u[e / 3][e % 3] = ldc(q + e * V);
+    }
     if constexpr (RECON == 12) {
       // u2 = conj(u0 x u1)  (exact for SU(3): det = 1, unitary)
       u[2][0] = conj(u[0][1] * u[1][2] - u[0][2] * u[1][1]);

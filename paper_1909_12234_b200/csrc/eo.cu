@@ -17,9 +17,12 @@ __global__ void eo_links_kernel(EoGeom E, const cplx<R> *__restrict__ full, cplx
     const int64_t c = idx - (int64_t)p * E.Vh;
     int x[4];
     const int64_t f = eo_coords(E, p, c, x);
-    cplx<R> *dst = cb + (int64_t)p * 4 * NL * E.Vh + c;
+    cplx<R> *dst = cb + (int64_t)p * 4 * NL * E.Vh;
+    constexpr int RECON = 2 * NL;
 #pragma unroll
-    for (int k = 0; k < 4 * NL; ++k) dst[(int64_t)k * E.Vh] = full[(int64_t)k * E.g.V + f];
+    for (int mu = 0; mu < 4; ++mu)
+#pragma unroll
+      for (int e = 0; e < NL; ++e) dst[link_index<RECON>(mu, e, c, E.Vh)] = full[link_index<RECON>(mu, e, f, E.g.V)];
   }
 }
 

@@ -55,7 +55,7 @@ __global__ void links_from_ref_kernel(Geom g, const double2 *__restrict__ ref, c
         cplx<R> o;
         o.x = (R)v.x;
         o.y = (R)v.y;
-        out[((int64_t)mu * NL + e) * g.V + s] = o;
+        out[link_index<RECON>(mu, e, s, g.V)] = o;
       }
     }
   }
