@@ -303,6 +303,12 @@ def run_ours(args):
             if world == 1 and not args.skip_eigen:
                 probes4 = probes_config4(M, rank, world)
     probes5 = probes_config5(M, rank, world) if args.config5 else None
+    dsolve = None
+    if (world > 1 or args.dist_solve) and args.prec == 64:
+        try:
+            dsolve = distributed_solve_rate(M, dims, rank, world, args.recon)
+        except Exception as e:  # reported, not fatal
+            dsolve = {"error": str(e)[:300]}
 
     if rank == 0:
         line = {
@@ -335,6 +341,7 @@ def run_ours(args):
             "deflated_probes_per_sec": probes3,
             "eigen_deflated_probes_per_sec": probes4,
             "full_box_deflated_probes_per_sec": probes5,
+            "distributed_solve": dsolve,
         }
         if world == 1 and not args.skip_cpu:
             try:
@@ -346,6 +353,42 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def distributed_solve_rate(M, dims, rank, world, recon, iters=30):
+    """t-sharded BiCGStab on the global L0 x L1 x L2 x (T * world) lattice
+    (mgt_bicgstab_solve_slab: face exchange before every stencil pass, one
+    NCCL all-reduce per reduction point): a fixed number of iterations of a
+    4-rhs solve, timed with CUDA events, max over ranks."""
+    import types
+
+    import torch
+    from paper_1909_12234_b200.distributed import Communicator, SlabBiCGStab, SlabWilsonOperator
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    gglob = M.LatticeGeometry(dims[:3] + (dims[3] * world,), "antiperiodic")
+    gauge = M.generate_gauge(geo, "su3", eps=0.2, seed=100 + rank)
+    op = SlabWilsonOperator(types.SimpleNamespace(geometry=gglob), 0.1, rank, world, prec=64, recon=recon,
+                            local_links=gauge.links)
+    del gauge
+    solver = SlabBiCGStab(op, Communicator())
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7 + rank)
+    b = torch.randn((4, 12, geo.site_count), dtype=torch.complex128, device="cuda", generator=g)
+    solver.solve_native(b, 1e-14, 2)
+    _max_over_ranks(0.0, world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _, reps, _ = solver.solve_native(b, 1e-14, iters)
+    e1.record()
+    torch.cuda.synchronize()
+    sec = _max_over_ranks(e0.elapsed_time(e1) / 1e3, world)
+    its = max(r.iterations for r in reps)
+    sites = geo.site_count * world
+    return {"config": f"4-rhs BiCGStab, {iters} iterations, global {dims[0]}x{dims[1]}x{dims[2]}x{dims[3] * world}"
+                      f" t-sharded over {world} GPU(s), full system", "iterations": its,
+            "ms_per_iteration": sec / max(its, 1) * 1e3,
+            "model_GBps": 4608 * 4 * sites * its / sec / 1e9, "model": "4608 B/site/rhs per iteration"}
 
 
 def _max_over_ranks(v, world):
@@ -513,6 +556,8 @@ def main():
     ap.add_argument("--dims", default="48x48x48x96")
     ap.add_argument("--prec", type=int, default=64, choices=[64, 32])
     ap.add_argument("--recon", type=int, default=12, choices=[18, 12])
+    ap.add_argument("--dist-solve", action="store_true",
+                    help="also time the t-sharded BiCGStab at N = 1 (always on at N > 1)")
     ap.add_argument("--halo", default="auto", choices=["auto", "p2p", "nccl"],
                     help="t-slab halo transport at N > 1 (auto: p2p when it validates)")
     ap.add_argument("--skip-probes", action="store_true")

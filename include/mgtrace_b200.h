@@ -171,6 +171,26 @@ int mgt_ipc_free(void *dev_ptr);
 int mgt_ipc_open(const void *handle, void **dev_ptr);
 int mgt_ipc_close(void *dev_ptr);
 
+/* ---- distributed (t-slab) solve ------------------------------------------- */
+/* One communicator per rank (NCCL, loaded at run time): rank 0 makes the
+ * 128-byte unique id, the host broadcasts it (torch.distributed), every rank
+ * calls mgt_comm_create with its rank after selecting its device.
+ * mgt_bicgstab_solve_slab is mgt_bicgstab_solve for a slab handle: the same
+ * kernels leave rank-local sums for one all-reduce per reduction point, and
+ * every stencil pass exchanges the spin-projected t-faces (SURVEY 8(e).2,
+ * "Krylov dots: local partials + ncclAllReduce").  It solves the full
+ * system; reports, relres and the quadratic forms are global. */
+typedef struct mgt_comm_s *mgt_comm_t;
+int mgt_comm_unique_id(void *id_out /* 128 bytes */);
+int mgt_comm_create(mgt_comm_t *out, const void *id, int nranks, int rank);
+int mgt_comm_destroy(mgt_comm_t comm);
+int mgt_comm_allreduce(mgt_comm_t comm, double *buf_dev, int64_t n, void *stream);
+size_t mgt_bicgstab_slab_workspace_bytes(mgt_wilson_t h, int n_rhs);
+int mgt_bicgstab_solve_slab(mgt_wilson_t h, mgt_comm_t comm, const void *b_dev, void *x_dev,
+                            int n_rhs, int flags, double tau, double tol, int max_iter,
+                            void *workspace_dev, int64_t *report_out, double *relres_out,
+                            double *dot_out_host, void *stream);
+
 /* ---- BLAS-1 on native fields (fp64) -------------------------------------- */
 /* out[r] = sum_i conj(a_i) b_i for each of n_rhs fields of `len` complex
  * entries (deterministic fixed-order reduction; numpy vdot semantics). */

@@ -50,6 +50,13 @@ _SIGNATURES = {
     "mgt_wilson_eo_split": (ct.c_int, [vp, vp, vp, vp, ct.c_int, vp]),
     "mgt_wilson_eo_merge": (ct.c_int, [vp, vp, vp, vp, ct.c_int, vp]),
     "mgt_wilson_schur_apply": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp]),
+    "mgt_comm_unique_id": (ct.c_int, [vp]),
+    "mgt_comm_create": (ct.c_int, [ct.POINTER(ct.c_void_p), vp, ct.c_int, ct.c_int]),
+    "mgt_comm_destroy": (ct.c_int, [vp]),
+    "mgt_comm_allreduce": (ct.c_int, [vp, vp, ct.c_int64, vp]),
+    "mgt_bicgstab_slab_workspace_bytes": (ct.c_size_t, [vp, ct.c_int]),
+    "mgt_bicgstab_solve_slab": (ct.c_int, [vp, vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, ct.c_double, ct.c_int,
+                                           vp, c_i64_p, c_dbl_p, c_dbl_p, vp]),
     "mgt_ipc_alloc": (ct.c_int, [ct.c_size_t, ct.POINTER(ct.c_void_p), vp]),
     "mgt_ipc_free": (ct.c_int, [vp]),
     "mgt_ipc_open": (ct.c_int, [vp, ct.POINTER(ct.c_void_p)]),

@@ -20,8 +20,10 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
+#include "comm.cuh"
 #include "eo_core.cuh"
 #include "handle.cuh"
 #include "reduce.cuh"
@@ -44,6 +46,7 @@ struct BiWS {
   unsigned *ticket;
   unsigned long long *ctr;   // dynamic chunk counter (dslash kernels), reset by their last block
   unsigned long long *ctr2;  // counter of the eo first-half kernels, reset by the following kernel
+  double *red;               // distributed solve: rank-local sums handed to the all-reduce
   BiState *st;
 };
 
@@ -76,14 +79,16 @@ __device__ __forceinline__ bool cfinite(C<double> a) { return isfinite(a.re) && 
 
 // Last-block scalar recurrences of the stencil kernels (shared by the full
 // and the even-odd kernels).  They also reset the chunk counters.
-template <int NR>
-__device__ __forceinline__ void k1_finish(const BiWS &w, int64_t nchunks) {
-  double out[NR * 2];
-  reduce_finish_n<NR * 2>(w.partials, nchunks, w.ticket, out);
+template <int M>
+__device__ __forceinline__ void store_red(const BiWS &w, const double (&out)[M]) {
   if (threadIdx.x == 0) {
-    *w.ctr = 0ull;
-    *w.ctr2 = 0ull;
+#pragma unroll
+    for (int j = 0; j < M; ++j) w.red[j] = out[j];
   }
+}
+
+template <int NR>
+__device__ __forceinline__ void k1_logic(const BiWS &w, const double (&out)[NR * 2]) {
   const int r = threadIdx.x;
   if (r < NR && w.st[r].status == ST_RUN) {
     BiState &s = w.st[r];
@@ -98,14 +103,22 @@ __device__ __forceinline__ void k1_finish(const BiWS &w, int64_t nchunks) {
   }
 }
 
-template <int NR>
-__device__ __forceinline__ void k3_finish(const BiWS &w, int64_t nchunks) {
-  double out[NR * 3];
-  reduce_finish_n<NR * 3>(w.partials, nchunks, w.ticket, out);
+template <int NR, int DIST = 0>
+__device__ __forceinline__ void k1_finish(const BiWS &w, int64_t nchunks) {
+  double out[NR * 2];
+  reduce_finish_n<NR * 2>(w.partials, nchunks, w.ticket, out);
   if (threadIdx.x == 0) {
     *w.ctr = 0ull;
     *w.ctr2 = 0ull;
   }
+  if (DIST)
+    store_red<NR * 2>(w, out);
+  else
+    k1_logic<NR>(w, out);
+}
+
+template <int NR>
+__device__ __forceinline__ void k3_logic(const BiWS &w, const double (&out)[NR * 3]) {
   const int r = threadIdx.x;
   if (r < NR && w.st[r].status == ST_RUN) {
     BiState &s = w.st[r];
@@ -123,14 +136,22 @@ __device__ __forceinline__ void k3_finish(const BiWS &w, int64_t nchunks) {
   }
 }
 
-template <int NR>
-__device__ __forceinline__ void resid_finish(const BiWS &w, int64_t nchunks) {
-  double out[NR];
-  reduce_finish_n<NR>(w.partials, nchunks, w.ticket, out);
+template <int NR, int DIST = 0>
+__device__ __forceinline__ void k3_finish(const BiWS &w, int64_t nchunks) {
+  double out[NR * 3];
+  reduce_finish_n<NR * 3>(w.partials, nchunks, w.ticket, out);
   if (threadIdx.x == 0) {
     *w.ctr = 0ull;
     *w.ctr2 = 0ull;
   }
+  if (DIST)
+    store_red<NR * 3>(w, out);
+  else
+    k3_logic<NR>(w, out);
+}
+
+template <int NR>
+__device__ __forceinline__ void resid_logic(const BiWS &w, const double (&out)[NR]) {
   const int r = threadIdx.x;
   if (r < NR) {
     BiState &s = w.st[r];
@@ -151,6 +172,20 @@ __device__ __forceinline__ void resid_finish(const BiWS &w, int64_t nchunks) {
   }
 }
 
+template <int NR, int DIST = 0>
+__device__ __forceinline__ void resid_finish(const BiWS &w, int64_t nchunks) {
+  double out[NR];
+  reduce_finish_n<NR>(w.partials, nchunks, w.ticket, out);
+  if (threadIdx.x == 0) {
+    *w.ctr = 0ull;
+    *w.ctr2 = 0ull;
+  }
+  if (DIST)
+    store_red<NR>(w, out);
+  else
+    resid_logic<NR>(w, out);
+}
+
 template <int NR>
 __device__ __forceinline__ bool resid_active(int st) {
   return st == ST_CONV || st == ST_MAXIT || st == ST_BREAK;
@@ -159,6 +194,34 @@ __device__ __forceinline__ bool resid_active(int st) {
 // ---------------------------------------------------------------------------
 // init: b -> workspace, r = rhat = p = b, x = 0, |b|^2
 template <int NR>
+__device__ __forceinline__ void init_logic(const BiWS &w, const double (&out)[NR], double tol, int maxit,
+                                           int use_bfull) {
+  const int r = threadIdx.x;
+  if (r < NR) {
+    BiState &s = w.st[r];
+    const double b2 = out[r];
+    // even-odd: the stopping norm is the FULL right-hand side's (the Schur
+    // residual is the full residual), set by bi_eo_split
+    s.b2 = use_bfull ? s.bfull2 : b2;
+    s.r2 = b2;
+    s.s2 = b2;
+    s.true_r2 = b2;
+    s.tol2 = tol * tol * s.b2;
+    s.rho = C<double>(b2, 0.0);
+    s.alpha = C<double>(1.0, 0.0);
+    s.omega = C<double>(1.0, 0.0);
+    s.beta = C<double>(0.0, 0.0);
+    s.dotq = C<double>(0.0, 0.0);
+    s.half = 0;
+    s.iters = 0;
+    s.maxit = maxit;
+    s.matvecs = 0;
+    s.reason = 0;
+    s.status = (b2 == 0.0) ? ST_DONE : ST_RUN;
+  }
+}
+
+template <int NR, int DIST = 0>
 __global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *__restrict__ b, BiWS w, double tol,
                                                      int maxit, int use_bfull) {
   RhsMap<NR> m;
@@ -180,34 +243,15 @@ __global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *_
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    const int r = threadIdx.x;
-    if (r < NR) {
-      BiState &s = w.st[r];
-      const double b2 = out[r];
-      // even-odd: the stopping norm is the FULL right-hand side's (the Schur
-      // residual is the full residual), set by bi_eo_split
-      s.b2 = use_bfull ? s.bfull2 : b2;
-      s.r2 = b2;
-      s.s2 = b2;
-      s.true_r2 = b2;
-      s.tol2 = tol * tol * s.b2;
-      s.rho = C<double>(b2, 0.0);
-      s.alpha = C<double>(1.0, 0.0);
-      s.omega = C<double>(1.0, 0.0);
-      s.beta = C<double>(0.0, 0.0);
-      s.dotq = C<double>(0.0, 0.0);
-      s.half = 0;
-      s.iters = 0;
-      s.maxit = maxit;
-      s.matvecs = 0;
-      s.reason = 0;
-      s.status = (b2 == 0.0) ? ST_DONE : ST_RUN;
-    }
+    if (DIST)
+      store_red<NR>(w, out);
+    else
+      init_logic<NR>(w, out, tol, maxit, use_bfull);
   }
 }
 
 // K1: v = A p ; sigma = (rhat, v)
-template <int NR, int RECON>
+template <int NR, int RECON, int DIST = 0>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
@@ -220,7 +264,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<
     if (run_me && o < V) {
       const int64_t site = sched_site(P.sched, o);
       C<double> y[4][3], xc[4][3];
-      wilson_eval<double, RECON>(P, w.p + off, L, site, y, xc);
+      wilson_eval<double, RECON>(P, w.p + off, L, site, y, xc, m.rhs);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -234,11 +278,21 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<
     }
     chunk_publish<NR, 2>(acc, w.partials + chunk * NR * 2);
   }
-  if (last_block(w.ticket)) k1_finish<NR>(w, nchunks);
+  if (last_block(w.ticket)) k1_finish<NR, DIST>(w, nchunks);
+}
+
+template <int NR>
+__device__ __forceinline__ void k2_logic(const BiWS &w, const double (&out)[NR]) {
+  const int r = threadIdx.x;
+  if (r < NR && w.st[r].status == ST_RUN) {
+    BiState &s = w.st[r];
+    s.s2 = out[r];
+    s.half = (s.s2 <= s.tol2) ? 1 : 0;
+  }
 }
 
 // K2: s = r - alpha v ; |s|^2
-template <int NR>
+template <int NR, int DIST = 0>
 __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
@@ -260,17 +314,15 @@ __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    const int r = threadIdx.x;
-    if (r < NR && w.st[r].status == ST_RUN) {
-      BiState &s = w.st[r];
-      s.s2 = out[r];
-      s.half = (s.s2 <= s.tol2) ? 1 : 0;
-    }
+    if (DIST)
+      store_red<NR>(w, out);
+    else
+      k2_logic<NR>(w, out);
   }
 }
 
 // K3: t = A s ; (t, s), |t|^2
-template <int NR, int RECON>
+template <int NR, int RECON, int DIST = 0>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
@@ -283,7 +335,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<
     if (run_me && o < V) {
       const int64_t site = sched_site(P.sched, o);
       C<double> y[4][3], xc[4][3];
-      wilson_eval<double, RECON>(P, w.s + off, L, site, y, xc);
+      wilson_eval<double, RECON>(P, w.s + off, L, site, y, xc, m.rhs);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -297,11 +349,35 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<
     }
     chunk_publish<NR, 3>(acc, w.partials + chunk * NR * 3);
   }
-  if (last_block(w.ticket)) k3_finish<NR>(w, nchunks);
+  if (last_block(w.ticket)) k3_finish<NR, DIST>(w, nchunks);
+}
+
+template <int NR>
+__device__ __forceinline__ void k4_logic(const BiWS &w, const double (&out)[NR * 3]) {
+  const int r = threadIdx.x;
+  if (r < NR && w.st[r].status == ST_RUN) {
+    BiState &s = w.st[r];
+    C<double> rho_new(out[3 * r], out[3 * r + 1]);
+    s.r2 = out[3 * r + 2];
+    s.iters += 1;
+    if (s.r2 <= s.tol2 || s.half) {
+      s.status = ST_CONV;
+    } else if (czero(rho_new) || czero(s.omega) || !isfinite(s.r2)) {
+      s.status = ST_BREAK;
+      s.reason = 2;
+    } else {
+      s.beta = cdiv(rho_new, s.rho) * cdiv(s.alpha, s.omega);
+      s.rho = rho_new;
+      if (s.iters >= s.maxit) {
+        s.status = ST_MAXIT;
+        s.reason = 1;
+      }
+    }
+  }
 }
 
 // K4: x += alpha p + omega s ; r = s - omega t ; rho' = (rhat, r), |r|^2
-template <int NR>
+template <int NR, int DIST = 0>
 __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w) {
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
@@ -328,26 +404,10 @@ __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w) {
   if (reduce_publish<NR, 3>(acc, w.partials, w.ticket)) {
     double out[NR * 3];
     reduce_finish<NR * 3>(w.partials, w.ticket, out);
-    const int r = threadIdx.x;
-    if (r < NR && w.st[r].status == ST_RUN) {
-      BiState &s = w.st[r];
-      C<double> rho_new(out[3 * r], out[3 * r + 1]);
-      s.r2 = out[3 * r + 2];
-      s.iters += 1;
-      if (s.r2 <= s.tol2 || s.half) {
-        s.status = ST_CONV;
-      } else if (czero(rho_new) || czero(s.omega) || !isfinite(s.r2)) {
-        s.status = ST_BREAK;
-        s.reason = 2;
-      } else {
-        s.beta = cdiv(rho_new, s.rho) * cdiv(s.alpha, s.omega);
-        s.rho = rho_new;
-        if (s.iters >= s.maxit) {
-          s.status = ST_MAXIT;
-          s.reason = 1;
-        }
-      }
-    }
+    if (DIST)
+      store_red<NR * 3>(w, out);
+    else
+      k4_logic<NR>(w, out);
   }
 }
 
@@ -369,7 +429,7 @@ __global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWS w) {
 }
 
 // True residual r = b - A x for every rhs that stopped (CONV/MAXIT/BREAK)
-template <int NR, int RECON>
+template <int NR, int RECON, int DIST = 0>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
   bool any = false;
 #pragma unroll
@@ -389,7 +449,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
     if (act_me && o < V) {
       const int64_t site = sched_site(P.sched, o);
       C<double> y[4][3], xc[4][3];
-      wilson_eval<double, RECON>(P, w.x + off, L, site, y, xc);
+      wilson_eval<double, RECON>(P, w.x + off, L, site, y, xc, m.rhs);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -402,11 +462,25 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
     }
     chunk_publish<NR, 1>(acc, w.partials + chunk * NR);
   }
-  if (last_block(w.ticket)) resid_finish<NR>(w, nchunks);
+  if (last_block(w.ticket)) resid_finish<NR, DIST>(w, nchunks);
+}
+
+template <int NR>
+__device__ __forceinline__ void restart_logic(const BiWS &w, const double (&out)[NR]) {
+  const int r = threadIdx.x;
+  if (r < NR && w.st[r].status == ST_RESTART) {
+    BiState &s = w.st[r];
+    s.r2 = out[r];
+    s.rho = C<double>(s.r2, 0.0);
+    s.alpha = C<double>(1.0, 0.0);
+    s.omega = C<double>(1.0, 0.0);
+    s.half = 0;
+    s.status = ST_RUN;
+  }
 }
 
 // Restart for rhs flagged ST_RESTART: rhat = p = r (r holds the true residual)
-template <int NR>
+template <int NR, int DIST = 0>
 __global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w) {
   if (!any_status<NR>(w.st, ST_RESTART)) return;
   RhsMap<NR> m;
@@ -428,21 +502,15 @@ __global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w) {
   if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
     double out[NR];
     reduce_finish<NR>(w.partials, w.ticket, out);
-    const int r = threadIdx.x;
-    if (r < NR && w.st[r].status == ST_RESTART) {
-      BiState &s = w.st[r];
-      s.r2 = out[r];
-      s.rho = C<double>(s.r2, 0.0);
-      s.alpha = C<double>(1.0, 0.0);
-      s.omega = C<double>(1.0, 0.0);
-      s.half = 0;
-      s.status = ST_RUN;
-    }
+    if (DIST)
+      store_red<NR>(w, out);
+    else
+      restart_logic<NR>(w, out);
   }
 }
 
 // copy x out and q = vdot(b, x) per rhs (Hutchinson quadratic form, trace.py:104)
-template <int NR>
+template <int NR, int DIST = 0>
 __global__ void __launch_bounds__(kRedBlock) bi_final(int64_t V, double2 *__restrict__ xout, BiWS w) {
   RhsMap<NR> m;
   double acc[2] = {0.0, 0.0};
@@ -460,11 +528,12 @@ __global__ void __launch_bounds__(kRedBlock) bi_final(int64_t V, double2 *__rest
   if (reduce_publish<NR, 2>(acc, w.partials, w.ticket)) {
     double out[NR * 2];
     reduce_finish<NR * 2>(w.partials, w.ticket, out);
-    const int r = threadIdx.x;
-    if (r < NR) w.st[r].dotq = C<double>(out[2 * r], out[2 * r + 1]);
+    if (DIST)
+      store_red<NR * 2>(w, out);
+    else if (threadIdx.x < NR)
+      w.st[threadIdx.x].dotq = C<double>(out[2 * threadIdx.x], out[2 * threadIdx.x + 1]);
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // Even-odd (Schur) solve, eo_core.cuh.  Fields in the workspace are parity
@@ -727,6 +796,7 @@ static BiWS carve(char *q, const WSLayout &Lw, bool eo = false) {
   w.ticket = (unsigned *)q;
   w.ctr = (unsigned long long *)(q + 8);
   w.ctr2 = (unsigned long long *)(q + 16);
+  w.red = (double *)(q + 32);  // up to 28 doubles
   q += 256;
   w.st = (BiState *)q;
   return w;
@@ -915,6 +985,149 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
   return MGT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Distributed t-slab solve: the same kernels with DIST = 1
+// leave their rank-local sums in w.red; one all-reduce per reduction point
+// (2 / 1 / 3 / 3 doubles per rhs) and a one-block finisher (bi_fin) apply the
+// scalar recurrences identically on every rank, so every rank takes the same
+// control path.  Each stencil pass is preceded by the spin-projected face
+// exchange (halo pack + grouped NCCL send/recv).
+enum : int { FIN_INIT, FIN_K1, FIN_K2, FIN_K3, FIN_K4, FIN_RESID, FIN_RESTART, FIN_FINAL };
+
+template <int NR, int KIND>
+__global__ void __launch_bounds__(kRedBlock) bi_fin(BiWS w, double tol, int maxit) {
+  constexpr int M = (KIND == FIN_K1 || KIND == FIN_FINAL) ? 2 * NR : ((KIND == FIN_K3 || KIND == FIN_K4) ? 3 * NR : NR);
+  double out[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) out[j] = w.red[j];
+  if constexpr (KIND == FIN_INIT) init_logic<NR>(w, out, tol, maxit, 0);
+  if constexpr (KIND == FIN_K1) k1_logic<NR>(w, out);
+  if constexpr (KIND == FIN_K2) k2_logic<NR>(w, out);
+  if constexpr (KIND == FIN_K3) k3_logic<NR>(w, out);
+  if constexpr (KIND == FIN_K4) k4_logic<NR>(w, out);
+  if constexpr (KIND == FIN_RESID) resid_logic<NR>(w, out);
+  if constexpr (KIND == FIN_RESTART) restart_logic<NR>(w, out);
+  if constexpr (KIND == FIN_FINAL)
+    if (threadIdx.x < NR) w.st[threadIdx.x].dotq = C<double>(out[2 * threadIdx.x], out[2 * threadIdx.x + 1]);
+}
+
+static size_t slab_face_bytes(const mgt_wilson_s *h) {
+  return align_up((size_t)kMaxGroup * 6 * h->g.stride[3] * sizeof(double2), 256);
+}
+
+template <int NR, int RECON>
+static int solve_group_slab(mgt_wilson_s *h, mgt_comm_s *comm, const WilsonParams &P0, const double2 *b, double2 *x,
+                            char *ws, const WSLayout &Lw, double tol, int max_iter, int64_t *report, double *relres,
+                            double *dot_out, cudaStream_t st) {
+  const int64_t V = h->g.V;
+  BiWS w = carve(ws, Lw);
+  const size_t fb = slab_face_bytes(h);
+  char *hb = ws + Lw.total;
+  void *to_prev = hb, *to_next = hb + fb, *from_next = hb + 2 * fb, *from_prev = hb + 3 * fb;
+  const size_t face = (size_t)NR * 6 * h->g.stride[3] * sizeof(double2);
+  WilsonParams P = P0;
+  P.slab = 1;
+  P.halo_next = from_next;
+  P.halo_prev = from_prev;
+  LinkField<double, RECON> lf{reinterpret_cast<const double2 *>(h->links), V};
+  static int g_dsl = 0, g_str = 0;
+  if (!g_dsl) g_dsl = resident_grid(bi_k1<NR, RECON, 1>, kRedBlock, (int64_t)1 << 40);
+  if (!g_str) g_str = resident_grid(bi_k4<NR, 1>, kRedBlock, (int64_t)1 << 40);
+  const int64_t need = (V + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
+  const int gd = (int)std::min<int64_t>(g_dsl, need), grid = (int)std::min<int64_t>(g_str, need);
+  MGT_CUDA(cudaMemsetAsync(w.ticket, 0, 24, st));
+  auto fin = [&](auto kind_tag, int m) -> int {
+    constexpr int KIND = decltype(kind_tag)::value;
+    int rc = comm_allreduce_sum(comm, w.red, (size_t)m, st);
+    if (rc) return rc;
+    bi_fin<NR, KIND><<<1, kRedBlock, 0, st>>>(w, tol, max_iter);
+    note_launch(1);
+    return MGT_OK;
+  };
+  auto exchange = [&](const double2 *f) -> int {
+    int rc = halo_pack_native(h, P0, f, to_prev, to_next, NR, st);
+    if (rc) return rc;
+    note_launch(1);
+    return comm_halo(comm, to_prev, to_next, from_next, from_prev, face, st);
+  };
+#define MGT_FIN(K, M)                                             \
+  do {                                                            \
+    int rc_ = fin(std::integral_constant<int, K>{}, M);           \
+    if (rc_) return rc_;                                          \
+  } while (0)
+#define MGT_XCH(F)              \
+  do {                          \
+    int rc_ = exchange(F);      \
+    if (rc_) return rc_;        \
+  } while (0)
+  bi_init<NR, 1><<<grid, kRedBlock, 0, st>>>(V, b, w, tol, max_iter, 0);
+  note_launch(1);
+  MGT_FIN(FIN_INIT, NR);
+  static thread_local int *hf = nullptr;
+  if (!hf) MGT_CUDA(cudaMallocHost((void **)&hf, 64 * sizeof(int)));
+  for (int round = 0; round < 1000000; ++round) {
+    for (int it = 0; it < kChunk; ++it) {
+      MGT_XCH(w.p);
+      bi_k1<NR, RECON, 1><<<gd, kRedBlock, 0, st>>>(P, lf, w);
+      MGT_FIN(FIN_K1, 2 * NR);
+      bi_k2<NR, 1><<<grid, kRedBlock, 0, st>>>(V, w);
+      MGT_FIN(FIN_K2, NR);
+      MGT_XCH(w.s);
+      bi_k3<NR, RECON, 1><<<gd, kRedBlock, 0, st>>>(P, lf, w);
+      MGT_FIN(FIN_K3, 3 * NR);
+      bi_k4<NR, 1><<<grid, kRedBlock, 0, st>>>(V, w);
+      MGT_FIN(FIN_K4, 3 * NR);
+      bi_k5<NR><<<grid, kRedBlock, 0, st>>>(V, w);
+      note_launch(5);
+    }
+    MGT_LAUNCH_CHECK("distributed bicgstab chunk");
+    for (int r = 0; r < NR; ++r)
+      MGT_CUDA(cudaMemcpyAsync(hf + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MGT_CUDA(cudaStreamSynchronize(st));
+    bool running = false;
+    for (int r = 0; r < NR; ++r) running |= (hf[r] == ST_RUN);
+    if (running) continue;
+    MGT_XCH(w.x);
+    bi_resid<NR, RECON, 1><<<gd, kRedBlock, 0, st>>>(P, lf, w);
+    MGT_FIN(FIN_RESID, NR);
+    bi_restart<NR, 1><<<grid, kRedBlock, 0, st>>>(V, w);
+    MGT_FIN(FIN_RESTART, NR);
+    note_launch(2);
+    MGT_LAUNCH_CHECK("distributed bicgstab residual");
+    for (int r = 0; r < NR; ++r)
+      MGT_CUDA(cudaMemcpyAsync(hf + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MGT_CUDA(cudaStreamSynchronize(st));
+    bool again = false;
+    for (int r = 0; r < NR; ++r) again |= (hf[r] == ST_RUN);
+    if (!again) break;
+  }
+  bi_final<NR, 1><<<grid, kRedBlock, 0, st>>>(V, x, w);
+  note_launch(1);
+  MGT_FIN(FIN_FINAL, 2 * NR);
+#undef MGT_FIN
+#undef MGT_XCH
+  MGT_LAUNCH_CHECK("bi_final (distributed)");
+  std::vector<BiState> hs(NR);
+  MGT_CUDA(cudaMemcpyAsync(hs.data(), w.st, NR * sizeof(BiState), cudaMemcpyDeviceToHost, st));
+  MGT_CUDA(cudaStreamSynchronize(st));
+  for (int r = 0; r < NR; ++r) {
+    const BiState &s = hs[r];
+    const bool zero_rhs = s.b2 == 0.0;
+    const double rel = zero_rhs ? 0.0 : sqrt(s.true_r2 / s.b2);
+    const bool conv = zero_rhs || s.true_r2 <= s.tol2;
+    report[4 * r + 0] = s.iters;
+    report[4 * r + 1] = s.matvecs;
+    report[4 * r + 2] = conv ? 1 : 0;
+    report[4 * r + 3] = conv ? 0 : (s.reason ? s.reason : 1);
+    relres[r] = rel;
+    if (dot_out) {
+      dot_out[2 * r] = s.dotq.re;
+      dot_out[2 * r + 1] = s.dotq.im;
+    }
+  }
+  return MGT_OK;
+}
+
 }  // namespace mgt
 
 using namespace mgt;
@@ -967,6 +1180,50 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs
       rc = MGT_SOLVE(2);
     else
       rc = MGT_SOLVE(1);
+#undef MGT_SOLVE
+    if (rc) return rc;
+    r0 += nr;
+  }
+  return MGT_OK;
+}
+
+size_t mgt_bicgstab_slab_workspace_bytes(mgt_wilson_t h, int n_rhs) {
+  if (!h) return 0;
+  return ws_layout(h->g.V).total + 4 * slab_face_bytes(h);
+}
+
+int mgt_bicgstab_solve_slab(mgt_wilson_t h, mgt_comm_t comm, const void *b_dev, void *x_dev, int n_rhs, int flags,
+                            double tau, double tol, int max_iter, void *workspace_dev, int64_t *report_out,
+                            double *relres_out, double *dot_out_host, void *stream) {
+  if (!h || !comm || !b_dev || !x_dev || !workspace_dev || !report_out || !relres_out)
+    return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve_slab: null argument");
+  if (!h->slab) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve_slab: needs a slab handle");
+  if (h->prec != 64) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve_slab: needs a complex128 operator");
+  if (!(tol > 0.0 && tol < 1.0)) return fail(MGT_ERR_INVALID, "tol must be in (0,1)");
+  if (max_iter < 1) return fail(MGT_ERR_INVALID, "max_iter must be >= 1");
+  if (n_rhs < 1) return fail(MGT_ERR_INVALID, "n_rhs must be >= 1");
+  if (comm->nranks * h->g.L[3] != h->T_global)
+    return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve_slab: communicator size does not match the slab decomposition");
+  cudaStream_t st = as_stream(stream);
+  WilsonParams P = make_params(h, flags & ~MGT_SOLVE_FULL, tau);
+  const int64_t V = h->g.V;
+  WSLayout Lw = ws_layout(V);
+  const size_t field = (size_t)12 * V;
+  int r0 = 0;
+  while (r0 < n_rhs) {
+    const int left = n_rhs - r0;
+    const int nr = left >= 4 ? 4 : (left >= 2 ? 2 : 1);
+    const double2 *b = (const double2 *)b_dev + r0 * field;
+    double2 *x = (double2 *)x_dev + r0 * field;
+    double *dot = dot_out_host ? dot_out_host + 2 * r0 : nullptr;
+    char *ws = (char *)workspace_dev;
+    int rc;
+#define MGT_SOLVE(NR)                                                                                          \
+  (h->recon == 18 ? solve_group_slab<NR, 18>(h, comm, P, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
+                                              relres_out + r0, dot, st)                                        \
+                  : solve_group_slab<NR, 12>(h, comm, P, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
+                                              relres_out + r0, dot, st))
+    rc = nr == 4 ? MGT_SOLVE(4) : (nr == 2 ? MGT_SOLVE(2) : MGT_SOLVE(1));
 #undef MGT_SOLVE
     if (rc) return rc;
     r0 += nr;

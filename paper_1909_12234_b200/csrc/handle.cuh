@@ -79,6 +79,10 @@ inline WilsonParams make_params(const mgt_wilson_s *h, int flags, double tau) {
 bool eo_available(const mgt_wilson_s *h);
 int eo_prepare(mgt_wilson_s *h, cudaStream_t st);
 
+// the two spin-projected t-faces of x (slab.cu; no peer fence)
+int halo_pack_native(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *to_prev, void *to_next,
+                     int n_rhs, cudaStream_t st);
+
 // forget cached solver graphs of a handle (bicgstab.cu)
 void drop_graphs(const void *h);
 

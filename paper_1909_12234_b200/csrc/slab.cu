@@ -119,6 +119,15 @@ static int slab_t(const mgt_wilson_s *h, const WilsonParams &P, const void *x, v
   return MGT_OK;
 }
 
+int halo_pack_native(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *to_prev, void *to_next,
+                     int n_rhs, cudaStream_t st) {
+  if (h->prec == 64)
+    return h->recon == 18 ? pack_t<double, 18>(h, P, x, to_prev, to_next, n_rhs, 0, st)
+                          : pack_t<double, 12>(h, P, x, to_prev, to_next, n_rhs, 0, st);
+  return h->recon == 18 ? pack_t<float, 18>(h, P, x, to_prev, to_next, n_rhs, 0, st)
+                        : pack_t<float, 12>(h, P, x, to_prev, to_next, n_rhs, 0, st);
+}
+
 }  // namespace mgt
 
 using namespace mgt;

@@ -315,6 +315,90 @@ class SlabWilsonOperator:
         return out
 
 
+class Communicator:
+    """NCCL communicator of the distributed solver (`mgt_comm_*`, NCCL loaded
+    at run time by the native library).  Rank 0's 128-byte unique id is
+    broadcast over `group`; without an initialised process group this is the
+    single-rank communicator (no NCCL calls are made)."""
+
+    def __init__(self, group=None):
+        from . import _lib
+        self._lib = _lib
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+        uid = (_lib.ct.c_char * 128)()
+        if self.world > 1:
+            if self.rank == 0:
+                _lib.check(_lib.lib().mgt_comm_unique_id(uid), "nccl unique id")
+            box = [bytes(uid)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(box, src=src, group=group)
+            uid = (_lib.ct.c_char * 128).from_buffer_copy(box[0])
+        self.handle = _lib.ct.c_void_p()
+        _lib.check(_lib.lib().mgt_comm_create(_lib.ct.byref(self.handle), uid, self.world, self.rank),
+                   "communicator")
+
+    def allreduce_(self, t):
+        """In-place sum over ranks of a float64 CUDA tensor (stream-ordered)."""
+        from ._device import ptr, stream_ptr
+        self._lib.check(self._lib.lib().mgt_comm_allreduce(self.handle, ptr(t), t.numel(), stream_ptr()),
+                        "allreduce")
+        return t
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.lib().mgt_comm_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class SlabBiCGStab:
+    """Distributed BiCGStab on a t-slab operator (`mgt_bicgstab_solve_slab`):
+    rank-local fields (n, 12, V_local), one all-reduce per reduction point,
+    a face exchange before every stencil pass.  Reports, relative residuals
+    and the quadratic forms z^H A^-1 z are global (identical on every rank)."""
+
+    MAX_GROUP = 4
+
+    def __init__(self, slab_op, comm, flags=0, tau=0.0):
+        from . import _lib
+        from ._device import device
+        if slab_op.prec != 64:
+            raise ValueError("the Krylov solver runs in complex128")
+        if comm.world != slab_op.world:
+            raise ValueError(f"communicator has {comm.world} ranks, slab decomposition {slab_op.world}")
+        self.op, self.comm, self.flags, self.tau = slab_op, comm, int(flags), float(tau)
+        self._lib = _lib
+        nbytes = _lib.lib().mgt_bicgstab_slab_workspace_bytes(slab_op._handle, self.MAX_GROUP)
+        self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=device())
+
+    def solve_native(self, b, tol, max_iter, x=None, want_dot=False):
+        import ctypes as ct
+        from ._device import ptr, stream_ptr
+        from .krylov import REASONS, SolveReport
+        n = b.shape[0]
+        b = b.contiguous()
+        x = torch.empty_like(b) if x is None else x
+        rep = (ct.c_int64 * (4 * n))()
+        rel = (ct.c_double * n)()
+        dots = (ct.c_double * (2 * n))() if want_dot else None
+        self._lib.check(self._lib.lib().mgt_bicgstab_solve_slab(
+            self.op._handle, self.comm.handle, ptr(b), ptr(x), n, self.flags, self.tau, float(tol), int(max_iter),
+            ptr(self.workspace), rep, rel, dots, stream_ptr()), "distributed bicgstab")
+        reports = []
+        for r in range(n):
+            it, mv, conv, reason = rep[4 * r:4 * r + 4]
+            reports.append(SolveReport(int(it), float(rel[r]), bool(conv), int(mv),
+                                       "" if conv else REASONS.get(int(reason), "max_iter")))
+        dv = np.array([complex(dots[2 * r], dots[2 * r + 1]) for r in range(n)]) if want_dot else None
+        return x, reports, dv
+
+
 def distributed_hutchinson(inv_op, geometry, n_noise, kind="rademacher", seed=0, group=None):
     """Probe-sharded `hutchinson` (trace.py:122-132) over the ranks of `group`."""
     from .probing import build_probe_set
