@@ -232,6 +232,13 @@ int mgt_gcr_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m,
  * Written in NATIVE layout (layout != 0) or ref layout (layout == 0). */
 int mgt_noise(const int dims[4], int kind, const uint64_t *seeds_host,
               int n_fields, int native_layout, void *out_dev, void *stream);
+/* The same probes restricted to a t-slab [t_begin, t_begin + t_local) of
+ * the global lattice, in the slab's native layout: bit-identical to the
+ * corresponding sites of the global mgt_noise field (probe sharding of a
+ * t-sharded solve). */
+int mgt_noise_slab(const int dims_global[4], int t_begin, int t_local, int kind,
+                   const uint64_t *seeds_host, int n_fields, void *out_native_dev,
+                   void *stream);
 
 /* ---- prolongator ------------------------------------------------------------ */
 /* Block-orthonormal chirality-split prolongator (multigrid.py:116-225).

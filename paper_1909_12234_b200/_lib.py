@@ -73,6 +73,7 @@ _SIGNATURES = {
     "mgt_gcr_workspace_bytes": (ct.c_size_t, [vp, ct.c_int]),
     "mgt_gcr_solve": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp, c_i64_p, c_dbl_p, vp]),
     "mgt_noise": (ct.c_int, [c_int_p, ct.c_int, c_u64_p, ct.c_int, ct.c_int, vp, vp]),
+    "mgt_noise_slab": (ct.c_int, [c_int_p, ct.c_int, ct.c_int, ct.c_int, c_u64_p, ct.c_int, vp, vp]),
     "mgt_prolong_build": (ct.c_int, [c_int_p, c_int_p, ct.c_int, vp, vp, c_int_p, vp]),
     "mgt_prolong": (ct.c_int, [c_int_p, c_int_p, ct.c_int, vp, vp, vp, ct.c_int, vp]),
     "mgt_restrict": (ct.c_int, [c_int_p, c_int_p, ct.c_int, vp, vp, vp, ct.c_int, ct.c_int, vp]),

@@ -73,14 +73,16 @@ __device__ __forceinline__ void emit(uint32_t w, double2 *dst) {
 }
 
 template <int KIND, bool NATIVE>
-__global__ void noise_kernel(Geom g, const __grid_constant__ NoiseBatch nb, int nf, int field0, double2 *__restrict__ out) {
+__global__ void noise_kernel(Geom g, Geom gref, int t_begin, const __grid_constant__ NoiseBatch nb, int nf, int field0,
+                             double2 *__restrict__ out) {
   const int64_t n = g.V * nf;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
     const int f = (int)(idx / g.V);
     const int64_t s = idx - (int64_t)f * g.V;
     int x[4];
     native_coords(g, s, x);
-    const int64_t r = ref_site(g, x);
+    x[3] += t_begin;  // t-slab: the probe is the global one restricted to this slab
+    const int64_t r = ref_site(gref, x);
     // jump 6r steps: st <- A_k st + C_k
     U128 st = nb.state[f];
     const U128 inc = nb.inc[f];
@@ -128,12 +130,12 @@ static int ensure_pow_table() {
 
 using namespace mgt;
 
-extern "C" int mgt_noise(const int dims[4], int kind, const uint64_t *seeds_host, int n_fields, int native_layout,
-                         void *out_dev, void *stream) {
+static int noise_impl(const int dims[4], const int dims_ref[4], int t_begin, int kind, const uint64_t *seeds_host,
+                      int n_fields, int native_layout, void *out_dev, void *stream) {
   if (!dims || !seeds_host || !out_dev || n_fields < 0) return fail(MGT_ERR_INVALID, "mgt_noise: bad argument");
   if (kind != 0 && kind != 1) return fail(MGT_ERR_INVALID, "mgt_noise: kind must be 0 (rademacher) or 1 (z4)");
-  Geom g = make_geom(dims);
-  if ((uint64_t)g.V * 6u >= (1ull << kJumpBits)) return fail(MGT_ERR_INVALID, "mgt_noise: lattice too large");
+  Geom g = make_geom(dims), gref = make_geom(dims_ref);
+  if ((uint64_t)gref.V * 6u >= (1ull << kJumpBits)) return fail(MGT_ERR_INVALID, "mgt_noise: lattice too large");
   int rc = ensure_pow_table();
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
@@ -155,14 +157,28 @@ extern "C" int mgt_noise(const int dims[4], int kind, const uint64_t *seeds_host
     const int block = 128, grid = grid_for(g.V * nf, block, 8);
     double2 *o = (double2 *)out_dev;
     if (kind == 0 && native_layout)
-      noise_kernel<0, true><<<grid, block, 0, st>>>(g, nb, nf, f0, o);
+      noise_kernel<0, true><<<grid, block, 0, st>>>(g, gref, t_begin, nb, nf, f0, o);
     else if (kind == 0)
-      noise_kernel<0, false><<<grid, block, 0, st>>>(g, nb, nf, f0, o);
+      noise_kernel<0, false><<<grid, block, 0, st>>>(g, gref, t_begin, nb, nf, f0, o);
     else if (native_layout)
-      noise_kernel<1, true><<<grid, block, 0, st>>>(g, nb, nf, f0, o);
+      noise_kernel<1, true><<<grid, block, 0, st>>>(g, gref, t_begin, nb, nf, f0, o);
     else
-      noise_kernel<1, false><<<grid, block, 0, st>>>(g, nb, nf, f0, o);
+      noise_kernel<1, false><<<grid, block, 0, st>>>(g, gref, t_begin, nb, nf, f0, o);
     MGT_LAUNCH_CHECK("noise_kernel");
   }
   return MGT_OK;
+}
+
+extern "C" int mgt_noise(const int dims[4], int kind, const uint64_t *seeds_host, int n_fields, int native_layout,
+                         void *out_dev, void *stream) {
+  if (!dims) return fail(MGT_ERR_INVALID, "mgt_noise: bad argument");
+  return noise_impl(dims, dims, 0, kind, seeds_host, n_fields, native_layout, out_dev, stream);
+}
+
+extern "C" int mgt_noise_slab(const int dims_global[4], int t_begin, int t_local, int kind, const uint64_t *seeds_host,
+                              int n_fields, void *out_native_dev, void *stream) {
+  if (!dims_global || t_begin < 0 || t_local < 1 || t_begin + t_local > dims_global[3])
+    return fail(MGT_ERR_INVALID, "mgt_noise_slab: slab outside the global t range");
+  const int dl[4] = {dims_global[0], dims_global[1], dims_global[2], t_local};
+  return noise_impl(dl, dims_global, t_begin, kind, seeds_host, n_fields, 1, out_native_dev, stream);
 }

@@ -399,6 +399,23 @@ class SlabBiCGStab:
         return x, reports, dv
 
 
+def slab_hutchinson(solver, n_noise, kind="rademacher", seed=0, tol=1e-8, max_iter=2000):
+    """Hutchinson (trace.py:122-132) with t-sharded solves: every rank holds
+    its slab of each probe (`noise_native_slab`, bit-identical to the global
+    probe) and `SlabBiCGStab` returns the GLOBAL quadratic forms, so the
+    samples and the finished estimate are identical on every rank."""
+    from .probing import noise_native_slab
+    op = solver.op
+    samples, inversions = [], 0
+    for j0 in range(0, n_noise, SlabBiCGStab.MAX_GROUP):
+        j1 = min(n_noise, j0 + SlabBiCGStab.MAX_GROUP)
+        z = noise_native_slab(op.global_geometry, op.t_begin, op.t_local, [seed + j for j in range(j0, j1)], kind)
+        _, reps, q = solver.solve_native(z, tol, max_iter, want_dot=True)
+        samples.extend(q)
+        inversions += len(reps)
+    return finish(0.0, np.array(samples, dtype=np.complex128), inversions)
+
+
 def distributed_hutchinson(inv_op, geometry, n_noise, kind="rademacher", seed=0, group=None):
     """Probe-sharded `hutchinson` (trace.py:122-132) over the ranks of `group`."""
     from .probing import build_probe_set

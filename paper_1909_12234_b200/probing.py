@@ -58,6 +58,22 @@ def noise_native(geometry, seeds, kind="rademacher", out=None):
     return _noise_call(geometry.dims, kind, seeds, True, out)
 
 
+def noise_native_slab(geometry, t_begin, t_local, seeds, kind="rademacher", out=None):
+    """The global probes for `seeds` restricted to the t-slab
+    [t_begin, t_begin + t_local) of `geometry`, in the slab's native layout
+    (n, 12, V_slab): bit-identical to those sites of `noise_native`."""
+    if kind not in KINDS:
+        raise ValueError(f"GPU noise kind must be one of {sorted(KINDS)}, got {kind!r}")
+    V = int(np.prod(geometry.dims[:3])) * int(t_local)
+    if out is None:
+        out = torch.empty((len(seeds), 12, V), dtype=torch.complex128, device=device())
+    words = np.ascontiguousarray(seed_words(seeds))
+    _lib.check(_lib.lib().mgt_noise_slab(_lib.dims_arg(geometry.dims), int(t_begin), int(t_local), KINDS[kind],
+                                         words.ctypes.data_as(_lib.c_u64_p), len(seeds), ptr(out), stream_ptr()),
+               "noise (slab)")
+    return out
+
+
 def noise_ref(n, seeds, kind="rademacher"):
     """Noise vectors of length n in reference order, (len(seeds), n) on device."""
     sites = -(-n // 12)

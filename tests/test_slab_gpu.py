@@ -159,3 +159,29 @@ def test_distributed_solver_single_rank_matches_full_solver(cuda):
     assert torch.equal(comm.allreduce_(buf.clone()), buf)  # one rank: identity
     with pytest.raises(ValueError):
         SlabBiCGStab(SlabWilsonOperator(gauge, 0.1, 0, 2, recon=12), comm)
+
+
+def test_slab_noise_is_the_global_probe_restricted(cuda):
+    from paper_1909_12234_b200.probing import noise_native, noise_native_slab
+    M, geo, gauge = _setup((4, 6, 4, 12))
+    S3 = 4 * 6 * 4
+    for kind in ("rademacher", "z4"):
+        full = noise_native(geo, [5, 9, 123], kind)
+        for t0, tl in ((0, 12), (0, 3), (3, 6), (9, 3)):
+            sl = noise_native_slab(geo, t0, tl, [5, 9, 123], kind)
+            assert torch.equal(torch.view_as_real(sl), torch.view_as_real(full[:, :, t0 * S3:(t0 + tl) * S3]))
+
+
+def test_slab_hutchinson_single_rank(cuda):
+    """t-sharded Hutchinson on one rank == the single-GPU Hutchinson (full
+    system solves) within the solver tolerance; same probes bitwise."""
+    from paper_1909_12234_b200.distributed import Communicator, SlabBiCGStab, SlabWilsonOperator, slab_hutchinson
+    M, geo, gauge = _setup((4, 4, 4, 8), eps=0.2)
+    full = M.build_wilson(gauge, 0.1, recon=12)
+    slab = SlabWilsonOperator(gauge, 0.1, 0, 1, recon=12)
+    est = slab_hutchinson(SlabBiCGStab(slab, Communicator()), 6, seed=40, tol=1e-10)
+    ps = M.build_probe_set(geo, 12, 6, hp_count=1, dilution=False, kind="rademacher", seed=40)
+    ref = M.hutchinson(M.TruncatedInverse(full, M.SolveConfig(tol=1e-10)), ps)
+    assert est.inversions == 6
+    assert np.max(np.abs(est.samples - ref.samples) / np.abs(ref.samples)) < 1e-8
+    assert abs(est.mean - ref.mean) < 1e-9 * abs(ref.mean)
