@@ -215,6 +215,16 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev,
                        int max_iter, void *workspace_dev,
                        int64_t *report_out, double *relres_out,
                        double *dot_out_host, void *stream);
+/* Same, with the workspace size: groups of 4 rhs are batched into one launch
+ * per solver kernel (blockIdx.y = group), as many groups as a workspace of
+ * mgt_bicgstab_workspace_bytes(h, 4 * G) holds -- the small-lattice form
+ * (BASELINE configs 1/3/4) that replaces several concurrent 4-rhs solves.
+ * mgt_bicgstab_solve assumes the 4-rhs workspace. */
+int mgt_bicgstab_solve_ws(mgt_wilson_t h, const void *b_dev, void *x_dev,
+                          int n_rhs, int flags, double tau, double tol,
+                          int max_iter, void *workspace_dev, size_t workspace_bytes,
+                          int64_t *report_out, double *relres_out,
+                          double *dot_out_host, void *stream);
 
 /* Fixed-iteration restarted GCR(m) with zero start (krylov.py:52-118 with
  * max_iter = restart = m, as called by generate_null_vectors,

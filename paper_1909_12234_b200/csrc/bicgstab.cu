@@ -48,6 +48,25 @@ struct BiWS {
   unsigned long long *ctr2;  // counter of the eo first-half kernels, reset by the following kernel
   double *red;               // distributed solve: rank-local sums handed to the all-reduce
   BiState *st;
+  // batched solves: group g of kMaxGroup rhs (blockIdx.y) owns field slice
+  // g*gfield, partials g*gpart, ticket area g*256 B and states g*kMaxGroup
+  int64_t gfield, gpart;
+  __host__ __device__ __forceinline__ BiWS at(int g) const {
+    BiWS o = *this;
+    const int64_t f = (int64_t)g * gfield;
+    double2 *BiWS::*fs[11] = {&BiWS::r, &BiWS::rhat, &BiWS::p, &BiWS::v, &BiWS::s, &BiWS::t,
+                              &BiWS::x, &BiWS::b, &BiWS::be, &BiWS::bo, &BiWS::tmp};
+#pragma unroll
+    for (int i = 0; i < 11; ++i)
+      if (o.*fs[i]) o.*fs[i] += f;
+    o.partials += (int64_t)g * gpart;
+    o.ticket = (unsigned *)((char *)ticket + 256 * (int64_t)g);
+    o.ctr = (unsigned long long *)((char *)ctr + 256 * (int64_t)g);
+    o.ctr2 = (unsigned long long *)((char *)ctr2 + 256 * (int64_t)g);
+    o.red = (double *)((char *)red + 256 * (int64_t)g);
+    o.st += (int64_t)g * 4;
+    return o;
+  }
 };
 
 template <int NR>
@@ -222,10 +241,12 @@ __device__ __forceinline__ void init_logic(const BiWS &w, const double (&out)[NR
 }
 
 template <int NR, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *__restrict__ b, BiWS w, double tol,
+__global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *__restrict__ b, BiWS w_, double tol,
                                                      int maxit, int use_bfull) {
+  const BiWS w = w_.at(blockIdx.y);
   RhsMap<NR> m;
   double acc[1] = {0.0};
+  b += (int64_t)blockIdx.y * NR * 12 * V;
   MGT_SITE_LOOP(m, V) {
     const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
@@ -252,7 +273,8 @@ __global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *_
 
 // K1: v = A p ; sigma = (rhat, v)
 template <int NR, int RECON, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<double, RECON> L, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
@@ -293,7 +315,8 @@ __device__ __forceinline__ void k2_logic(const BiWS &w, const double (&out)[NR])
 
 // K2: s = r - alpha v ; |s|^2
 template <int NR, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
@@ -323,7 +346,8 @@ __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w) {
 
 // K3: t = A s ; (t, s), |t|^2
 template <int NR, int RECON, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<double, RECON> L, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
@@ -378,7 +402,8 @@ __device__ __forceinline__ void k4_logic(const BiWS &w, const double (&out)[NR *
 
 // K4: x += alpha p + omega s ; r = s - omega t ; rho' = (rhat, r), |r|^2
 template <int NR, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
@@ -413,7 +438,8 @@ __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w) {
 
 // K5: p = r + beta (p - omega v)
 template <int NR>
-__global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   if (w.st[m.rhs].status != ST_RUN) return;
@@ -430,7 +456,8 @@ __global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWS w) {
 
 // True residual r = b - A x for every rhs that stopped (CONV/MAXIT/BREAK)
 template <int NR, int RECON, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkField<double, RECON> L, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkField<double, RECON> L, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   bool any = false;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
@@ -481,7 +508,8 @@ __device__ __forceinline__ void restart_logic(const BiWS &w, const double (&out)
 
 // Restart for rhs flagged ST_RESTART: rhat = p = r (r holds the true residual)
 template <int NR, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RESTART)) return;
   RhsMap<NR> m;
   const bool act_me = w.st[m.rhs].status == ST_RESTART;
@@ -511,7 +539,9 @@ __global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w) {
 
 // copy x out and q = vdot(b, x) per rhs (Hutchinson quadratic form, trace.py:104)
 template <int NR, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock) bi_final(int64_t V, double2 *__restrict__ xout, BiWS w) {
+__global__ void __launch_bounds__(kRedBlock) bi_final(int64_t V, double2 *__restrict__ xout, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
+  xout += (int64_t)blockIdx.y * NR * 12 * V;
   RhsMap<NR> m;
   double acc[2] = {0.0, 0.0};
   MGT_SITE_LOOP(m, V) {
@@ -546,7 +576,9 @@ struct BiEo {
 
 // b (full) -> b_e, b_o, tmp = u_o = Dg^-1 G_out b_o ; |b|^2 of the full rhs
 template <int NR>
-__global__ void __launch_bounds__(kRedBlock) bi_eo_split(BiEo X, const double2 *__restrict__ b, BiWS w, double g5out) {
+__global__ void __launch_bounds__(kRedBlock) bi_eo_split(BiEo X, const double2 *__restrict__ b, BiWS w_, double g5out) {
+  const BiWS w = w_.at(blockIdx.y);
+  b += (int64_t)blockIdx.y * NR * 12 * X.E.g.V;
   RhsMap<NR> m;
   const int64_t Vh = X.E.Vh, V = X.E.g.V;
   const C<double> iu(X.R.iu_re, X.R.iu_im), id(X.R.id_re, X.R.id_im);
@@ -577,7 +609,8 @@ __global__ void __launch_bounds__(kRedBlock) bi_eo_split(BiEo X, const double2 *
 // bh_e = G_out [ G_out b_e + 1/2 H_eo u_o ]  -> w.b
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_rhs(BiEo X, LinkField<double, RECON> le,
-                                                          LinkField<double, RECON> lo, BiWS w) {
+                                                          LinkField<double, RECON> lo, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   RhsMap<NR> m;
   const int64_t Vh = X.E.Vh;
   const int64_t off = (int64_t)m.rhs * 12 * Vh;
@@ -596,8 +629,10 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_rhs(BiEo X, LinkField<doub
 // still iterating, mode 1: rhs whose true residual is due)
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<double, RECON> le,
-                                                            LinkField<double, RECON> lo, const double2 *f, BiWS w,
+                                                            LinkField<double, RECON> lo, const double2 *f, BiWS w_,
                                                             int mode) {
+  const BiWS w = w_.at(blockIdx.y);
+  f += (int64_t)blockIdx.y * w_.gfield;
   bool any = false;
 #pragma unroll
   for (int r = 0; r < NR; ++r) any |= mode ? resid_active<NR>(w.st[r].status) : w.st[r].status == ST_RUN;
@@ -624,7 +659,8 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<do
 // K1 (eo): v = S p = G_out [ Dg G_in p - 1/4 H_eo tmp ] ; sigma = (rhat, v)
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<double, RECON> le,
-                                                         LinkField<double, RECON> lo, BiWS w) {
+                                                         LinkField<double, RECON> lo, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
@@ -656,7 +692,8 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<doubl
 // K3 (eo): t = S s ; (t, s), |t|^2
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_k3_eo(BiEo X, LinkField<double, RECON> le,
-                                                         LinkField<double, RECON> lo, BiWS w) {
+                                                         LinkField<double, RECON> lo, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
@@ -688,7 +725,8 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3_eo(BiEo X, LinkField<doubl
 // true Schur residual r = bh - S x (= the full residual, odd rows exact)
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_resid_eo(BiEo X, LinkField<double, RECON> le,
-                                                            LinkField<double, RECON> lo, BiWS w) {
+                                                            LinkField<double, RECON> lo, BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
   bool any = false;
 #pragma unroll
   for (int r = 0; r < NR; ++r) any |= resid_active<NR>(w.st[r].status);
@@ -724,7 +762,9 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid_eo(BiEo X, LinkField<do
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_final(BiEo X, LinkField<double, RECON> le,
                                                             LinkField<double, RECON> lo, double2 *__restrict__ xout,
-                                                            BiWS w) {
+                                                            BiWS w_) {
+  const BiWS w = w_.at(blockIdx.y);
+  xout += (int64_t)blockIdx.y * NR * 12 * X.E.g.V;
   RhsMap<NR> m;
   const int64_t Vh = X.E.Vh, V = X.E.g.V;
   const int64_t off = (int64_t)m.rhs * 12 * Vh;
@@ -768,17 +808,26 @@ constexpr int kChunk = 8;  // iterations per graph replay
 
 struct WSLayout {
   size_t field, partials, total;
+  int64_t V;
+  int groups;
+  size_t gpart;  // partial doubles per group
 };
 
-static WSLayout ws_layout(int64_t V) {
+// groups: batched solves of groups * kMaxGroup rhs share one workspace (and
+// one launch per kernel, blockIdx.y = group)
+static WSLayout ws_layout(int64_t V, int groups = 1) {
   WSLayout L;
-  L.field = align_up((size_t)kMaxGroup * 12 * V * sizeof(double2), 512);
+  L.V = V;
+  L.groups = groups;
+  L.field = align_up((size_t)groups * kMaxGroup * 12 * V * sizeof(double2), 512);
   // static-grid kernels: one NR*NV slot per block; dynamic kernels: one per
   // chunk of 128 / NR sites (NR = 4 is the largest)
   const size_t per_block = (size_t)kNumSMs * 16 * kMaxGroup * 4;
   const size_t per_chunk = (size_t)((V + 31) / 32) * kMaxGroup * 3;
-  L.partials = align_up(std::max(per_block, per_chunk) * sizeof(double), 256);
-  L.total = 8 * L.field + L.partials + 256 /*ticket*/ + align_up(kMaxGroup * sizeof(BiState), 256);
+  L.gpart = align_up(std::max(per_block, per_chunk), 32);
+  L.partials = align_up((size_t)groups * L.gpart * sizeof(double), 256);
+  L.total = 8 * L.field + L.partials + 256 * (size_t)groups /*tickets*/ +
+            align_up((size_t)groups * kMaxGroup * sizeof(BiState), 256);
   return L;
 }
 
@@ -797,8 +846,10 @@ static BiWS carve(char *q, const WSLayout &Lw, bool eo = false) {
   w.ctr = (unsigned long long *)(q + 8);
   w.ctr2 = (unsigned long long *)(q + 16);
   w.red = (double *)(q + 32);  // up to 28 doubles
-  q += 256;
+  q += 256 * (size_t)Lw.groups;
   w.st = (BiState *)q;
+  w.gfield = (int64_t)kMaxGroup * 12 * (eo ? Lw.V / 2 : Lw.V);
+  w.gpart = (int64_t)Lw.gpart;
   return w;
 }
 
@@ -806,10 +857,11 @@ static BiWS carve(char *q, const WSLayout &Lw, bool eo = false) {
 // (workspace, NR, RECON, operator variant).
 struct GraphKey {
   const void *h, *ws;
-  int nr, recon, flags, eo;
+  int nr, recon, flags, eo, groups;
   double tau;
   bool operator<(const GraphKey &o) const {
-    return std::tie(h, ws, nr, recon, flags, eo, tau) < std::tie(o.h, o.ws, o.nr, o.recon, o.flags, o.eo, o.tau);
+    return std::tie(h, ws, nr, recon, flags, eo, groups, tau) <
+           std::tie(o.h, o.ws, o.nr, o.recon, o.flags, o.eo, o.groups, o.tau);
   }
 };
 static std::mutex g_graph_mu;
@@ -828,7 +880,7 @@ void drop_graphs(const void *h) {
 }
 
 template <int NR, int RECON>
-static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &lf, const BiWS &w, int gd, int grid,
+static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &lf, const BiWS &w, dim3 gd, dim3 grid,
                         cudaStream_t st) {
   const int64_t V = P.g.V;
   for (int it = 0; it < kChunk; ++it) {
@@ -843,7 +895,7 @@ static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &l
 
 template <int NR, int RECON>
 static int launch_chunk_eo(const BiEo &X, const LinkField<double, RECON> &le, const LinkField<double, RECON> &lo,
-                           const BiWS &w, int gd, int g1, int grid, cudaStream_t st) {
+                           const BiWS &w, dim3 gd, dim3 g1, dim3 grid, cudaStream_t st) {
   const int64_t Vh = X.E.Vh;
   for (int it = 0; it < kChunk; ++it) {
     bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
@@ -857,10 +909,28 @@ static int launch_chunk_eo(const BiEo &X, const LinkField<double, RECON> &le, co
   return MGT_OK;
 }
 
+// pinned per-thread mailbox for the solver states (concurrent solves on
+// several streams may share a handle)
+static BiState *state_mailbox(int n) {
+  static thread_local BiState *hs = nullptr;
+  static thread_local int cap = 0;
+  if (n > cap) {
+    if (hs) cudaFreeHost(hs);
+    cap = std::max(n, 64);
+    if (cudaMallocHost((void **)&hs, cap * sizeof(BiState)) != cudaSuccess) {
+      hs = nullptr;
+      cap = 0;
+    }
+  }
+  return hs;
+}
+
+// Solve G groups of NR rhs (G > 1 only with NR = kMaxGroup): one launch per
+// kernel for all groups (blockIdx.y = group).
 template <int NR, int RECON>
 static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b, double2 *x,
                        char *ws, const WSLayout &Lw, double tol, int max_iter, int64_t *report, double *relres,
-                       double *dot_out, bool eo, cudaStream_t st) {
+                       double *dot_out, bool eo, int G, cudaStream_t st) {
   const int64_t V = h->g.V;
   const int64_t Vs = eo ? V / 2 : V;  // sites of the solved system
   BiWS w = carve(ws, Lw, eo);
@@ -887,10 +957,13 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
   if (eo && !g_e1) g_e1 = resident_grid(bi_eo_first<NR, RECON>, kRedBlock, (int64_t)1 << 40);
   if (eo && !g_e2) g_e2 = resident_grid(bi_k1_eo<NR, RECON>, kRedBlock, (int64_t)1 << 40);
   const int64_t need = (Vs + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
-  const int grid = (int)std::min<int64_t>(g_str, need);
-  const int gd = (int)std::min<int64_t>(eo ? g_e2 : g_dsl, need);
-  const int g1 = eo ? (int)std::min<int64_t>(g_e1, need) : 0;
-  MGT_CUDA(cudaMemsetAsync(w.ticket, 0, 24, st));  // ticket and chunk counters
+  auto per_group = [&](int resident) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, std::max(1, resident / G)));
+  };
+  const dim3 grid(per_group(g_str), G);
+  const dim3 gd(per_group(eo ? g_e2 : g_dsl), G);
+  const dim3 g1(eo ? per_group(g_e1) : 1, G);
+  MGT_CUDA(cudaMemsetAsync(w.ticket, 0, 256 * (size_t)G, st));  // tickets and chunk counters
   if (eo) {
     bi_eo_split<NR><<<grid, kRedBlock, 0, st>>>(X, b, w, P.g5out);
     bi_eo_rhs<NR, RECON><<<grid, kRedBlock, 0, st>>>(X, le, lo, w);
@@ -905,7 +978,7 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
   cudaGraphExec_t exec = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    GraphKey key{h, ws, NR, RECON, flags, eo ? 1 : 0, tau};
+    GraphKey key{h, ws, NR, RECON, flags, eo ? 1 : 0, G, tau};
     auto it = g_graphs.find(key);
     if (it != g_graphs.end()) {
       exec = it->second;
@@ -928,19 +1001,26 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
     }
   }
   const int per_iter = eo ? 7 : 5;
-  // pinned per-thread mailbox: concurrent solves on several streams may share a handle
-  static thread_local int *hf = nullptr;
-  if (!hf) MGT_CUDA(cudaMallocHost((void **)&hf, 64 * sizeof(int)));
+  const int nst = G * NR;  // states of group g at w.st + g * kMaxGroup
+  BiState *hs = state_mailbox(G * kMaxGroup);
+  if (!hs) return fail(MGT_ERR_CUDA, "pinned state mailbox");
+  auto fetch = [&]() -> int {
+    MGT_CUDA(cudaMemcpyAsync(hs, w.st, (size_t)G * kMaxGroup * sizeof(BiState), cudaMemcpyDeviceToHost, st));
+    MGT_CUDA(cudaStreamSynchronize(st));
+    return MGT_OK;
+  };
+  auto any_state = [&](int want) {
+    for (int g = 0; g < G; ++g)
+      for (int r = 0; r < NR; ++r)
+        if (hs[g * kMaxGroup + r].status == want) return true;
+    return false;
+  };
   for (int round = 0; round < 1000000; ++round) {
     MGT_CUDA(cudaGraphLaunch(exec, st));
     note_launch(per_iter * kChunk);
-    MGT_CUDA(cudaMemcpyAsync(hf, &w.st[0].status, sizeof(int), cudaMemcpyDeviceToHost, st));
-    for (int r = 1; r < NR; ++r)
-      MGT_CUDA(cudaMemcpyAsync(hf + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
-    MGT_CUDA(cudaStreamSynchronize(st));
-    bool running = false;
-    for (int r = 0; r < NR; ++r) running |= (hf[r] == ST_RUN);
-    if (running) continue;
+    int rc = fetch();
+    if (rc) return rc;
+    if (any_state(ST_RUN)) continue;
     if (eo) {
       bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.x, w, 1);
       bi_resid_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
@@ -951,12 +1031,9 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
     bi_restart<NR><<<grid, kRedBlock, 0, st>>>(Vs, w);
     note_launch(2);
     MGT_LAUNCH_CHECK("bicgstab residual");
-    for (int r = 0; r < NR; ++r)
-      MGT_CUDA(cudaMemcpyAsync(hf + r, &w.st[r].status, sizeof(int), cudaMemcpyDeviceToHost, st));
-    MGT_CUDA(cudaStreamSynchronize(st));
-    bool again = false;
-    for (int r = 0; r < NR; ++r) again |= (hf[r] == ST_RUN);
-    if (!again) break;
+    rc = fetch();
+    if (rc) return rc;
+    if (!any_state(ST_RUN)) break;
   }
   if (eo)
     bi_eo_final<NR, RECON><<<grid, kRedBlock, 0, st>>>(X, le, lo, x, w);
@@ -964,24 +1041,26 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
     bi_final<NR><<<grid, kRedBlock, 0, st>>>(V, x, w);
   note_launch(1);
   MGT_LAUNCH_CHECK("bi_final");
-  std::vector<BiState> hs(NR);
-  MGT_CUDA(cudaMemcpyAsync(hs.data(), w.st, NR * sizeof(BiState), cudaMemcpyDeviceToHost, st));
-  MGT_CUDA(cudaStreamSynchronize(st));
-  for (int r = 0; r < NR; ++r) {
-    const BiState &s = hs[r];
-    const bool zero_rhs = s.b2 == 0.0;
-    const double rel = zero_rhs ? 0.0 : sqrt(s.true_r2 / s.b2);
-    const bool conv = zero_rhs || s.true_r2 <= s.tol2;
-    report[4 * r + 0] = s.iters;
-    report[4 * r + 1] = s.matvecs;
-    report[4 * r + 2] = conv ? 1 : 0;
-    report[4 * r + 3] = conv ? 0 : (s.reason ? s.reason : 1);
-    relres[r] = rel;
-    if (dot_out) {
-      dot_out[2 * r] = s.dotq.re;
-      dot_out[2 * r + 1] = s.dotq.im;
+  int rc = fetch();
+  if (rc) return rc;
+  (void)nst;
+  for (int g = 0; g < G; ++g)
+    for (int r = 0; r < NR; ++r) {
+      const BiState &s = hs[g * kMaxGroup + r];
+      const int i = g * NR + r;
+      const bool zero_rhs = s.b2 == 0.0;
+      const double rel = zero_rhs ? 0.0 : sqrt(s.true_r2 / s.b2);
+      const bool conv = zero_rhs || s.true_r2 <= s.tol2;
+      report[4 * i + 0] = s.iters;
+      report[4 * i + 1] = s.matvecs;
+      report[4 * i + 2] = conv ? 1 : 0;
+      report[4 * i + 3] = conv ? 0 : (s.reason ? s.reason : 1);
+      relres[i] = rel;
+      if (dot_out) {
+        dot_out[2 * i] = s.dotq.re;
+        dot_out[2 * i + 1] = s.dotq.im;
+      }
     }
-  }
   return MGT_OK;
 }
 
@@ -995,7 +1074,8 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
 enum : int { FIN_INIT, FIN_K1, FIN_K2, FIN_K3, FIN_K4, FIN_RESID, FIN_RESTART, FIN_FINAL };
 
 template <int NR, int KIND>
-__global__ void __launch_bounds__(kRedBlock) bi_fin(BiWS w, double tol, int maxit) {
+__global__ void __launch_bounds__(kRedBlock) bi_fin(BiWS w_, double tol, int maxit) {
+  const BiWS w = w_.at(blockIdx.y);
   constexpr int M = (KIND == FIN_K1 || KIND == FIN_FINAL) ? 2 * NR : ((KIND == FIN_K3 || KIND == FIN_K4) ? 3 * NR : NR);
   double out[M];
 #pragma unroll
@@ -1136,12 +1216,12 @@ extern "C" {
 
 size_t mgt_bicgstab_workspace_bytes(mgt_wilson_t h, int n_rhs) {
   if (!h) return 0;
-  return ws_layout(h->g.V).total;
+  return ws_layout(h->g.V, std::max(1, n_rhs / kMaxGroup)).total;
 }
 
-int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau, double tol,
-                       int max_iter, void *workspace_dev, int64_t *report_out, double *relres_out,
-                       double *dot_out_host, void *stream) {
+static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau,
+                               double tol, int max_iter, void *workspace_dev, size_t workspace_bytes,
+                               int64_t *report_out, double *relres_out, double *dot_out_host, void *stream) {
   if (!h || !b_dev || !x_dev || !workspace_dev || !report_out || !relres_out)
     return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: null argument");
   if (h->prec != 64) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: needs a complex128 operator");
@@ -1158,33 +1238,55 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs
   }
   WilsonParams P = make_params(h, flags, tau);
   const int64_t V = h->g.V;
-  WSLayout Lw = ws_layout(V);
+  // groups of kMaxGroup rhs batched into one launch per kernel, as many as
+  // the workspace holds
+  int gmax = 1;
+  while (gmax < 64 && ws_layout(V, gmax + 1).total <= workspace_bytes) ++gmax;
+  if (ws_layout(V, 1).total > workspace_bytes) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: workspace too small");
   const size_t field = (size_t)12 * V;
   int r0 = 0;
   while (r0 < n_rhs) {
     const int left = n_rhs - r0;
-    const int nr = left >= 4 ? 4 : (left >= 2 ? 2 : 1);
+    const int G = std::min(gmax, left / kMaxGroup);
+    const int nr = G >= 1 ? 4 : (left >= 2 ? 2 : 1);
+    const int Gc = std::max(G, 1);
+    const WSLayout Lw = ws_layout(V, Gc);
     const double2 *b = (const double2 *)b_dev + r0 * field;
     double2 *x = (double2 *)x_dev + r0 * field;
     double *dot = dot_out_host ? dot_out_host + 2 * r0 : nullptr;
     char *ws = (char *)workspace_dev;
     int rc;
-#define MGT_SOLVE(NR)                                                                                           \
+#define MGT_SOLVE(NR, GG)                                                                                       \
   (h->recon == 18 ? solve_group<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
-                                         relres_out + r0, dot, eo, st)                                           \
+                                         relres_out + r0, dot, eo, GG, st)                                       \
                   : solve_group<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
-                                         relres_out + r0, dot, eo, st))
+                                         relres_out + r0, dot, eo, GG, st))
     if (nr == 4)
-      rc = MGT_SOLVE(4);
+      rc = MGT_SOLVE(4, Gc);
     else if (nr == 2)
-      rc = MGT_SOLVE(2);
+      rc = MGT_SOLVE(2, 1);
     else
-      rc = MGT_SOLVE(1);
+      rc = MGT_SOLVE(1, 1);
 #undef MGT_SOLVE
     if (rc) return rc;
-    r0 += nr;
+    r0 += nr * Gc;
   }
   return MGT_OK;
+}
+
+int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau, double tol,
+                       int max_iter, void *workspace_dev, int64_t *report_out, double *relres_out,
+                       double *dot_out_host, void *stream) {
+  if (!h) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: null argument");
+  return bicgstab_solve_impl(h, b_dev, x_dev, n_rhs, flags, tau, tol, max_iter, workspace_dev,
+                             ws_layout(h->g.V, 1).total, report_out, relres_out, dot_out_host, stream);
+}
+
+int mgt_bicgstab_solve_ws(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau,
+                          double tol, int max_iter, void *workspace_dev, size_t workspace_bytes, int64_t *report_out,
+                          double *relres_out, double *dot_out_host, void *stream) {
+  return bicgstab_solve_impl(h, b_dev, x_dev, n_rhs, flags, tau, tol, max_iter, workspace_dev, workspace_bytes,
+                             report_out, relres_out, dot_out_host, stream);
 }
 
 size_t mgt_bicgstab_slab_workspace_bytes(mgt_wilson_t h, int n_rhs) {

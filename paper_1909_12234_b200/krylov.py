@@ -63,17 +63,32 @@ def _base_operator(op):
     raise TypeError(f"GPU solver needs a WilsonOperator (or a form of one), got {type(op)}")
 
 
+def solve_batch(volume):
+    """Right-hand sides per solver call: groups of 4 rhs are batched into one
+    launch per kernel (blockIdx.y) until ~8 resident waves of 148 SMs x 384
+    threads are busy (even-odd: V/2 sites per group and rhs), at most 8
+    groups.  MGT_SOLVE_BATCH overrides."""
+    import os
+    if os.environ.get("MGT_SOLVE_BATCH"):
+        return max(4, 4 * (int(os.environ["MGT_SOLVE_BATCH"]) // 4))
+    want = 8 * 148 * 384
+    groups = -(-want // (4 * max(1, volume // 2)))
+    return 4 * int(max(1, min(8, groups)))
+
+
 class BiCGStab:
-    """Reusable solver state (device workspace) for one operator."""
+    """Reusable solver state (device workspace) for one operator; one call
+    solves up to `max_rhs` systems (batched groups of 4)."""
 
     MAX_GROUP = 4
 
-    def __init__(self, op):
+    def __init__(self, op, max_rhs=None):
         self.op, self.flags, self.tau = _base_operator(op)
         if self.op.prec != 64:
             raise ValueError("the Krylov solver runs in complex128")
-        nbytes = _lib.lib().mgt_bicgstab_workspace_bytes(self.op.handle, self.MAX_GROUP)
-        self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=device())
+        self.max_rhs = int(max_rhs) if max_rhs else solve_batch(self.op.volume)
+        self.ws_bytes = int(_lib.lib().mgt_bicgstab_workspace_bytes(self.op.handle, self.max_rhs))
+        self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device())
 
     def solve_native(self, b, tol, max_iter, x=None, want_dot=False, even_odd=True):
         """Solve A x_r = b_r for native fields b (n, 12, V); returns
@@ -86,10 +101,10 @@ class BiCGStab:
         rep = (ct.c_int64 * (4 * n))()
         rel = (ct.c_double * n)()
         dots = (ct.c_double * (2 * n))() if want_dot else None
-        _lib.check(_lib.lib().mgt_bicgstab_solve(
+        _lib.check(_lib.lib().mgt_bicgstab_solve_ws(
             self.op.handle, ptr(b), ptr(x), n, int(self.flags) | (0 if even_odd else _lib.SOLVE_FULL),
             float(self.tau), float(tol), int(max_iter),
-            ptr(self.workspace), rep, rel, dots, stream_ptr()), "bicgstab")
+            ptr(self.workspace), self.ws_bytes, rep, rel, dots, stream_ptr()), "bicgstab")
         reports = []
         for r in range(n):
             it, mv, conv, reason = rep[4 * r:4 * r + 4]
@@ -166,8 +181,8 @@ class TruncatedInverse:
         """Batched native-layout application (the estimators' fast path)."""
         solver = _solver_for(self.op)
         xs, reps, dots = [], [], []
-        for r0 in range(0, b.shape[0], BiCGStab.MAX_GROUP):
-            x, rr, d = solver.solve_native(b[r0:r0 + BiCGStab.MAX_GROUP], self.config.tol,
+        for r0 in range(0, b.shape[0], solver.max_rhs):
+            x, rr, d = solver.solve_native(b[r0:r0 + solver.max_rhs], self.config.tol,
                                            self.config.max_iter, want_dot=want_dot,
                                            even_odd=getattr(self.config, "even_odd", True))
             xs.append(x)

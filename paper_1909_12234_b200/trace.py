@@ -83,7 +83,7 @@ def _warn_flagged(flagged):
 
 
 def _solve_batches_concurrently(inv_op, probes, batches, correction, streams):
-    """Solve probe batches (4 rhs each) on `streams` CUDA streams from host
+    """Solve probe batches (one multi-rhs solve each) on `streams` CUDA streams from host
     worker threads: at small volumes one multi-rhs solve cannot fill 148 SMs,
     several independent ones can.  Returns [(reports, q)] in batch order;
     every result is a pure function of its probes (bitwise reproducible)."""
@@ -133,18 +133,19 @@ def _worker_pool(n):
 
 
 def default_streams(volume, batch=4):
-    """Concurrent multi-rhs solves needed to fill the GPU: one 4-rhs even-odd
-    solve of V sites exposes 4 V/2 stencil threads per kernel; ~8 resident
-    waves of 148 SMs x 384 threads hide the per-kernel launch and tail gaps
-    (measured on B200: 16^4 saturates at 4 streams, 8^4 at 8)."""
+    """Concurrent multi-rhs solves: one even-odd solve of `batch` rhs on V
+    sites exposes batch V/2 stencil threads per kernel; ~32 resident waves
+    of 148 SMs x 384 threads in flight hide the per-kernel launch/tail gaps
+    and the host-side status polls (measured on B200, tools/batch_sweep.sh:
+    16^4 best at 16 rhs x 4 streams, 8^4 at 32 rhs x 1)."""
     import os
     if os.environ.get("MGT_SOLVE_STREAMS"):
         return max(1, int(os.environ["MGT_SOLVE_STREAMS"]))
-    want = 8 * 148 * 384
+    want = 32 * 148 * 384
     return int(max(1, min(8, -(-want // (batch * max(1, volume // 2))))))
 
 
-def group_samples_gpu(inv_op, probes, batch=4, correction=None, streams=None, deferred=None):
+def group_samples_gpu(inv_op, probes, batch=None, correction=None, streams=None, deferred=None):
     """Per-group samples sum_slots w * vdot(slot, A^-1 slot) with the solves
     batched on the GPU; `correction(j, slots_native, x_native)` may return a
     per-slot complex array subtracted from the quadratic forms (deflation).
@@ -160,6 +161,9 @@ def group_samples_gpu(inv_op, probes, batch=4, correction=None, streams=None, de
     if deferred is not None:
         correction = lambda j0, z, x: deferred[0](j0, z, x) or 0.0  # noqa: E731
     if probes.slots_per_group == 1:
+        if batch is None:
+            from .krylov import solve_batch
+            batch = solve_batch(probes.geometry.site_count)
         batches = [(j0, min(ns, j0 + batch)) for j0 in range(0, ns, batch)]
         if streams is None:
             streams = default_streams(probes.geometry.site_count, batch)

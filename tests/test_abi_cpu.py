@@ -129,7 +129,9 @@ def test_estimator_statistics_match_reference_formulas():
 
 def test_default_streams_rule():
     from paper_1909_12234_b200.trace import default_streams
-    assert default_streams(8 ** 4) == 8
-    assert default_streams(12 ** 4) == 8
-    assert default_streams(16 ** 4) == 4
-    assert default_streams(32 ** 4) == 1
+    from paper_1909_12234_b200.krylov import solve_batch
+    assert solve_batch(8 ** 4) == 32 and solve_batch(16 ** 4) == 16 and solve_batch(32 ** 4) == 4
+    assert default_streams(8 ** 4, 32) == 8
+    assert default_streams(16 ** 4, 16) == 4
+    assert default_streams(32 ** 4, 4) == 1
+    assert default_streams(48 ** 3 * 96, 4) == 1
