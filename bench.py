@@ -423,6 +423,14 @@ def _sharded_estimate(M, estimate, geo, s, seed, rank, world, reps=2):
     return est, _max_over_ranks(el, world)
 
 
+def _solver_desc(volume):
+    from paper_1909_12234_b200.krylov import solve_batch
+    from paper_1909_12234_b200.trace import default_streams
+    b = solve_batch(volume)
+    return (f"BiCGStab on the even-odd Schur complement (stopping test on the full residual), {b} rhs per "
+            f"solve call (batched groups of 4), up to {default_streams(volume, b)} concurrent solve streams")
+
+
 def probes_config1(M, rank, world, dims=(8, 8, 8, 8), s=32, tol=1e-8):
     """BASELINE configs[0]: undeflated Hutchinson, 8^4, s = 32, tol 1e-8."""
     geo = M.LatticeGeometry(dims, "antiperiodic")
@@ -432,7 +440,7 @@ def probes_config1(M, rank, world, dims=(8, 8, 8, 8), s=32, tol=1e-8):
     its = inv.total_iterations / max(1, inv.n_solves)
     return {"config": "8x8x8x8 eps=0.2 m0=0.1 s=32 rademacher tol=1e-8 (BASELINE configs[0])",
             "value": s / el, "unit": "probes/s", "seconds": el, "mean_iterations": its,
-            "solver": "BiCGStab on the even-odd Schur complement (stopping test on the full residual), 4 rhs per solve, 8 concurrent solves",
+            "solver": _solver_desc(geo.site_count),
             "estimate_re": float(est.mean.real) if world == 1 else None}
 
 
@@ -463,7 +471,7 @@ def probes_config3(M, rank, world, dims=(16, 16, 16, 16), s=128, tol=1e-8, nv=24
             "value_including_setup": s / (el + setup), "Nc": pro.coarse_dim,
             "t0_re": float(est.t0.real), "estimate_re": float(est.mean.real) if world == 1 else None,
             "variance": float(est.variance) if world == 1 else None,
-            "mean_iterations": inv.total_iterations / max(1, inv.n_solves)}
+            "mean_iterations": inv.total_iterations / max(1, inv.n_solves), "solver": _solver_desc(geo.site_count)}
 
 
 def probes_config4(M, rank, world, dims=(16, 16, 16, 16), s=128, k=64, tol=1e-8):
