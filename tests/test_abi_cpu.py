@@ -7,6 +7,7 @@ import ctypes as ct
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -135,3 +136,22 @@ def test_default_streams_rule():
     assert default_streams(16 ** 4, 16) == 4
     assert default_streams(32 ** 4, 4) == 1
     assert default_streams(48 ** 3 * 96, 4) == 1
+
+
+@pytest.mark.parametrize("restart,max_iter,tol", [(8, 8, 1e-12), (4, 30, 1e-10), (32, 200, 1e-9)])
+def test_coarse_level_gcr_follows_the_reference_control_flow(restart, max_iter, tol):
+    """mglevel.gcr_torch (the coarse-level GCR of 3-level hierarchies and
+    smoothers) against the oracle's restatement of krylov.py:52-118 on a
+    CPU tensor: same iterations, matvec count, convergence flag and x."""
+    import torch
+    from oracle import krylov as OK
+    from paper_1909_12234_b200.mglevel import gcr_torch
+    rng = np.random.default_rng(restart + max_iter)
+    n = 60
+    A = np.eye(n) * 3 + (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))) / np.sqrt(n)
+    b = rng.normal(size=n) + 1j * rng.normal(size=n)
+    At, bt = torch.as_tensor(A), torch.as_tensor(b)
+    x, rep = gcr_torch(lambda v: At @ v, bt, tol, max_iter, restart)
+    xo, ro = OK.gcr(lambda v: A @ v, b, tol, max_iter, restart)
+    assert rep.iterations == ro.iterations and rep.matvecs == ro.matvecs and rep.converged == ro.converged
+    assert np.linalg.norm(x.numpy() - xo) <= 1e-12 * np.linalg.norm(xo)
