@@ -293,6 +293,12 @@ int mgt_coarse_build(mgt_wilson_t h, const int block[4], int nv,
 int mgt_coarse_apply(const int dims[4], const int block[4], int nv,
                      const void *C_dev, const void *xc_dev, void *yc_dev,
                      int n_rhs, void *stream);
+/* The same stencil with the fp32 copy of C (half the bytes; fp64 vectors and
+ * accumulation): used for the loose (tol >= 1e-5) inner solves of the coarse
+ * Davidson, whose explicit-residual confirmation stays on the fp64 C. */
+int mgt_coarse_apply_c32(const int dims[4], const int block[4], int nv,
+                         const void *C32_dev, const void *xc_dev, void *yc_dev,
+                         int n_rhs, void *stream);
 
 /* ---- deflation projection (trace.py:161-188, :266-267; eigen.py:79-86) --- */
 /* H (k x s, column major, complex128) = V^H X;  V: (k, len) row-major

@@ -128,8 +128,10 @@ __global__ void scatter_column_kernel(int64_t nb, int nc, int col, const double2
 // block is contiguous in rows); the neighbour vectors are staged in shared
 // memory and read as broadcasts.  The G group partials are summed in group
 // order (fixed, deterministic).
-template <int NR>
-__global__ void __launch_bounds__(256) coarse_apply_kernel(CoarseGeom cg, int G, const double2 *__restrict__ Cm,
+// CT: double2 (the Galerkin operator) or float2 (its fp32 copy for loose
+// inner solves: half the bytes, fp64 vectors and accumulation)
+template <int NR, typename CT = double2>
+__global__ void __launch_bounds__(256) coarse_apply_kernel(CoarseGeom cg, int G, const CT *__restrict__ Cm,
                                                            const double2 *__restrict__ x, double2 *__restrict__ y) {
   extern __shared__ double2 sm[];
   const int nc = cg.nc;
@@ -148,11 +150,12 @@ __global__ void __launch_bounds__(256) coarse_apply_kernel(CoarseGeom cg, int G,
 #pragma unroll
     for (int r = 0; r < NR; ++r) acc[r] = C<double>(0.0, 0.0);
     for (int dir = grp; dir < 9; dir += G) {
-      const double2 *Cb = Cm + (b * 9 + dir) * (int64_t)nc * nc + row;
+      const CT *Cb = Cm + (b * 9 + dir) * (int64_t)nc * nc + row;
       const double2 *xs = sx + dir * nc * NR;
 #pragma unroll 4
       for (int col = 0; col < nc; ++col) {
-        const C<double> cv = ldc(Cb + (int64_t)col * nc);
+        const auto cl = ldc(Cb + (int64_t)col * nc);
+        const C<double> cv((double)cl.re, (double)cl.im);
 #pragma unroll
         for (int r = 0; r < NR; ++r) acc[r] = cfma(cv, C<double>(xs[col * NR + r].x, xs[col * NR + r].y), acc[r]);
       }
@@ -172,8 +175,8 @@ __global__ void __launch_bounds__(256) coarse_apply_kernel(CoarseGeom cg, int G,
   }
 }
 
-template <int NR>
-static int launch_coarse_apply(const CoarseGeom &cg, const double2 *C, const double2 *x, double2 *y,
+template <int NR, typename CT = double2>
+static int launch_coarse_apply(const CoarseGeom &cg, const CT *C, const double2 *x, double2 *y,
                                cudaStream_t st) {
   const int G = std::max(1, std::min(9, 256 / cg.nc));
   const int block = ((G * cg.nc + 31) / 32) * 32;
@@ -181,11 +184,12 @@ static int launch_coarse_apply(const CoarseGeom &cg, const double2 *C, const dou
   if (smem > 48 * 1024) {
     static size_t set = 0;
     if (smem > set) {
-      MGT_CUDA(cudaFuncSetAttribute(coarse_apply_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      MGT_CUDA(cudaFuncSetAttribute(coarse_apply_kernel<NR, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
       set = smem;
     }
   }
-  coarse_apply_kernel<NR><<<(unsigned)cg.nb, block, smem, st>>>(cg, G, C, x, y);
+  coarse_apply_kernel<NR, CT><<<(unsigned)cg.nb, block, smem, st>>>(cg, G, C, x, y);
   MGT_LAUNCH_CHECK("coarse_apply_kernel");
   return MGT_OK;
 }
@@ -251,8 +255,12 @@ int mgt_coarse_build(mgt_wilson_t h, const int block[4], int nv, const void *P_d
   return rc;
 }
 
-int mgt_coarse_apply(const int dims[4], const int block[4], int nv, const void *C_dev, const void *xc_dev,
-                     void *yc_dev, int n_rhs, void *stream) {
+}  // extern "C"
+
+namespace mgt {
+template <typename CT>
+static int coarse_apply_impl(const int dims[4], const int block[4], int nv, const void *C_dev, const void *xc_dev,
+                             void *yc_dev, int n_rhs, void *stream) {
   if (!dims || !block || !C_dev || !xc_dev || !yc_dev || n_rhs < 1)
     return fail(MGT_ERR_INVALID, "mgt_coarse_apply: bad argument");
   if (xc_dev == yc_dev) return fail(MGT_ERR_INVALID, "mgt_coarse_apply: in-place apply is not supported");
@@ -260,20 +268,34 @@ int mgt_coarse_apply(const int dims[4], const int block[4], int nv, const void *
   int rc = make_cg(dims, block, nv, cg);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
-  const double2 *Cp = (const double2 *)C_dev, *xp = (const double2 *)xc_dev;
+  const CT *Cp = (const CT *)C_dev;
+  const double2 *xp = (const double2 *)xc_dev;
   double2 *yp = (double2 *)yc_dev;
   const int64_t stride = cg.nb * cg.nc;
   int r = 0;
   while (r < n_rhs) {
     const int left = n_rhs - r;
     const int nr = left >= 4 ? 4 : (left >= 2 ? 2 : 1);
-    rc = nr == 4 ? launch_coarse_apply<4>(cg, Cp, xp + r * stride, yp + r * stride, st)
-                 : (nr == 2 ? launch_coarse_apply<2>(cg, Cp, xp + r * stride, yp + r * stride, st)
-                            : launch_coarse_apply<1>(cg, Cp, xp + r * stride, yp + r * stride, st));
+    rc = nr == 4 ? launch_coarse_apply<4, CT>(cg, Cp, xp + r * stride, yp + r * stride, st)
+                 : (nr == 2 ? launch_coarse_apply<2, CT>(cg, Cp, xp + r * stride, yp + r * stride, st)
+                            : launch_coarse_apply<1, CT>(cg, Cp, xp + r * stride, yp + r * stride, st));
     if (rc) return rc;
     r += nr;
   }
   return MGT_OK;
+}
+}  // namespace mgt
+
+extern "C" {
+
+int mgt_coarse_apply(const int dims[4], const int block[4], int nv, const void *C_dev, const void *xc_dev,
+                     void *yc_dev, int n_rhs, void *stream) {
+  return coarse_apply_impl<double2>(dims, block, nv, C_dev, xc_dev, yc_dev, n_rhs, stream);
+}
+
+int mgt_coarse_apply_c32(const int dims[4], const int block[4], int nv, const void *C32_dev, const void *xc_dev,
+                         void *yc_dev, int n_rhs, void *stream) {
+  return coarse_apply_impl<float2>(dims, block, nv, C32_dev, xc_dev, yc_dev, n_rhs, stream);
 }
 
 }  // extern "C"

@@ -56,9 +56,14 @@ def generate_gauge(geometry, kind="su3", eps=0.2, seed=0, chunk_sites=1 << 20):
         raise ValueError(f"unknown gauge kind {kind!r}")
     links = torch.empty((V, 4, 3, 3), dtype=torch.complex128, device=dev)
     rng = np.random.default_rng(seed)
+    # standard_normal into a pinned buffer: the same stream and values as
+    # rng.normal(size=(n, 4, 8)) (loc 0, scale 1), without temporaries
+    buf = torch.empty(min(chunk_sites, V) * 32, dtype=torch.float64).pin_memory()
     for s0 in range(0, V, chunk_sites):
         n = min(chunk_sites, V - s0)
-        normals = torch.from_numpy(rng.normal(size=(n, 4, 8))).to(dev)
+        hb = buf[:n * 32]
+        rng.standard_normal(out=hb.numpy())
+        normals = hb.to(dev, non_blocking=True)
         _lib.check(_lib.lib().mgt_su3_expm(float(eps), ptr(normals), s0, n, ptr(links), stream_ptr()),
                    "generate_gauge")
         torch.cuda.current_stream().synchronize()

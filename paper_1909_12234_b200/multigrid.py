@@ -105,10 +105,18 @@ def generate_null_vectors(op, n, tol=1e-2, max_iter=200, seed=0):
     vecs = op.new_field(n)
     ratios = np.empty(n)
     degenerate = np.zeros(n, dtype=bool)
+    # the start y0 = normal(N) + 1j normal(N) of the reference, drawn with
+    # standard_normal into pinned buffers (the same stream and values as
+    # rng.normal: loc 0, scale 1) and combined on the device
+    re_h = torch.empty(N, dtype=torch.float64).pin_memory()
+    im_h = torch.empty(N, dtype=torch.float64).pin_memory()
     for i in range(n):
         for attempt in range(3):
-            y0h = rng.normal(size=N) + 1j * rng.normal(size=N)
-            y0 = op.to_native(torch.from_numpy(y0h).to(device()))
+            rng.standard_normal(out=re_h.numpy())
+            rng.standard_normal(out=im_h.numpy())
+            y0 = op.to_native(torch.complex(re_h.to(device(), non_blocking=True),
+                                            im_h.to(device(), non_blocking=True)))
+            torch.cuda.current_stream().synchronize()  # the pinned buffers are refilled next
             b = -op.apply_native(y0)
             d, its, conv, why, _ = gcr_relax(op, b, tol, max_iter, max_iter)
             y = y0 + d
@@ -419,11 +427,19 @@ class CoarseOperator:
     def shape(self):
         return (self.dim, self.dim)
 
-    def apply_native(self, xc, out=None):
+    def apply_native(self, xc, out=None, low=False):
+        """C xc for native coarse fields (n, nb, 2nv); low=True reads the
+        fp32 copy of C (loose inner solves only)."""
         pr = self.prolongator
         xc = xc.contiguous()
         out = torch.empty_like(xc) if out is None else out
         d, b = pr._dims()
+        if low:
+            if getattr(self, "_c32", None) is None:
+                self._c32 = self.C.to(torch.complex64)
+            _lib.check(_lib.lib().mgt_coarse_apply_c32(d, b, pr.nv, ptr(self._c32), ptr(xc), ptr(out), xc.shape[0],
+                                                        stream_ptr()), "coarse apply (fp32 C)")
+            return out
         _lib.check(_lib.lib().mgt_coarse_apply(d, b, pr.nv, ptr(self.C), ptr(xc), ptr(out), xc.shape[0],
                                                 stream_ptr()), "coarse apply")
         return out
@@ -481,6 +497,9 @@ def coarse_gamma5(x, nv):
     return y
 
 
+LOW_PRECISION_TOL = 1e-5  # coarse solves at least this loose iterate with fp32 C
+
+
 def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
     """BiCGStab on the coarse operator (C + i tau g5_c) for native coarse
     fields b (n, nb, 2nv), every rhs with its own scalars; zero start,
@@ -489,9 +508,12 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
     batched device tensor ops (coarse vectors are Nc = 48 x aggregates long).
     Returns (x, [(iterations, relres, converged, matvecs)])."""
     nv = coarse.prolongator.nv
+    # loose solves (the coarse Davidson's inner tol 1e-3) iterate with the
+    # fp32 copy of C; the explicit-residual confirmation below uses fp64 C
+    low = tol >= LOW_PRECISION_TOL
 
-    def A(v):
-        y = coarse.apply_native(v)
+    def A(v, exact=False):
+        y = coarse.apply_native(v, low=low and not exact)
         if tau != 0.0:
             y = y + 1j * tau * coarse_gamma5(v, nv)
         return y
@@ -536,7 +558,7 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
         conv = ((r2 <= tol2) | (omega.abs() == 0) | (rho.abs() == 0)).cpu().numpy() & act
         if conv.any():
             # confirm on the explicit residual; restart the ones that drifted
-            rt = b - A(x)
+            rt = b - A(x, exact=True)
             mv[act] += 1
             rt2 = dot(rt, rt).real.cpu().numpy()
             ok = conv & (rt2 <= tol2.cpu().numpy())
@@ -549,7 +571,7 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
                 p = torch.where(ag[:, None, None], rt, p)
                 rho = torch.where(ag, dot(rt, rt), rho)
             active = torch.as_tensor(~done, device=b.device)
-    rt = b - A(x)
+    rt = b - A(x, exact=True)
     rel = (dot(rt, rt).real / torch.where(b2 > 0, b2, 1)).sqrt().cpu().numpy()
     reps = [(int(its[i]), float(rel[i]), bool(rel[i] <= tol or float(b2[i]) == 0.0), int(mv[i] + 1))
             for i in range(n)]
