@@ -474,7 +474,7 @@ def probes_config3(M, rank, world, dims=(16, 16, 16, 16), s=128, tol=1e-8, nv=24
             "mean_iterations": inv.total_iterations / max(1, inv.n_solves), "solver": _solver_desc(geo.site_count)}
 
 
-def probes_config4(M, rank, world, dims=(16, 16, 16, 16), s=128, k=64, tol=1e-8):
+def probes_config4(M, rank, world, dims=(16, 16, 16, 16), s=128, k=64, tol=1e-8, block=8):
     """BASELINE configs[3]: 64 smallest-|lambda| eigenpairs of A gamma5 from
     the inexact Davidson (inner GPU solves at 1e-3; outer tol 1e-3 because the
     reference's lock test cannot go below the inner tolerance, SURVEY finding
@@ -484,7 +484,7 @@ def probes_config4(M, rank, world, dims=(16, 16, 16, 16), s=128, k=64, tol=1e-8)
     from paper_1909_12234_b200 import trace as TR
     geo = M.LatticeGeometry(dims, "antiperiodic")
     op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.2, seed=0), 0.1)
-    conf = E.EigenConfig(k=k, tol=1e-3, inner=M.SolveConfig(tol=1e-3))
+    conf = E.EigenConfig(k=k, tol=1e-3, inner=M.SolveConfig(tol=1e-3), block=block)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = E.inexact_eigensolve(op, op.gamma5_diag, conf, E.shift_inverter_factory(op, conf.inner))
@@ -492,8 +492,8 @@ def probes_config4(M, rank, world, dims=(16, 16, 16, 16), s=128, k=64, tol=1e-8)
     setup = _max_over_ranks(time.perf_counter() - t0, world)
     inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
     est, el = _sharded_estimate(M, lambda p: TR.deflate_orthogonal(inv, res.vectors, p), geo, s, 200, rank, world)
-    return {"config": "16^4 eps=0.2 m0=0.1, k=64 inexact Davidson (inner 1e-3, outer 1e-3), orthogonal "
-                      "deflation, s=128 rademacher tol=1e-8 (BASELINE configs[3])",
+    return {"config": f"16^4 eps=0.2 m0=0.1, k=64 inexact Davidson (block {block}, inner 1e-3, outer 1e-3), "
+                      "orthogonal deflation, s=128 rademacher tol=1e-8 (BASELINE configs[3])",
             "value": s / el, "unit": "probes/s", "seconds": el, "setup_seconds": setup,
             "value_including_setup": s / (el + setup), "eigen_inversions": int(res.inversions),
             "eigen_converged": int(np.sum(res.converged)),

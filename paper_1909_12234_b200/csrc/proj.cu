@@ -7,8 +7,11 @@
 // partial in a fixed order and a final kernel sums the partials in block
 // order, so results are bitwise reproducible.
 //  * s <= 8 ("GEMV-like", HBM-bound on V): thread per element, each warp
-//    owns 8 vectors, a block 64; X comes from L1 to the 8 warps.
-//  * s > 8  ("GEMM-like", FP64-bound): 64x64 output tiles staged through
+//    owns 2-8 vectors, a block 8 warps; X comes from L1 to the 8 warps.
+//  * k <= 8 < s (a few vectors against many, e.g. a Davidson block against
+//    the search space): the same kernel with the roles swapped, H = (X^H V)^H
+//    conjugate-transposed by the final reduction.
+//  * k, s > 8  ("GEMM-like", FP64-bound): 64x64 output tiles staged through
 //    shared memory with 4x4 complex register micro-tiles.
 #include <algorithm>
 
@@ -21,12 +24,13 @@ namespace mgt {
 // so the loads in flight per SM) up.
 template <int S>
 constexpr int warp_vecs() {
-  return S <= 2 ? 8 : 4;
+  return S <= 2 ? 8 : (S <= 4 ? 4 : 2);
 }
 
+// S: compile-time column capacity, s <= S the actual column count
 template <int S>
 __global__ void __launch_bounds__(256) vhx_small_kernel(const double2 *__restrict__ V, const double2 *__restrict__ X,
-                                                        int64_t len, int k, double2 *__restrict__ part) {
+                                                        int64_t len, int k, int s, double2 *__restrict__ part) {
   constexpr int kWarpVecs = warp_vecs<S>();
   constexpr int kBlockVecs = 8 * kWarpVecs;
   __shared__ double2 red[8][kWarpVecs * S];
@@ -40,7 +44,7 @@ __global__ void __launch_bounds__(256) vhx_small_kernel(const double2 *__restric
   for (int64_t e = blockIdx.x * 32 + lane; e < len; e += (int64_t)gridDim.x * 32) {
     C<double> xv[S];
 #pragma unroll
-    for (int j = 0; j < S; ++j) xv[j] = ldc(X + (int64_t)j * len + e);
+    for (int j = 0; j < S; ++j) xv[j] = j < s ? ldc(X + (int64_t)j * len + e) : C<double>(0.0, 0.0);
 #pragma unroll
     for (int a = 0; a < kWarpVecs; ++a) {
       if (i0 + a < k) {
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(256) vhx_small_kernel(const double2 *__restric
   __syncwarp();
   for (int q = lane; q < kWarpVecs * S; q += 32) {
     const int a = q / S, j = q % S;
-    if (i0 + a < k) part[((int64_t)blockIdx.x * k + (i0 + a)) * S + j] = red[warp][q];
+    if (i0 + a < k && j < s) part[((int64_t)blockIdx.x * k + (i0 + a)) * s + j] = red[warp][q];
   }
 }
 
@@ -117,8 +121,10 @@ __global__ void __launch_bounds__(256) vhx_tile_kernel(const double2 *__restrict
 
 // H[j*k + i] (column major k x s) = sum over blocks of part[b][i][j]
 // one warp per output: lanes stride over the block partials, then a fixed
-// shuffle tree (deterministic)
-__global__ void vhx_reduce_kernel(const double2 *__restrict__ part, int nblk, int k, int s, double2 *__restrict__ H) {
+// shuffle tree (deterministic).  swapped: part holds (X^H V) as [b][j][i]
+// (k = its column count), so H[q] = conj(sum part[b][q]).
+__global__ void vhx_reduce_kernel(const double2 *__restrict__ part, int nblk, int k, int s, double2 *__restrict__ H,
+                                  int swapped) {
   const int64_t n = (int64_t)k * s;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -131,7 +137,12 @@ __global__ void vhx_reduce_kernel(const double2 *__restrict__ part, int nblk, in
       t.re += __shfl_xor_sync(0xffffffffu, t.re, off);
       t.im += __shfl_xor_sync(0xffffffffu, t.im, off);
     }
-    if (lane == 0) H[(int64_t)j * k + i] = make_double2(t.re, t.im);
+    if (lane == 0) {
+      if (swapped)
+        H[q] = make_double2(t.re, -t.im);
+      else
+        H[(int64_t)j * k + i] = make_double2(t.re, t.im);
+    }
   }
 }
 
@@ -178,19 +189,27 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
   const double2 *V = (const double2 *)V_dev, *X = (const double2 *)X_dev;
   int nblk;
   double2 *part = nullptr;
-  if (s <= 4) {
-    const int bv = 8 * (s <= 2 ? warp_vecs<1>() : warp_vecs<4>());
-    const int gy = (k + bv - 1) / bv;
+  // few columns (or, swapped, few vectors): the GEMV-like kernel
+  const bool swapped = s > 8 && k <= 8;
+  if (s <= 8 || swapped) {
+    const double2 *Vv = swapped ? X : V, *Xv = swapped ? V : X;
+    const int kk = swapped ? s : k, ss = swapped ? k : s;
+    const int bv = 8 * (ss <= 2 ? warp_vecs<1>() : (ss <= 4 ? warp_vecs<4>() : warp_vecs<8>()));
+    const int gy = (kk + bv - 1) / bv;
     nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, (int64_t)kNumSMs * 6 / gy + 1));
     MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy);
-#define MGT_VHX(SS) vhx_small_kernel<SS><<<grid, 256, 0, st>>>(V, X, len, k, part)
-    switch (s) {
-      case 1: MGT_VHX(1); break;
-      case 2: MGT_VHX(2); break;
-      case 3: MGT_VHX(3); break;
-      default: MGT_VHX(4); break;
-    }
+#define MGT_VHX(SS) vhx_small_kernel<SS><<<grid, 256, 0, st>>>(Vv, Xv, len, kk, ss, part)
+    if (ss == 1)
+      MGT_VHX(1);
+    else if (ss == 2)
+      MGT_VHX(2);
+    else if (ss == 3)
+      MGT_VHX(3);
+    else if (ss == 4)
+      MGT_VHX(4);
+    else
+      MGT_VHX(8);
 #undef MGT_VHX
     MGT_LAUNCH_CHECK("vhx_small_kernel");
   } else {
@@ -201,7 +220,9 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
     vhx_tile_kernel<<<grid, 256, 0, st>>>(V, X, len, k, s, part);
     MGT_LAUNCH_CHECK("vhx_tile_kernel");
   }
-  vhx_reduce_kernel<<<grid_for((int64_t)k * s * 32, 128, 8), 128, 0, st>>>(part, nblk, k, s, (double2 *)H_dev);
+  // the reduction reads part as [blk][rows][cols]: swapped, rows = s and cols = k
+  vhx_reduce_kernel<<<grid_for((int64_t)k * s * 32, 128, 8), 128, 0, st>>>(
+      part, nblk, swapped ? s : k, swapped ? k : s, (double2 *)H_dev, swapped ? 1 : 0);
   MGT_LAUNCH_CHECK("vhx_reduce_kernel");
   MGT_CUDA(cudaFreeAsync(part, st));
   return MGT_OK;
