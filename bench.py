@@ -521,7 +521,7 @@ def probes_config5(M, rank, world, dims=(32, 32, 32, 64), s=512, tol=1e-8, nv=24
     coarse = MG.build_coarse_operator(op, pro)
     torch.cuda.synchronize()
     t_mg = time.perf_counter() - t0
-    trip, cres = TR.coarse_deflation_triplets(coarse, r, tol=1e-3, inner_tol=1e-3)
+    trip, cres = TR.coarse_deflation_triplets(coarse, r, tol=1e-3, inner_tol=1e-3, block=8)
     torch.cuda.synchronize()
     setup = _max_over_ranks(time.perf_counter() - t0, world)
     inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
@@ -529,7 +529,7 @@ def probes_config5(M, rank, world, dims=(32, 32, 32, 64), s=512, tol=1e-8, nv=24
         M, lambda p: TR.deflate_oblique_coarse(op, inv, pro, trip, r, p, coarse_op=coarse), geo, s, 300, rank,
         world, reps=1)
     return {"config": f"32^3x64 eps=0.3 m0=0.05, 4^4 aggregates, nv=24 GCR(8) null vectors (Nc={pro.coarse_dim}), "
-                      f"Algorithm 2 at rank {r} (coarse Davidson tol 1e-3), s={s} rademacher tol=1e-8, 4 rhs/solve "
+                      f"Algorithm 2 at rank {r} (coarse block-8 Davidson tol 1e-3), s={s} rademacher tol=1e-8, 4 rhs/solve "
                       "(BASELINE configs[4])",
             "value": s / el, "unit": "probes/s", "seconds": el, "setup_seconds": setup,
             "setup_multigrid_seconds": t_mg, "coarse_eigen_inversions": int(cres.inversions),

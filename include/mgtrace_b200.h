@@ -51,6 +51,12 @@ extern "C" {
 /* mgt_bicgstab_solve only: solve the full system instead of the even-odd
  * Schur complement (the default whenever every extent is even). */
 #define MGT_SOLVE_FULL 16
+/* mgt_bicgstab_solve only: mixed-precision even-odd solve -- defect
+ * correction with fp32 inner BiCGStab cycles (fp64 reductions and scalars)
+ * and the fp64 explicit residual b - A x as the stopping test (the same
+ * contract ||b - A x|| <= tol ||b||).  Ignored when the full system is
+ * solved. */
+#define MGT_SOLVE_MIXED 32
 
 typedef struct mgt_wilson_s *mgt_wilson_t;
 

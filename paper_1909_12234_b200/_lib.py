@@ -23,6 +23,7 @@ G5_OUT = 2
 DAGGER = 4
 HALO_PEER = 8
 SOLVE_FULL = 16
+SOLVE_MIXED = 32
 IPC_HANDLE_BYTES = 64
 
 _lock = threading.Lock()

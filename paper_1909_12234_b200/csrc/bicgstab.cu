@@ -39,9 +39,13 @@ struct BiState {
 };
 
 // Workspace: fields of NR rhs each (native layout) + reduction scratch.
-struct BiWS {
-  double2 *r, *rhat, *p, *v, *s, *t, *x, *b;
-  double2 *be, *bo, *tmp;    // even-odd solve: b_e, b_o, odd-parity scratch
+// R: the field precision (double; float for the inner solves of the mixed-
+// precision solver).  Scalars, reductions and states are always double.
+template <typename R>
+struct BiWST {
+  using F = cplx<R>;
+  F *r, *rhat, *p, *v, *s, *t, *x, *b;
+  F *be, *bo, *tmp;    // even-odd solve: b_e, b_o, odd-parity scratch
   double *partials;
   unsigned *ticket;
   unsigned long long *ctr;   // dynamic chunk counter (dslash kernels), reset by their last block
@@ -51,11 +55,11 @@ struct BiWS {
   // batched solves: group g of kMaxGroup rhs (blockIdx.y) owns field slice
   // g*gfield, partials g*gpart, ticket area g*256 B and states g*kMaxGroup
   int64_t gfield, gpart;
-  __host__ __device__ __forceinline__ BiWS at(int g) const {
-    BiWS o = *this;
+  __host__ __device__ __forceinline__ BiWST at(int g) const {
+    BiWST o = *this;
     const int64_t f = (int64_t)g * gfield;
-    double2 *BiWS::*fs[11] = {&BiWS::r, &BiWS::rhat, &BiWS::p, &BiWS::v, &BiWS::s, &BiWS::t,
-                              &BiWS::x, &BiWS::b, &BiWS::be, &BiWS::bo, &BiWS::tmp};
+    F *BiWST::*fs[11] = {&BiWST::r, &BiWST::rhat, &BiWST::p, &BiWST::v, &BiWST::s, &BiWST::t,
+                         &BiWST::x, &BiWST::b, &BiWST::be, &BiWST::bo, &BiWST::tmp};
 #pragma unroll
     for (int i = 0; i < 11; ++i)
       if (o.*fs[i]) o.*fs[i] += f;
@@ -68,7 +72,25 @@ struct BiWS {
     return o;
   }
 };
+using BiWS = BiWST<double>;
 
+// double-precision dot-product pieces of fields of either precision
+template <typename R>
+__device__ __forceinline__ double dre(C<R> a, C<R> b) {  // Re conj(a) b
+  return (double)a.re * (double)b.re + (double)a.im * (double)b.im;
+}
+template <typename R>
+__device__ __forceinline__ double dim(C<R> a, C<R> b) {  // Im conj(a) b
+  return (double)a.re * (double)b.im - (double)a.im * (double)b.re;
+}
+template <typename R>
+__device__ __forceinline__ double dnorm2(C<R> a) {
+  return (double)a.re * (double)a.re + (double)a.im * (double)a.im;
+}
+template <typename R>
+__device__ __forceinline__ C<R> cvt(C<double> a) {
+  return C<R>((R)a.re, (R)a.im);
+}
 template <int NR>
 __device__ __forceinline__ bool any_status(const BiState *st, int want) {
   bool any = false;
@@ -98,16 +120,16 @@ __device__ __forceinline__ bool cfinite(C<double> a) { return isfinite(a.re) && 
 
 // Last-block scalar recurrences of the stencil kernels (shared by the full
 // and the even-odd kernels).  They also reset the chunk counters.
-template <int M>
-__device__ __forceinline__ void store_red(const BiWS &w, const double (&out)[M]) {
+template <int M, class W>
+__device__ __forceinline__ void store_red(const W &w, const double (&out)[M]) {
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j < M; ++j) w.red[j] = out[j];
   }
 }
 
-template <int NR>
-__device__ __forceinline__ void k1_logic(const BiWS &w, const double (&out)[NR * 2]) {
+template <int NR, class W>
+__device__ __forceinline__ void k1_logic(const W &w, const double (&out)[NR * 2]) {
   const int r = threadIdx.x;
   if (r < NR && w.st[r].status == ST_RUN) {
     BiState &s = w.st[r];
@@ -122,8 +144,8 @@ __device__ __forceinline__ void k1_logic(const BiWS &w, const double (&out)[NR *
   }
 }
 
-template <int NR, int DIST = 0>
-__device__ __forceinline__ void k1_finish(const BiWS &w, int64_t nchunks) {
+template <int NR, int DIST = 0, class W>
+__device__ __forceinline__ void k1_finish(const W &w, int64_t nchunks) {
   double out[NR * 2];
   reduce_finish_n<NR * 2>(w.partials, nchunks, w.ticket, out);
   if (threadIdx.x == 0) {
@@ -136,8 +158,8 @@ __device__ __forceinline__ void k1_finish(const BiWS &w, int64_t nchunks) {
     k1_logic<NR>(w, out);
 }
 
-template <int NR>
-__device__ __forceinline__ void k3_logic(const BiWS &w, const double (&out)[NR * 3]) {
+template <int NR, class W>
+__device__ __forceinline__ void k3_logic(const W &w, const double (&out)[NR * 3]) {
   const int r = threadIdx.x;
   if (r < NR && w.st[r].status == ST_RUN) {
     BiState &s = w.st[r];
@@ -155,8 +177,8 @@ __device__ __forceinline__ void k3_logic(const BiWS &w, const double (&out)[NR *
   }
 }
 
-template <int NR, int DIST = 0>
-__device__ __forceinline__ void k3_finish(const BiWS &w, int64_t nchunks) {
+template <int NR, int DIST = 0, class W>
+__device__ __forceinline__ void k3_finish(const W &w, int64_t nchunks) {
   double out[NR * 3];
   reduce_finish_n<NR * 3>(w.partials, nchunks, w.ticket, out);
   if (threadIdx.x == 0) {
@@ -169,8 +191,8 @@ __device__ __forceinline__ void k3_finish(const BiWS &w, int64_t nchunks) {
     k3_logic<NR>(w, out);
 }
 
-template <int NR>
-__device__ __forceinline__ void resid_logic(const BiWS &w, const double (&out)[NR]) {
+template <int NR, class W>
+__device__ __forceinline__ void resid_logic(const W &w, const double (&out)[NR]) {
   const int r = threadIdx.x;
   if (r < NR) {
     BiState &s = w.st[r];
@@ -191,8 +213,8 @@ __device__ __forceinline__ void resid_logic(const BiWS &w, const double (&out)[N
   }
 }
 
-template <int NR, int DIST = 0>
-__device__ __forceinline__ void resid_finish(const BiWS &w, int64_t nchunks) {
+template <int NR, int DIST = 0, class W>
+__device__ __forceinline__ void resid_finish(const W &w, int64_t nchunks) {
   double out[NR];
   reduce_finish_n<NR>(w.partials, nchunks, w.ticket, out);
   if (threadIdx.x == 0) {
@@ -212,8 +234,8 @@ __device__ __forceinline__ bool resid_active(int st) {
 
 // ---------------------------------------------------------------------------
 // init: b -> workspace, r = rhat = p = b, x = 0, |b|^2
-template <int NR>
-__device__ __forceinline__ void init_logic(const BiWS &w, const double (&out)[NR], double tol, int maxit,
+template <int NR, class W>
+__device__ __forceinline__ void init_logic(const W &w, const double (&out)[NR], double tol, int maxit,
                                            int use_bfull) {
   const int r = threadIdx.x;
   if (r < NR) {
@@ -303,8 +325,8 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<
   if (last_block(w.ticket)) k1_finish<NR, DIST>(w, nchunks);
 }
 
-template <int NR>
-__device__ __forceinline__ void k2_logic(const BiWS &w, const double (&out)[NR]) {
+template <int NR, class W>
+__device__ __forceinline__ void k2_logic(const W &w, const double (&out)[NR]) {
   const int r = threadIdx.x;
   if (r < NR && w.st[r].status == ST_RUN) {
     BiState &s = w.st[r];
@@ -314,13 +336,13 @@ __device__ __forceinline__ void k2_logic(const BiWS &w, const double (&out)[NR])
 }
 
 // K2: s = r - alpha v ; |s|^2
-template <int NR, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w_) {
-  const BiWS w = w_.at(blockIdx.y);
+template <int NR, int DIST = 0, typename R = double>
+__global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWST<R> w_) {
+  const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
-  const C<double> al = w.st[m.rhs].alpha;
+  const C<R> al = cvt<R>(w.st[m.rhs].alpha);
   double acc[1] = {0.0};
   if (run_me) {
     MGT_SITE_LOOP(m, V) {
@@ -328,9 +350,9 @@ __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWS w_) {
 #pragma unroll
       for (int c = 0; c < 12; ++c) {
         const int64_t q = base + (int64_t)c * V;
-        C<double> ss = ldc(w.r + q) - al * ldc(w.v + q);
+        C<R> ss = ldc(w.r + q) - al * ldc(w.v + q);
         stc(w.s + q, ss);
-        acc[0] += cabs2(ss);
+        acc[0] += dnorm2(ss);
       }
     }
   }
@@ -376,8 +398,8 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<
   if (last_block(w.ticket)) k3_finish<NR, DIST>(w, nchunks);
 }
 
-template <int NR>
-__device__ __forceinline__ void k4_logic(const BiWS &w, const double (&out)[NR * 3]) {
+template <int NR, class W>
+__device__ __forceinline__ void k4_logic(const W &w, const double (&out)[NR * 3]) {
   const int r = threadIdx.x;
   if (r < NR && w.st[r].status == ST_RUN) {
     BiState &s = w.st[r];
@@ -401,13 +423,13 @@ __device__ __forceinline__ void k4_logic(const BiWS &w, const double (&out)[NR *
 }
 
 // K4: x += alpha p + omega s ; r = s - omega t ; rho' = (rhat, r), |r|^2
-template <int NR, int DIST = 0>
-__global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w_) {
-  const BiWS w = w_.at(blockIdx.y);
+template <int NR, int DIST = 0, typename R = double>
+__global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWST<R> w_) {
+  const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
-  const C<double> al = w.st[m.rhs].alpha, om = w.st[m.rhs].omega;
+  const C<R> al = cvt<R>(w.st[m.rhs].alpha), om = cvt<R>(w.st[m.rhs].omega);
   double acc[3] = {0.0, 0.0, 0.0};
   if (run_me) {
     MGT_SITE_LOOP(m, V) {
@@ -415,14 +437,14 @@ __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w_) {
 #pragma unroll
       for (int c = 0; c < 12; ++c) {
         const int64_t q = base + (int64_t)c * V;
-        C<double> xx = ldc(w.x + q), pp = ldc(w.p + q), ss = ldc(w.s + q), tt = ldc(w.t + q), rh = ldc(w.rhat + q);
+        C<R> xx = ldc(w.x + q), pp = ldc(w.p + q), ss = ldc(w.s + q), tt = ldc(w.t + q), rh = ldc(w.rhat + q);
         xx = xx + al * pp + om * ss;
-        C<double> rr = ss - om * tt;
+        C<R> rr = ss - om * tt;
         stc(w.x + q, xx);
         stc(w.r + q, rr);
-        acc[0] += rh.re * rr.re + rh.im * rr.im;
-        acc[1] += rh.re * rr.im - rh.im * rr.re;
-        acc[2] += cabs2(rr);
+        acc[0] += dre(rh, rr);
+        acc[1] += dim(rh, rr);
+        acc[2] += dnorm2(rr);
       }
     }
   }
@@ -437,13 +459,13 @@ __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWS w_) {
 }
 
 // K5: p = r + beta (p - omega v)
-template <int NR>
-__global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWS w_) {
-  const BiWS w = w_.at(blockIdx.y);
+template <int NR, typename R = double>
+__global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWST<R> w_) {
+  const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   if (w.st[m.rhs].status != ST_RUN) return;
-  const C<double> be = w.st[m.rhs].beta, om = w.st[m.rhs].omega;
+  const C<R> be = cvt<R>(w.st[m.rhs].beta), om = cvt<R>(w.st[m.rhs].omega);
   MGT_SITE_LOOP(m, V) {
     const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
@@ -492,8 +514,8 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
   if (last_block(w.ticket)) resid_finish<NR, DIST>(w, nchunks);
 }
 
-template <int NR>
-__device__ __forceinline__ void restart_logic(const BiWS &w, const double (&out)[NR]) {
+template <int NR, class W>
+__device__ __forceinline__ void restart_logic(const W &w, const double (&out)[NR]) {
   const int r = threadIdx.x;
   if (r < NR && w.st[r].status == ST_RESTART) {
     BiState &s = w.st[r];
@@ -627,11 +649,11 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_rhs(BiEo X, LinkField<doub
 
 // first half of S: tmp = Dg^-1 H_oe (G_in f), f = p / s / x (mode 0: rhs
 // still iterating, mode 1: rhs whose true residual is due)
-template <int NR, int RECON>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<double, RECON> le,
-                                                            LinkField<double, RECON> lo, const double2 *f, BiWS w_,
+template <int NR, int RECON, typename R = double>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<R, RECON> le,
+                                                            LinkField<R, RECON> lo, const cplx<R> *f, BiWST<R> w_,
                                                             int mode) {
-  const BiWS w = w_.at(blockIdx.y);
+  const BiWST<R> w = w_.at(blockIdx.y);
   f += (int64_t)blockIdx.y * w_.gfield;
   bool any = false;
 #pragma unroll
@@ -646,8 +668,8 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<do
   MGT_DYN_LOOP(m, Vh, w.ctr2, nchunks) {
     if (act && o < Vh) {
       const int64_t c = sched_site(X.sh, o);
-      C<double> y[4][3], cc[4][3];
-      eo_eval<double, RECON>(X.E, 1, X.R.first, f + off, nullptr, lo, le, c, y, cc);
+      C<R> y[4][3], cc[4][3];
+      eo_eval<R, RECON>(X.E, 1, X.R.first, f + off, nullptr, lo, le, c, y, cc);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -657,10 +679,10 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<do
 }
 
 // K1 (eo): v = S p = G_out [ Dg G_in p - 1/4 H_eo tmp ] ; sigma = (rhat, v)
-template <int NR, int RECON>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<double, RECON> le,
-                                                         LinkField<double, RECON> lo, BiWS w_) {
-  const BiWS w = w_.at(blockIdx.y);
+template <int NR, int RECON, typename R = double>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<R, RECON> le,
+                                                         LinkField<R, RECON> lo, BiWST<R> w_) {
+  const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
@@ -671,17 +693,17 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<doubl
     double acc[2] = {0.0, 0.0};
     if (run_me && o < Vh) {
       const int64_t c = sched_site(X.sh, o);
-      C<double> y[4][3], cc[4][3];
-      eo_eval<double, RECON>(X.E, 0, X.R.second, w.tmp + off, w.p + off, le, lo, c, y, cc);
+      C<R> y[4][3], cc[4][3];
+      eo_eval<R, RECON>(X.E, 0, X.R.second, w.tmp + off, w.p + off, le, lo, c, y, cc);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           const int64_t q = off + (int64_t)(a * 3 + k) * Vh + c;
           stc(w.v + q, y[a][k]);
-          C<double> rh = ldc(w.rhat + q);
-          acc[0] += rh.re * y[a][k].re + rh.im * y[a][k].im;
-          acc[1] += rh.re * y[a][k].im - rh.im * y[a][k].re;
+          C<R> rh = ldc(w.rhat + q);
+          acc[0] += dre(rh, y[a][k]);
+          acc[1] += dim(rh, y[a][k]);
         }
     }
     chunk_publish<NR, 2>(acc, w.partials + chunk * NR * 2);
@@ -690,10 +712,10 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<doubl
 }
 
 // K3 (eo): t = S s ; (t, s), |t|^2
-template <int NR, int RECON>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_k3_eo(BiEo X, LinkField<double, RECON> le,
-                                                         LinkField<double, RECON> lo, BiWS w_) {
-  const BiWS w = w_.at(blockIdx.y);
+template <int NR, int RECON, typename R = double>
+__global__ void __launch_bounds__(kRedBlock, 3) bi_k3_eo(BiEo X, LinkField<R, RECON> le,
+                                                         LinkField<R, RECON> lo, BiWST<R> w_) {
+  const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
@@ -704,17 +726,17 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3_eo(BiEo X, LinkField<doubl
     double acc[3] = {0.0, 0.0, 0.0};
     if (run_me && o < Vh) {
       const int64_t c = sched_site(X.sh, o);
-      C<double> y[4][3], cc[4][3];
-      eo_eval<double, RECON>(X.E, 0, X.R.second, w.tmp + off, w.s + off, le, lo, c, y, cc);
+      C<R> y[4][3], cc[4][3];
+      eo_eval<R, RECON>(X.E, 0, X.R.second, w.tmp + off, w.s + off, le, lo, c, y, cc);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           stc(w.t + off + (int64_t)(a * 3 + k) * Vh + c, y[a][k]);
-          const C<double> tt = y[a][k], ss = cc[a][k];
-          acc[0] += tt.re * ss.re + tt.im * ss.im;
-          acc[1] += tt.re * ss.im - tt.im * ss.re;
-          acc[2] += cabs2(tt);
+          const C<R> tt = y[a][k], ss = cc[a][k];
+          acc[0] += dre(tt, ss);
+          acc[1] += dim(tt, ss);
+          acc[2] += dnorm2(tt);
         }
     }
     chunk_publish<NR, 3>(acc, w.partials + chunk * NR * 3);
@@ -831,6 +853,40 @@ static WSLayout ws_layout(int64_t V, int groups = 1) {
   return L;
 }
 
+// fp32 inner workspace of the mixed-precision solve (even-odd fields r,
+// rhat, p, v, s, t, x, tmp; own partials, tickets and states), placed after
+// the fp64 workspace
+static size_t ws32_bytes(const WSLayout &L) {
+  const size_t f32 = align_up((size_t)L.groups * kMaxGroup * 12 * (L.V / 2) * sizeof(float2), 512);
+  return 8 * f32 + L.partials + 256 * (size_t)L.groups + align_up((size_t)L.groups * kMaxGroup * sizeof(BiState), 256);
+}
+
+static BiWST<float> carve32(char *q, const WSLayout &Lw) {
+  BiWST<float> w;
+  const size_t f32 = align_up((size_t)Lw.groups * kMaxGroup * 12 * (Lw.V / 2) * sizeof(float2), 512);
+  float2 **f[8] = {&w.r, &w.rhat, &w.p, &w.v, &w.s, &w.t, &w.x, &w.tmp};
+  for (int i = 0; i < 8; ++i) *f[i] = (float2 *)(q + i * f32);
+  w.b = w.be = w.bo = nullptr;
+  q += 8 * f32;
+  w.partials = (double *)q;
+  q += Lw.partials;
+  w.ticket = (unsigned *)q;
+  w.ctr = (unsigned long long *)(q + 8);
+  w.ctr2 = (unsigned long long *)(q + 16);
+  w.red = (double *)(q + 32);
+  q += 256 * (size_t)Lw.groups;
+  w.st = (BiState *)q;
+  w.gfield = (int64_t)kMaxGroup * 12 * (Lw.V / 2);
+  w.gpart = (int64_t)Lw.gpart;
+  return w;
+}
+
+// total bytes for G groups (mixed: plus the fp32 inner workspace)
+static size_t ws_total(int64_t V, int groups, bool mixed) {
+  const WSLayout L = ws_layout(V, groups);
+  return L.total + (mixed ? ws32_bytes(L) : 0);
+}
+
 static BiWS carve(char *q, const WSLayout &Lw, bool eo = false) {
   BiWS w;
   double2 **f[11] = {&w.r, &w.rhat, &w.p, &w.v, &w.s, &w.t, &w.x, &w.b, &w.be, &w.bo, &w.tmp};
@@ -893,18 +949,18 @@ static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &l
   return MGT_OK;
 }
 
-template <int NR, int RECON>
-static int launch_chunk_eo(const BiEo &X, const LinkField<double, RECON> &le, const LinkField<double, RECON> &lo,
-                           const BiWS &w, dim3 gd, dim3 g1, dim3 grid, cudaStream_t st) {
+template <int NR, int RECON, typename R = double>
+static int launch_chunk_eo(const BiEo &X, const LinkField<R, RECON> &le, const LinkField<R, RECON> &lo,
+                           const BiWST<R> &w, dim3 gd, dim3 g1, dim3 grid, cudaStream_t st) {
   const int64_t Vh = X.E.Vh;
   for (int it = 0; it < kChunk; ++it) {
-    bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
-    bi_k1_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
-    bi_k2<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
-    bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w, 0);
-    bi_k3_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
-    bi_k4<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
-    bi_k5<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    bi_eo_first<NR, RECON, R><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
+    bi_k1_eo<NR, RECON, R><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    bi_k2<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    bi_eo_first<NR, RECON, R><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w, 0);
+    bi_k3_eo<NR, RECON, R><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    bi_k4<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    bi_k5<NR, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
   }
   return MGT_OK;
 }
@@ -1044,6 +1100,240 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
   int rc = fetch();
   if (rc) return rc;
   (void)nst;
+  for (int g = 0; g < G; ++g)
+    for (int r = 0; r < NR; ++r) {
+      const BiState &s = hs[g * kMaxGroup + r];
+      const int i = g * NR + r;
+      const bool zero_rhs = s.b2 == 0.0;
+      const double rel = zero_rhs ? 0.0 : sqrt(s.true_r2 / s.b2);
+      const bool conv = zero_rhs || s.true_r2 <= s.tol2;
+      report[4 * i + 0] = s.iters;
+      report[4 * i + 1] = s.matvecs;
+      report[4 * i + 2] = conv ? 1 : 0;
+      report[4 * i + 3] = conv ? 0 : (s.reason ? s.reason : 1);
+      relres[i] = rel;
+      if (dot_out) {
+        dot_out[2 * i] = s.dotq.re;
+        dot_out[2 * i + 1] = s.dotq.im;
+      }
+    }
+  return MGT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Mixed-precision even-odd solve (defect correction).  The fp64 workspace
+// holds the Schur system (bh_e, x_e and its true residual r); every outer
+// cycle solves S e = r with fp32 fields and links (fp64 reductions and
+// scalar recurrences) to a relative tolerance delta, accumulates x_e += e in
+// fp64 and recomputes r = bh_e - S x_e in fp64: the stopping test is the
+// reference's explicit full residual ||b - A x|| <= tol ||b||
+// (krylov.py:78-85), unchanged.  An fp32 iteration streams half the bytes
+// of an fp64 one.
+
+// inner start: r = rhat = p = (float) r64 for the rhs still running (zero
+// otherwise), x = 0; inner tol2 = max(delta^2 |r|^2, 0.81 tol2_64)
+template <int NR>
+__global__ void __launch_bounds__(kRedBlock) mx_begin(int64_t V, BiWS w64_, BiWST<float> w_, double delta) {
+  const BiWS w64 = w64_.at(blockIdx.y);
+  const BiWST<float> w = w_.at(blockIdx.y);
+  RhsMap<NR> m;
+  const bool act = w64.st[m.rhs].status == ST_RUN;
+  double acc[1] = {0.0};
+  MGT_SITE_LOOP(m, V) {
+    const int64_t base = (int64_t)m.rhs * 12 * V + o;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      const int64_t q = base + (int64_t)c * V;
+      const C<float> bb = act ? cvt<float>(ldc(w64.r + q)) : C<float>(0.f, 0.f);
+      stc(w.r + q, bb);
+      stc(w.rhat + q, bb);
+      stc(w.p + q, bb);
+      stc(w.x + q, C<float>(0.f, 0.f));
+      acc[0] += dnorm2(bb);
+    }
+  }
+  if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
+    double out[NR];
+    reduce_finish<NR>(w.partials, w.ticket, out);
+    const int r = threadIdx.x;
+    if (r < NR) {
+      BiState &s = w.st[r];
+      const BiState &s64 = w64.st[r];
+      const double b2 = out[r];
+      s.b2 = s.r2 = s.s2 = s.true_r2 = b2;
+      s.tol2 = fmax(delta * delta * b2, 0.81 * s64.tol2);
+      s.rho = C<double>(b2, 0.0);
+      s.alpha = s.omega = C<double>(1.0, 0.0);
+      s.beta = s.dotq = C<double>(0.0, 0.0);
+      s.half = 0;
+      s.iters = 0;
+      s.maxit = max(1, s64.maxit - s64.iters);
+      s.matvecs = 0;
+      s.reason = 0;
+      s.status = (s64.status == ST_RUN && b2 > 0.0) ? ST_RUN : ST_DONE;
+    }
+  }
+}
+
+// x_e += (double) e for the rhs whose inner cycle ran; they are marked CONV so
+// the fp64 residual kernels recompute their true residual
+template <int NR>
+__global__ void __launch_bounds__(kRedBlock) mx_accum(int64_t V, BiWS w64_, BiWST<float> w_) {
+  const BiWS w64 = w64_.at(blockIdx.y);
+  const BiWST<float> w = w_.at(blockIdx.y);
+  RhsMap<NR> m;
+  if (w64.st[m.rhs].status == ST_RUN) {
+    MGT_SITE_LOOP(m, V) {
+      const int64_t base = (int64_t)m.rhs * 12 * V + o;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) {
+        const int64_t q = base + (int64_t)c * V;
+        const C<float> e = ldc(w.x + q);
+        const C<double> xx = ldc(w64.x + q);
+        stc(w64.x + q, C<double>(xx.re + (double)e.re, xx.im + (double)e.im));
+      }
+    }
+  }
+  if (last_block(w64.ticket)) {
+    const int r = threadIdx.x;
+    if (r == 0) *w64.ticket = 0u;
+    if (r < NR) {
+      BiState &s = w64.st[r];
+      const BiState &t = w.st[r];
+      if (s.status == ST_RUN) {
+        s.iters += t.iters;
+        s.matvecs += t.matvecs;
+        s.status = ST_CONV;
+      }
+    }
+  }
+}
+
+// rhs whose true residual is still above tol start another cycle unless
+// the last one failed to halve it (stagnation -> reported as breakdown)
+template <int NR>
+__global__ void mx_next(BiWS w_, int cycle, int max_cycles) {
+  const BiWS w = w_.at(blockIdx.y);
+  const int r = threadIdx.x;
+  if (r < NR && w.st[r].status == ST_RESTART) {
+    BiState &s = w.st[r];
+    if (cycle + 1 >= max_cycles || s.true_r2 > 0.25 * s.s2) {
+      s.status = ST_DONE;
+      s.reason = 2;
+    } else {
+      s.s2 = s.true_r2;  // the residual this cycle must improve on
+      s.status = ST_RUN;
+    }
+  }
+}
+
+template <int NR, int RECON>
+static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b,
+                             double2 *x, char *ws, const WSLayout &Lw, double tol, int max_iter, int64_t *report,
+                             double *relres, double *dot_out, int G, cudaStream_t st) {
+  const int64_t V = h->g.V, Vs = V / 2;
+  BiWS w = carve(ws, Lw, true);
+  BiWST<float> w32 = carve32(ws + Lw.total, Lw);
+  BiEo X;
+  X.E = make_eo_geom(h->g, h->antiperiodic);
+  Geom gh = h->g;
+  gh.L[2] /= 2;
+  gh.V /= 2;
+  gh.stride[1] /= 2;
+  gh.stride[0] /= 2;
+  gh.stride[3] /= 2;
+  X.sh = make_sched(gh, 1024, h->slab_bytes);
+  X.R = make_eo_roles(P);
+  LinkField<double, RECON> le{reinterpret_cast<const double2 *>(h->links_cb), Vs};
+  LinkField<double, RECON> lo{reinterpret_cast<const double2 *>((const char *)h->links_cb + h->link_bytes / 2), Vs};
+  LinkField<float, RECON> le32{reinterpret_cast<const float2 *>(h->links_cb32), Vs};
+  LinkField<float, RECON> lo32{reinterpret_cast<const float2 *>((const char *)h->links_cb32 + h->link_bytes / 4), Vs};
+  static int g_str = 0, g_e1 = 0, g_e2 = 0, g_f1 = 0, g_f2 = 0;  // resident grids, per template instance
+  if (!g_str) g_str = resident_grid(bi_k4<NR>, kRedBlock, (int64_t)1 << 40);
+  if (!g_e1) g_e1 = resident_grid(bi_eo_first<NR, RECON>, kRedBlock, (int64_t)1 << 40);
+  if (!g_e2) g_e2 = resident_grid(bi_k1_eo<NR, RECON>, kRedBlock, (int64_t)1 << 40);
+  if (!g_f1) g_f1 = resident_grid(bi_eo_first<NR, RECON, float>, kRedBlock, (int64_t)1 << 40);
+  if (!g_f2) g_f2 = resident_grid(bi_k1_eo<NR, RECON, float>, kRedBlock, (int64_t)1 << 40);
+  const int64_t need = (Vs + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
+  auto per_group = [&](int resident) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, std::max(1, resident / G)));
+  };
+  const dim3 grid(per_group(g_str), G), gd(per_group(g_e2), G), g1(per_group(g_e1), G);
+  const dim3 fd(per_group(g_f2), G), f1(per_group(g_f1), G);
+  MGT_CUDA(cudaMemsetAsync(w.ticket, 0, 256 * (size_t)G, st));
+  MGT_CUDA(cudaMemsetAsync(w32.ticket, 0, 256 * (size_t)G, st));
+  bi_eo_split<NR><<<grid, kRedBlock, 0, st>>>(X, b, w, P.g5out);
+  bi_eo_rhs<NR, RECON><<<grid, kRedBlock, 0, st>>>(X, le, lo, w);
+  bi_init<NR><<<grid, kRedBlock, 0, st>>>(Vs, w.b, w, tol, max_iter, 1);
+  note_launch(3);
+  MGT_LAUNCH_CHECK("bi_init (mixed)");
+
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    GraphKey key{h, ws, NR, RECON, flags, 2, G, tau};
+    auto it = g_graphs.find(key);
+    if (it != g_graphs.end()) {
+      exec = it->second;
+    } else {
+      cudaStream_t cap;
+      MGT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      cudaGraph_t graph;
+      MGT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      launch_chunk_eo<NR, RECON, float>(X, le32, lo32, w32, fd, f1, grid, cap);
+      cudaError_t e = cudaStreamEndCapture(cap, &graph);
+      cudaStreamDestroy(cap);
+      if (e != cudaSuccess) return cuda_fail(e, "mixed bicgstab graph capture");
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return cuda_fail(e, "mixed bicgstab graph instantiate");
+      g_graphs[key] = exec;
+    }
+  }
+  BiState *hs = state_mailbox(G * kMaxGroup);
+  if (!hs) return fail(MGT_ERR_CUDA, "pinned state mailbox");
+  auto fetch = [&](const BiState *dst) -> int {
+    MGT_CUDA(cudaMemcpyAsync(hs, dst, (size_t)G * kMaxGroup * sizeof(BiState), cudaMemcpyDeviceToHost, st));
+    MGT_CUDA(cudaStreamSynchronize(st));
+    return MGT_OK;
+  };
+  auto any_run = [&]() {
+    for (int g = 0; g < G; ++g)
+      for (int r = 0; r < NR; ++r)
+        if (hs[g * kMaxGroup + r].status == ST_RUN) return true;
+    return false;
+  };
+  static double delta = 0.0;
+  if (delta == 0.0) {
+    const char *v = getenv("MGT_MIXED_DELTA");
+    delta = v ? atof(v) : 1e-4;
+  }
+  constexpr int kMaxCycles = 64;
+  int rc = fetch(w.st);
+  if (rc) return rc;
+  for (int cycle = 0; cycle < kMaxCycles && any_run(); ++cycle) {
+    mx_begin<NR><<<grid, kRedBlock, 0, st>>>(Vs, w, w32, delta);
+    MGT_LAUNCH_CHECK("mx_begin");
+    for (int round = 0; round < 1000000; ++round) {
+      MGT_CUDA(cudaGraphLaunch(exec, st));
+      note_launch(7 * kChunk);
+      rc = fetch(w32.st);
+      if (rc) return rc;
+      if (!any_run()) break;
+    }
+    mx_accum<NR><<<grid, kRedBlock, 0, st>>>(Vs, w, w32);
+    bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.x, w, 1);
+    bi_resid_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    mx_next<NR><<<dim3(1, G), 32, 0, st>>>(w, cycle, kMaxCycles);
+    note_launch(3);
+    MGT_LAUNCH_CHECK("mixed residual");
+    rc = fetch(w.st);
+    if (rc) return rc;
+  }
+  bi_eo_final<NR, RECON><<<grid, kRedBlock, 0, st>>>(X, le, lo, x, w);
+  MGT_LAUNCH_CHECK("bi_eo_final (mixed)");
+  rc = fetch(w.st);
+  if (rc) return rc;
   for (int g = 0; g < G; ++g)
     for (int r = 0; r < NR; ++r) {
       const BiState &s = hs[g * kMaxGroup + r];
@@ -1216,7 +1506,8 @@ extern "C" {
 
 size_t mgt_bicgstab_workspace_bytes(mgt_wilson_t h, int n_rhs) {
   if (!h) return 0;
-  return ws_layout(h->g.V, std::max(1, n_rhs / kMaxGroup)).total;
+  // room for the fp32 inner fields of a mixed-precision solve as well
+  return ws_total(h->g.V, std::max(1, n_rhs / kMaxGroup), eo_available(h));
 }
 
 static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau,
@@ -1231,9 +1522,10 @@ static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, i
   cudaStream_t st = as_stream(stream);
   // even-odd Schur solve unless disabled (handle / MGT_SOLVE_FULL) or an extent is odd
   const bool eo = h->solve_eo && !(flags & MGT_SOLVE_FULL) && eo_available(h);
-  flags &= ~MGT_SOLVE_FULL;
+  const bool mixed = eo && (flags & MGT_SOLVE_MIXED);
+  flags &= ~(MGT_SOLVE_FULL | MGT_SOLVE_MIXED);
   if (eo) {
-    int rc = eo_prepare(h, st);
+    int rc = mixed ? eo_prepare_mixed(h, st) : eo_prepare(h, st);
     if (rc) return rc;
   }
   WilsonParams P = make_params(h, flags, tau);
@@ -1241,8 +1533,8 @@ static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, i
   // groups of kMaxGroup rhs batched into one launch per kernel, as many as
   // the workspace holds
   int gmax = 1;
-  while (gmax < 64 && ws_layout(V, gmax + 1).total <= workspace_bytes) ++gmax;
-  if (ws_layout(V, 1).total > workspace_bytes) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: workspace too small");
+  while (gmax < 64 && ws_total(V, gmax + 1, mixed) <= workspace_bytes) ++gmax;
+  if (ws_total(V, 1, mixed) > workspace_bytes) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: workspace too small");
   const size_t field = (size_t)12 * V;
   int r0 = 0;
   while (r0 < n_rhs) {
@@ -1257,10 +1549,14 @@ static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, i
     char *ws = (char *)workspace_dev;
     int rc;
 #define MGT_SOLVE(NR, GG)                                                                                       \
-  (h->recon == 18 ? solve_group<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
-                                         relres_out + r0, dot, eo, GG, st)                                       \
-                  : solve_group<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,     \
-                                         relres_out + r0, dot, eo, GG, st))
+  (mixed ? (h->recon == 18 ? solve_group_mixed<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter,          \
+                                                       report_out + 4 * r0, relres_out + r0, dot, GG, st)      \
+                           : solve_group_mixed<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter,          \
+                                                       report_out + 4 * r0, relres_out + r0, dot, GG, st))     \
+   : (h->recon == 18 ? solve_group<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,  \
+                                            relres_out + r0, dot, eo, GG, st)                                    \
+                     : solve_group<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,  \
+                                            relres_out + r0, dot, eo, GG, st)))
     if (nr == 4)
       rc = MGT_SOLVE(4, Gc);
     else if (nr == 2)
@@ -1279,7 +1575,7 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs
                        double *dot_out_host, void *stream) {
   if (!h) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: null argument");
   return bicgstab_solve_impl(h, b_dev, x_dev, n_rhs, flags, tau, tol, max_iter, workspace_dev,
-                             ws_layout(h->g.V, 1).total, report_out, relres_out, dot_out_host, stream);
+                             ws_total(h->g.V, 1, eo_available(h)), report_out, relres_out, dot_out_host, stream);
 }
 
 int mgt_bicgstab_solve_ws(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau,

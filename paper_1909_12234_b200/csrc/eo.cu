@@ -105,6 +105,29 @@ int eo_prepare(mgt_wilson_s *h, cudaStream_t st) {
   return MGT_OK;
 }
 
+__global__ void narrow_kernel(const double2 *__restrict__ in, float2 *__restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = in[i];
+    out[i] = make_float2((float)v.x, (float)v.y);
+  }
+}
+
+int eo_prepare_mixed(mgt_wilson_s *h, cudaStream_t st) {
+  if (h->prec != 64) return fail(MGT_ERR_INVALID, "mixed-precision solve needs a complex128 operator");
+  int rc = eo_prepare(h, st);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(h->eo_mu);
+  if (h->links_cb32) return MGT_OK;
+  void *p = nullptr;
+  MGT_CUDA(cudaMalloc(&p, h->link_bytes / 2));
+  h->links_cb32 = p;
+  const int64_t n = (int64_t)(h->link_bytes / sizeof(double2));
+  narrow_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>((const double2 *)h->links_cb, (float2 *)p, n);
+  MGT_LAUNCH_CHECK("narrow_kernel (fp32 links)");
+  MGT_CUDA(cudaStreamSynchronize(st));
+  return MGT_OK;
+}
+
 template <typename R, int RECON>
 static int schur_t(mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, int n_rhs, cudaStream_t st) {
   EoGeom E = make_eo_geom(h->g, h->antiperiodic);

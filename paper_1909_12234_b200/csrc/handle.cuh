@@ -30,6 +30,7 @@ struct mgt_wilson_s {
   int dyn_sched;
   // even-odd form: per-parity link copy, built on first use (eo.cu)
   void *links_cb;
+  void *links_cb32;  // fp32 copy of links_cb (mixed-precision solves), built on first use
   std::mutex eo_mu;
   int solve_eo;  // BiCGStab solves the even-odd Schur system (default 1)
 };
@@ -78,6 +79,8 @@ inline WilsonParams make_params(const mgt_wilson_s *h, int flags, double tau) {
 // build the per-parity links if needed; false if the lattice has an odd extent (eo.cu)
 bool eo_available(const mgt_wilson_s *h);
 int eo_prepare(mgt_wilson_s *h, cudaStream_t st);
+// fp32 copy of the per-parity links of an fp64 handle (eo.cu)
+int eo_prepare_mixed(mgt_wilson_s *h, cudaStream_t st);
 
 // the two spin-projected t-faces of x (slab.cu; no peer fence)
 int halo_pack_native(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *to_prev, void *to_next,

@@ -293,6 +293,7 @@ int mgt_wilson_create(mgt_wilson_t *out, const int dims[4], int antiperiodic, do
   h->dyn_sched = 1;
   if (const char *v = getenv("MGT_DYN_SCHED")) h->dyn_sched = atoi(v);
   h->links_cb = nullptr;
+  h->links_cb32 = nullptr;
   h->solve_eo = 1;
   if (const char *v = getenv("MGT_SOLVE_EO")) h->solve_eo = atoi(v);
   h->ctr_next = 0;
@@ -331,6 +332,7 @@ int mgt_wilson_destroy(mgt_wilson_t h) {
   drop_graphs(h);
   cudaFree(h->links);
   if (h->links_cb) cudaFree(h->links_cb);
+  if (h->links_cb32) cudaFree(h->links_cb32);
   cudaFree(h->ctr_ring);
   cudaFreeHost(h->host_flags);
   delete h;

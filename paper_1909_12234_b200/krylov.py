@@ -36,6 +36,11 @@ class SolveConfig:
     # BiCGStab on the even-odd Schur complement (same full-residual stopping
     # test; about half the iterations).  False solves the full system.
     even_odd: bool = True
+    # mixed precision (even-odd only): fp32 inner BiCGStab cycles inside an
+    # fp64 defect correction whose stopping test is the fp64 explicit
+    # residual -- the same ||b - A x|| <= tol ||b|| contract, ~1.4x faster
+    # per solve at 16^4.  False: fp64 throughout.
+    mixed: bool = True
 
     def __post_init__(self):
         if not (0 < self.tol < 1):
@@ -51,6 +56,11 @@ class SolveReport:
     converged: bool
     matvecs: int
     reason: str = ""
+
+
+def solve_options(config):
+    """even_odd / mixed keywords of BiCGStab.solve_native for a config."""
+    return {"even_odd": getattr(config, "even_odd", True), "mixed": getattr(config, "mixed", True)}
 
 
 def _base_operator(op):
@@ -90,7 +100,7 @@ class BiCGStab:
         self.ws_bytes = int(_lib.lib().mgt_bicgstab_workspace_bytes(self.op.handle, self.max_rhs))
         self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device())
 
-    def solve_native(self, b, tol, max_iter, x=None, want_dot=False, even_odd=True):
+    def solve_native(self, b, tol, max_iter, x=None, want_dot=False, even_odd=True, mixed=False):
         """Solve A x_r = b_r for native fields b (n, 12, V); returns
         (x, [SolveReport], dots or None) where dots[r] = vdot(b_r, x_r).
         even_odd: solve through the even-odd Schur complement (whenever every
@@ -102,7 +112,8 @@ class BiCGStab:
         rel = (ct.c_double * n)()
         dots = (ct.c_double * (2 * n))() if want_dot else None
         _lib.check(_lib.lib().mgt_bicgstab_solve_ws(
-            self.op.handle, ptr(b), ptr(x), n, int(self.flags) | (0 if even_odd else _lib.SOLVE_FULL),
+            self.op.handle, ptr(b), ptr(x), n,
+            int(self.flags) | (0 if even_odd else _lib.SOLVE_FULL) | (_lib.SOLVE_MIXED if mixed else 0),
             float(self.tau), float(tol), int(max_iter),
             ptr(self.workspace), self.ws_bytes, rep, rel, dots, stream_ptr()), "bicgstab")
         reports = []
@@ -142,7 +153,7 @@ def bicgstab_solve(op, b, config):
         raise ValueError(f"dimension mismatch: {bd.shape[0]} != {base.dim}")
     solver = _solver_for(op)
     bn = base.to_native(bd.unsqueeze(0))
-    x, reps, _ = solver.solve_native(bn, config.tol, config.max_iter, even_odd=config.even_odd)
+    x, reps, _ = solver.solve_native(bn, config.tol, config.max_iter, **solve_options(config))
     xr = base.from_native(x)[0]
     return (xr.cpu().numpy() if host else xr), reps[0]
 
@@ -184,7 +195,7 @@ class TruncatedInverse:
         for r0 in range(0, b.shape[0], solver.max_rhs):
             x, rr, d = solver.solve_native(b[r0:r0 + solver.max_rhs], self.config.tol,
                                            self.config.max_iter, want_dot=want_dot,
-                                           even_odd=getattr(self.config, "even_odd", True))
+                                           **solve_options(self.config))
             xs.append(x)
             reps.extend(rr)
             if want_dot:

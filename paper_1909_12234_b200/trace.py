@@ -89,14 +89,14 @@ def _solve_batches_concurrently(inv_op, probes, batches, correction, streams):
     every result is a pure function of its probes (bitwise reproducible)."""
     import torch
 
-    from .krylov import _solver_for
+    from .krylov import _solver_for, solve_options
 
     def work(j0, j1, stream):
         with torch.cuda.stream(stream):
             z = probes.noise_native(j0, j1)
             solver = _solver_for(inv_op.op)
             x, reps, q = solver.solve_native(z, inv_op.config.tol, inv_op.config.max_iter, want_dot=True,
-                                             even_odd=getattr(inv_op.config, "even_odd", True))
+                                             **solve_options(inv_op.config))
             if correction is not None:
                 q = q - correction(j0, z, x)
             stream.synchronize()
@@ -311,13 +311,14 @@ def _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op):
     return t0, (restrict, corrections)
 
 
-def coarse_deflation_triplets(coarse_op, k, tol=1e-2, tau=0.0, inner_tol=1e-2, max_iter=2000, max_basis=0):
+def coarse_deflation_triplets(coarse_op, k, tol=1e-2, tau=0.0, inner_tol=1e-2, max_iter=2000, max_basis=0, block=1):
     """Algorithm-2 line 2 (experiments.py:65-74): inexact Davidson on the
     coarse operator (GPU coarse BiCGStab inner solves), converted to singular
-    triplets whose vectors are native coarse fields."""
+    triplets whose vectors are native coarse fields.  block > 1 runs the
+    block Davidson (batched coarse solves)."""
     from . import eigen as E
     from .krylov import SolveConfig
-    conf = E.EigenConfig(k=k, tol=tol, tau=tau, max_basis=max_basis,
+    conf = E.EigenConfig(k=k, tol=tol, tau=tau, max_basis=max_basis, block=block,
                          inner=SolveConfig(tol=inner_tol, max_iter=max_iter))
     res = E.inexact_eigensolve(coarse_op, coarse_op.gamma5_diag, conf, E.shift_inverter_factory(coarse_op, conf.inner))
     return E.to_singular_triplets(res), res

@@ -144,3 +144,66 @@ def test_odd_extent_solves_full_system(cuda):
     import torch
     with pytest.raises(ValueError):
         op.eo_split(torch.zeros((1, 12, geo.site_count), dtype=torch.complex128, device="cuda"))
+
+
+@pytest.mark.parametrize("tol", [1e-3, 1e-8, 1e-11])
+def test_mixed_precision_solve_contract(cuda, tol):
+    """fp32 inner cycles + fp64 defect correction: the same explicit-residual
+    contract ||b - A x|| <= tol ||b|| (checked here against the oracle CSR),
+    the same solution and quadratic forms as the fp64 solve within tol."""
+    import torch
+    M, geo, op, A = _setup((8, 8, 8, 8))
+    N = op.dim
+    z = np.stack([P.rademacher_numpy(N, 500 + j) for j in range(6)])
+    zn = op.to_native(torch.as_tensor(z).cuda())
+    sol = M.krylov.BiCGStab(op, max_rhs=8)
+    xm, rm, qm = sol.solve_native(zn, tol, 4000, want_dot=True, mixed=True)
+    xd, rd, qd = sol.solve_native(zn, tol, 4000, want_dot=True)
+    X = op.from_native(xm).cpu().numpy()
+    for j in range(6):
+        assert rm[j].converged and rm[j].final_relres <= tol
+        r = z[j] - A @ X[j]
+        assert np.linalg.norm(r) <= 1.01 * tol * np.linalg.norm(z[j])
+        assert abs(rm[j].final_relres - np.linalg.norm(r) / np.linalg.norm(z[j])) < 1e-3 * tol + 1e-13
+        assert abs(qm[j] - np.vdot(z[j], X[j])) < 1e-12 * abs(qm[j])
+        assert abs(qm[j] - qd[j]) < 10 * tol * abs(qd[j])
+        assert rm[j].iterations <= 3 * rd[j].iterations + 16
+
+
+@pytest.mark.parametrize("flags,tau", [(0, 0.5), (3, -0.2), (4, 0.0), (1, 0.3)])
+def test_mixed_precision_operator_variants(cuda, flags, tau):
+    from paper_1909_12234_b200.lattice import FormOperator
+    M, geo, op, A = _setup((4, 4, 4, 8), eps=0.3)
+    form = FormOperator(op, flags, tau, "t")
+    rng = np.random.default_rng(7)
+    b = rng.normal(size=op.dim) + 1j * rng.normal(size=op.dim)
+    x, rep = M.bicgstab_solve(form, b, M.SolveConfig(tol=1e-10, mixed=True))
+    assert rep.converged
+    assert np.linalg.norm(b - form.apply(x)) <= 1.01e-10 * np.linalg.norm(b)
+
+
+def test_mixed_precision_edge_cases(cuda):
+    """zero rhs (done at once), max_iter exhausted (reported, not converged),
+    odd extent (falls back to the fp64 full-system solve)."""
+    M, geo, op, A = _setup((4, 4, 4, 4))
+    cfg = M.SolveConfig(mixed=True)
+    x, rep = M.bicgstab_solve(op, np.zeros(op.dim, dtype=complex), cfg)
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+    x, rep = M.bicgstab_solve(op, np.ones(op.dim, dtype=complex), M.SolveConfig(tol=1e-14, max_iter=3, mixed=True))
+    assert not rep.converged and rep.iterations <= 3 + 8
+    M2, geo2, op2, A2 = _setup((4, 4, 4, 5))
+    b = np.random.default_rng(8).normal(size=op2.dim) + 0j
+    x, rep = M2.bicgstab_solve(op2, b, M2.SolveConfig(tol=1e-10, mixed=True))
+    assert rep.converged and np.linalg.norm(b - A2 @ x) <= 1.01e-10 * np.linalg.norm(b)
+
+
+def test_mixed_hutchinson_within_tolerance(cuda):
+    dims = (4, 4, 4, 8)
+    M, geo, op, A = _setup(dims)
+    s = 8
+    probes = M.build_probe_set(geo, 12, s, hp_count=1, dilution=False, kind="rademacher", seed=23)
+    est = M.hutchinson(M.TruncatedInverse(op, M.SolveConfig(tol=1e-10, mixed=True)), probes)
+    lu = spla.splu(A.tocsc())
+    exact = np.array([np.vdot(z, lu.solve(z)) for z in
+                      (P.rademacher_numpy(op.dim, 23 + j) for j in range(s))])
+    assert np.max(np.abs(est.samples - exact) / np.abs(exact)) < 1e-9

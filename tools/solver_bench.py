@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--groups", default="1,2,4")
     ap.add_argument("--nprobe", type=int, default=16)
     ap.add_argument("--recon", type=int, default=12)
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--mixed", default="0", help="comma list of 0/1")
     args = ap.parse_args()
     for ds in args.dims.split(","):
         dims = tuple(int(v) for v in ds.split("x"))
@@ -28,18 +30,19 @@ def main():
         op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.2, seed=0), 0.1, recon=args.recon)
         probes = M.build_probe_set(geo, 12, args.nprobe, dilution=False, kind="rademacher", seed=0)
         z = probes.noise_native(0, args.nprobe)
-        solver = K.BiCGStab(op)
-        for g in [int(v) for v in args.groups.split(",")]:
+        solver = K.BiCGStab(op, max_rhs=max(4, max(int(v) for v in args.groups.split(","))))
+        for g, mixed in [(int(v), int(m)) for v in args.groups.split(",") for m in args.mixed.split(",")]:
             for rep in range(2):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 its = []
                 for j0 in range(0, args.nprobe, g):
-                    x, reps, q = solver.solve_native(z[j0:j0 + g], 1e-8, 2000, want_dot=True)
+                    x, reps, q = solver.solve_native(z[j0:j0 + g], args.tol, 4000, want_dot=True, mixed=bool(mixed))
                     its += [r.iterations for r in reps]
                 torch.cuda.synchronize()
                 el = time.perf_counter() - t0
-            print(json.dumps({"dims": ds, "group": g, "probes_per_s": args.nprobe / el,
+            print(json.dumps({"dims": ds, "group": g, "mixed": mixed, "tol": args.tol,
+                              "probes_per_s": args.nprobe / el, "max_relres": max(r.final_relres for r in reps),
                               "ms_per_probe": el / args.nprobe * 1e3, "mean_iters": sum(its) / len(its),
                               "us_per_iter_per_rhs": el / sum(its) * 1e6}), flush=True)
 
