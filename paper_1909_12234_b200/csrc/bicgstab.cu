@@ -107,6 +107,16 @@ __device__ __forceinline__ bool czero(C<double> a) { return a.re == 0.0 && a.im 
 __device__ __forceinline__ double cabs2(C<double> a) { return a.re * a.re + a.im * a.im; }
 __device__ __forceinline__ bool cfinite(C<double> a) { return isfinite(a.re) && isfinite(a.im); }
 
+// resident blocks per SM of the even-odd stencil kernels: fp64 at 3 (168
+// registers, no spills); the fp32 inner kernels need fewer registers
+#ifndef MGT_F32_MINB
+#define MGT_F32_MINB 3
+#endif
+template <typename R>
+constexpr int eo_minb() {
+  return sizeof(R) == 4 ? MGT_F32_MINB : 3;
+}
+
 #define MGT_SITE_LOOP(M, V) for (int64_t o = (M).first(); o < (V); o += (M).stride())
 
 // Dynamically scheduled loop over chunks of RhsMap<NR>::SPB ordered sites
@@ -650,7 +660,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_rhs(BiEo X, LinkField<doub
 // first half of S: tmp = Dg^-1 H_oe (G_in f), f = p / s / x (mode 0: rhs
 // still iterating, mode 1: rhs whose true residual is due)
 template <int NR, int RECON, typename R = double>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<R, RECON> le,
+__global__ void __launch_bounds__(kRedBlock, eo_minb<R>()) bi_eo_first(BiEo X, LinkField<R, RECON> le,
                                                             LinkField<R, RECON> lo, const cplx<R> *f, BiWST<R> w_,
                                                             int mode) {
   const BiWST<R> w = w_.at(blockIdx.y);
@@ -680,7 +690,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_first(BiEo X, LinkField<R,
 
 // K1 (eo): v = S p = G_out [ Dg G_in p - 1/4 H_eo tmp ] ; sigma = (rhat, v)
 template <int NR, int RECON, typename R = double>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<R, RECON> le,
+__global__ void __launch_bounds__(kRedBlock, eo_minb<R>()) bi_k1_eo(BiEo X, LinkField<R, RECON> le,
                                                          LinkField<R, RECON> lo, BiWST<R> w_) {
   const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
@@ -713,7 +723,7 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1_eo(BiEo X, LinkField<R, RE
 
 // K3 (eo): t = S s ; (t, s), |t|^2
 template <int NR, int RECON, typename R = double>
-__global__ void __launch_bounds__(kRedBlock, 3) bi_k3_eo(BiEo X, LinkField<R, RECON> le,
+__global__ void __launch_bounds__(kRedBlock, eo_minb<R>()) bi_k3_eo(BiEo X, LinkField<R, RECON> le,
                                                          LinkField<R, RECON> lo, BiWST<R> w_) {
   const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;

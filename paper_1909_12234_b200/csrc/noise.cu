@@ -72,41 +72,58 @@ __device__ __forceinline__ void emit(uint32_t w, double2 *dst) {
   }
 }
 
+// Thread = (field, spatial site, run of kSeg consecutive t): reference order
+// has t fastest, so the run's 6 * kSeg outputs are consecutive steps of the
+// stream -- one jump ahead per run instead of one per site (the jump's
+// 128-bit multiplies were the kernel's cost).  A warp covers 32 consecutive
+// native spatial sites, so every store is coalesced.
+constexpr int kSeg = 8;
+
 template <int KIND, bool NATIVE>
 __global__ void noise_kernel(Geom g, Geom gref, int t_begin, const __grid_constant__ NoiseBatch nb, int nf, int field0,
                              double2 *__restrict__ out) {
-  const int64_t n = g.V * nf;
+  const int64_t plane = g.stride[3];
+  const int nseg = (g.L[3] + kSeg - 1) / kSeg;
+  const int64_t per_field = plane * nseg;
+  const int64_t n = per_field * nf;
+  const U128 M = {0x2360ED051FC65DA4ULL, 0x4385DF649FCCF645ULL};
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int f = (int)(idx / g.V);
-    const int64_t s = idx - (int64_t)f * g.V;
+    const int f = (int)(idx / per_field);
+    const int64_t rem = idx - (int64_t)f * per_field;
+    const int seg = (int)(rem / plane);
+    const int64_t sp = rem - (int64_t)seg * plane;  // native spatial index (t = 0)
+    const int tl0 = seg * kSeg, tl1 = min(g.L[3], tl0 + kSeg);
     int x[4];
-    native_coords(g, s, x);
-    x[3] += t_begin;  // t-slab: the probe is the global one restricted to this slab
-    const int64_t r = ref_site(gref, x);
-    // jump 6r steps: st <- A_k st + C_k
+    native_coords(g, sp, x);
+    x[3] = t_begin + tl0;  // t-slab: the probe is the global one restricted to this slab
+    const int64_t r0 = ref_site(gref, x);
+    // jump 6 r0 steps: st <- A_k st + C_k
     U128 st = nb.state[f];
     const U128 inc = nb.inc[f];
-    uint64_t k = (uint64_t)r * 6u;
+    uint64_t k = (uint64_t)r0 * 6u;
     for (int b = 0; k; ++b, k >>= 1) {
       if (k & 1) st = add128(mul128(st, c_mult_pow[b]), nb.cpow[f][b]);
     }
-    const U128 M = {0x2360ED051FC65DA4ULL, 0x4385DF649FCCF645ULL};
     const int fg = field0 + f;
+    for (int tl = tl0; tl < tl1; ++tl) {
+      const int64_t s = (int64_t)tl * plane + sp;
+      const int64_t r = r0 + (tl - tl0);
 #pragma unroll
-    for (int m = 0; m < 6; ++m) {
-      st = add128(mul128(st, M), inc);
-      const uint64_t o = xsl_rr(st);
-      const int c0 = 2 * m, c1 = 2 * m + 1;
-      double2 *d0, *d1;
-      if (NATIVE) {
-        d0 = out + ((int64_t)fg * 12 + c0) * g.V + s;
-        d1 = out + ((int64_t)fg * 12 + c1) * g.V + s;
-      } else {
-        d0 = out + (int64_t)fg * 12 * g.V + r * 12 + c0;
-        d1 = d0 + 1;
+      for (int m = 0; m < 6; ++m) {
+        st = add128(mul128(st, M), inc);
+        const uint64_t o = xsl_rr(st);
+        const int c0 = 2 * m, c1 = 2 * m + 1;
+        double2 *d0, *d1;
+        if (NATIVE) {
+          d0 = out + ((int64_t)fg * 12 + c0) * g.V + s;
+          d1 = out + ((int64_t)fg * 12 + c1) * g.V + s;
+        } else {
+          d0 = out + (int64_t)fg * 12 * g.V + r * 12 + c0;
+          d1 = d0 + 1;
+        }
+        emit<KIND>((uint32_t)(o & 0xFFFFFFFFu), d0);
+        emit<KIND>((uint32_t)(o >> 32), d1);
       }
-      emit<KIND>((uint32_t)(o & 0xFFFFFFFFu), d0);
-      emit<KIND>((uint32_t)(o >> 32), d1);
     }
   }
 }
@@ -154,7 +171,8 @@ static int noise_impl(const int dims[4], const int dims_ref[4], int t_begin, int
         a = mul128(a, a);
       }
     }
-    const int block = 128, grid = grid_for(g.V * nf, block, 8);
+    const int block = 128;
+    const int grid = grid_for(g.stride[3] * ((g.L[3] + kSeg - 1) / kSeg) * nf, block, 8);
     double2 *o = (double2 *)out_dev;
     if (kind == 0 && native_layout)
       noise_kernel<0, true><<<grid, block, 0, st>>>(g, gref, t_begin, nb, nf, f0, o);

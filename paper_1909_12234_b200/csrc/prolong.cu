@@ -168,14 +168,30 @@ __global__ void __launch_bounds__(256) prolong_kernel(Agg a, int n_rhs, const do
 // the x block of its aggregate/chirality (all NR rhs, tiles of JT entries)
 // in shared memory; warp w owns columns k = w, w+8, .., so every P entry is
 // read from HBM once for all rhs and every staged x entry feeds CPW columns.
+// The gather offsets of the support entries (comp * V + site offset inside
+// the aggregate, the same for every aggregate since the native index is
+// linear in the coordinates) are tabulated once per CTA in shared memory,
+// so the staging loop does no index arithmetic.
 // Fixed reduction order: per-lane partial sums, then a shuffle-xor tree.
 constexpr int kRestrictJT = 1024;
+
+// native offset of local site s inside an aggregate, relative to its origin
+__device__ __forceinline__ int64_t agg_local_offset(const Agg &a, int s) {
+  const int l2 = s % a.B[2];
+  int q = s / a.B[2];
+  const int l1 = q % a.B[1];
+  q /= a.B[1];
+  const int l0 = q % a.B[0];
+  const int l3 = q / a.B[0];
+  return (int64_t)l3 * a.g.stride[3] + (int64_t)l0 * a.g.stride[0] + (int64_t)l1 * a.g.stride[1] + l2;
+}
 
 template <int CPW, int NR>
 __global__ void __launch_bounds__(256) restrict_mrhs_kernel(Agg a, const double2 *__restrict__ P,
                                                            const double2 *__restrict__ x,
                                                            double2 *__restrict__ xc, int gamma5_in) {
-  extern __shared__ double2 sx[];  // [NR][kRestrictJT]
+  extern __shared__ double2 sx[];  // [NR][kRestrictJT], then the bs gather offsets
+  int64_t *joff = reinterpret_cast<int64_t *>(sx + NR * kRestrictJT);
   const int64_t grp = blockIdx.x;
   const int64_t b = grp >> 1;
   const int c = (int)(grp & 1);
@@ -183,6 +199,12 @@ __global__ void __launch_bounds__(256) restrict_mrhs_kernel(Agg a, const double2
   const double sign = (gamma5_in && c == 1) ? -1.0 : 1.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double2 *G = P + grp * a.nv * (int64_t)a.bs;
+  const double2 *xb = x + agg_site(a, b, 0);
+  for (int j = threadIdx.x; j < a.bs; j += blockDim.x) {
+    const int q = j / a.S, s = j - (j / a.S) * a.S;
+    const int comp = (2 * c + q / 3) * 3 + q % 3;
+    joff[j] = (int64_t)comp * a.g.V + agg_local_offset(a, s);
+  }
   C<double> acc[CPW][NR];
 #pragma unroll
   for (int i = 0; i < CPW; ++i)
@@ -191,13 +213,14 @@ __global__ void __launch_bounds__(256) restrict_mrhs_kernel(Agg a, const double2
   for (int j0 = 0; j0 < a.bs; j0 += kRestrictJT) {
     const int jn = min(kRestrictJT, a.bs - j0);
     __syncthreads();
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const double2 *xr = xb + (int64_t)r * 12 * a.g.V;
 #pragma unroll 4
-    for (int t = threadIdx.x; t < jn * NR; t += blockDim.x) {
-      const int r = t / jn, jj = t - r * jn, j = j0 + jj;
-      const int q = j / a.S, s = j % a.S;
-      const int comp = (2 * c + q / 3) * 3 + q % 3;
-      const double2 v = x[((int64_t)r * 12 + comp) * a.g.V + agg_site(a, b, s)];
-      sx[r * kRestrictJT + jj] = make_double2(sign * v.x, sign * v.y);
+      for (int jj = threadIdx.x; jj < jn; jj += blockDim.x) {
+        const double2 v = xr[joff[j0 + jj]];
+        sx[r * kRestrictJT + jj] = make_double2(sign * v.x, sign * v.y);
+      }
     }
     __syncthreads();
 #pragma unroll 4
@@ -235,11 +258,12 @@ __global__ void __launch_bounds__(256) restrict_mrhs_kernel(Agg a, const double2
 template <int CPW, int NR>
 static int launch_restrict_mrhs(const Agg &a, const double2 *P, const double2 *x, double2 *xc, int g5,
                                 cudaStream_t st) {
-  const size_t smem = (size_t)NR * kRestrictJT * sizeof(double2);
+  const size_t smem = (size_t)NR * kRestrictJT * sizeof(double2) + (size_t)a.bs * sizeof(int64_t);
+  if (smem > 200 * 1024) return fail(MGT_ERR_INVALID, "mgt_restrict: aggregate too large");
   static bool attr = false;
   if (!attr) {
     MGT_CUDA(cudaFuncSetAttribute(restrict_mrhs_kernel<CPW, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+                                  200 * 1024));
     attr = true;
   }
   restrict_mrhs_kernel<CPW, NR><<<(unsigned)(a.nb * 2), 256, smem, st>>>(a, P, x, xc, g5);

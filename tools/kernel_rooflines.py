@@ -119,11 +119,15 @@ def main():
         # full system: 4608 B/site/rhs per iteration; even-odd Schur system:
         # 2 x (first half 480 + second half 576) + 15 parity-field streams x 96
         # = 3552 B per full site per rhs
-        for eo, model, name in [(False, 4608, "full"), (True, 3552, "even-odd Schur")]:
-            solver.solve_native(z, 1e-8, 2000, even_odd=eo)
+        # mixed: fp32 inner iterations stream half of the even-odd bytes
+        # (1776 B per full site per rhs); the fp64 residual recomputations and
+        # corrections are inside the whole-solve time
+        for eo, mixed, model, name in [(False, False, 4608, "full"), (True, False, 3552, "even-odd Schur"),
+                                       (True, True, 1776, "mixed even-odd Schur, fp32 inner")]:
+            solver.solve_native(z, 1e-8, 2000, even_odd=eo, mixed=mixed)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            _, reps, _ = solver.solve_native(z, 1e-8, 2000, even_odd=eo)
+            _, reps, _ = solver.solve_native(z, 1e-8, 2000, even_odd=eo, mixed=mixed)
             torch.cuda.synchronize()
             el = time.perf_counter() - t0
             its = sum(r.iterations for r in reps) / 4
