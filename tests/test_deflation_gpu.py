@@ -62,6 +62,24 @@ def test_orthogonal_deflation_matches_reference(gold, setup):
         TR.deflate_orthogonal(inv, 2.0 * gold["eig_vectors"], probes)
 
 
+def test_orthogonal_deflation_guess_matches_zero_start(gold, setup):
+    """The deflated start x0 = Y U^H z computes the same slot values
+    z^H (x - Y U^H z) within the solver tolerance; residuals are reported
+    relative to the probe and meet tol."""
+    M, geo, op = setup
+    from paper_1909_12234_b200 import trace as TR
+    probes = M.build_probe_set(geo, 12, 6, hp_count=1, dilution=False, kind="rademacher", seed=77)
+    tol = 1e-9
+    inv_g = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
+    inv_z = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
+    eg = TR.deflate_orthogonal(inv_g, gold["eig_vectors"], probes, guess=True)
+    ez = TR.deflate_orthogonal(inv_z, gold["eig_vectors"], probes, guess=False)
+    assert eg.t0 == ez.t0
+    assert np.max(np.abs(eg.samples - ez.samples) / np.abs(ez.samples)) < 10 * tol
+    assert inv_g.n_solves == inv_z.n_solves
+    assert inv_g.n_failed == 0 and inv_g.last_report.final_relres <= tol
+
+
 def test_davidson_eigenpairs_match_reference(gold, setup):
     M, geo, op = setup
     from paper_1909_12234_b200 import eigen as E
