@@ -302,7 +302,8 @@ def run_ours(args):
             probes3 = probes_config3(M, rank, world)
             if world == 1 and not args.skip_eigen:
                 probes4 = probes_config4(M, rank, world)
-    probes5 = probes_config5(M, rank, world) if args.config5 else None
+    torch.cuda.empty_cache()
+    probes5 = probes_config5(M, rank, world) if not (args.skip_probes or args.skip_config5) else None
     dsolve = None
     if (world > 1 or args.dist_solve) and args.prec == 64:
         try:
@@ -571,7 +572,8 @@ def main():
     ap.add_argument("--skip-probes", action="store_true")
     ap.add_argument("--skip-deflated", action="store_true")
     ap.add_argument("--skip-eigen", action="store_true")
-    ap.add_argument("--config5", action="store_true", help="also run BASELINE configs[4] (minutes)")
+    ap.add_argument("--config5", action="store_true", help="(default now) run BASELINE configs[4]")
+    ap.add_argument("--skip-config5", action="store_true", help="skip BASELINE configs[4] (~45 s)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

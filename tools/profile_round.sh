@@ -6,7 +6,7 @@ P=${1:-prof}
 O=gpurun_out
 python bench.py --steps 20 --warmup 3 > $O/${P}_bench.json 2> $O/${P}_bench.err || exit 1
 python tools/kernel_rooflines.py > $O/${P}_kernel_rooflines.jsonl 2> $O/${P}_kernel_rooflines.err
-CMD="python bench.py --skip-eigen --skip-cpu --steps 3 --warmup 3"
+CMD="python bench.py --skip-eigen --skip-cpu --skip-config5 --steps 3 --warmup 3"
 MGT_SOLVE_STREAMS=1 $CMD > $O/${P}_plain_s1.log 2>&1 || exit 2
 MGT_SOLVE_STREAMS=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file $O/${P}_launches.csv $CMD > $O/${P}_ncu_launch.log 2>&1
