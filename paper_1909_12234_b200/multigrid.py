@@ -105,15 +105,19 @@ def generate_null_vectors(op, n, tol=1e-2, max_iter=200, seed=0):
     vecs = op.new_field(n)
     ratios = np.empty(n)
     degenerate = np.zeros(n, dtype=bool)
-    # the start y0 = normal(N) + 1j normal(N) of the reference, drawn with
-    # standard_normal into pinned buffers (the same stream and values as
-    # rng.normal: loc 0, scale 1) and combined on the device
+    # the start y0 = normal(N) + 1j normal(N) of the reference: the same
+    # stream and values as rng.normal (loc 0, scale 1), replayed by parallel
+    # host threads (rng.NormalStream, bitwise equal; the next vector's draws
+    # are decoded while this one relaxes on the GPU) into pinned buffers and
+    # combined on the device
+    from .rng import NormalStream
+    normals = NormalStream(rng)
     re_h = torch.empty(N, dtype=torch.float64).pin_memory()
     im_h = torch.empty(N, dtype=torch.float64).pin_memory()
     for i in range(n):
         for attempt in range(3):
-            rng.standard_normal(out=re_h.numpy())
-            rng.standard_normal(out=im_h.numpy())
+            normals.take(N, out=re_h.numpy())
+            normals.take(N, out=im_h.numpy())
             y0 = op.to_native(torch.complex(re_h.to(device(), non_blocking=True),
                                             im_h.to(device(), non_blocking=True)))
             torch.cuda.current_stream().synchronize()  # the pinned buffers are refilled next
