@@ -146,6 +146,22 @@ def test_coarse_davidson_and_rank_r_oblique_deflation(gold, setup):
     assert np.max(np.abs(est2.samples - gold["oblr_samples"]) / np.abs(gold["oblr_samples"])) < 1e-6
 
 
+@pytest.mark.parametrize("block", [2, 4])
+def test_coarse_block_davidson(gold, setup, block):
+    """Block Davidson on the coarse operator (batched coarse BiCGStab inner
+    solves): the reference's coarse eigenvalues within the eigen tolerance."""
+    M, MG, geo, op, A, Pg = setup
+    from paper_1909_12234_b200 import trace as TR
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    C = MG.build_coarse_operator(op, pro)
+    trip, res = TR.coarse_deflation_triplets(C, 8, tol=1e-6, inner_tol=1e-12, block=block)
+    assert res.converged.all()
+    exact = gold["ceig_exact"]
+    assert np.max(np.abs(res.lambdas - exact) / np.abs(exact)) < 1e-9
+    assert np.all(np.diff(trip.sigmas) >= 0)
+
+
 def test_posterior_rank_sweep_matches_reference(gold, setup):
     M, MG, geo, op, A, Pg = setup
     from paper_1909_12234_b200 import trace as TR
