@@ -11,6 +11,7 @@ Gaussian noise (not a BASELINE probe kind) is drawn with numpy exactly as the
 reference does.
 """
 
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -29,14 +30,21 @@ class NoiseVector:
     values: object
 
 
-def seed_words(seeds):
-    """(n, 4) uint64 {state_hi, state_lo, inc_hi, inc_lo} per numpy seed."""
-    out = np.empty((len(seeds), 4), dtype=np.uint64)
+@functools.lru_cache(maxsize=1 << 16)
+def _seed_word(s):
+    st = np.random.PCG64(s).state["state"]
+    state, inc = int(st["state"]), int(st["inc"])
     m = (1 << 64) - 1
+    return (state >> 64, state & m, inc >> 64, inc & m)
+
+
+def seed_words(seeds):
+    """(n, 4) uint64 {state_hi, state_lo, inc_hi, inc_lo} per numpy seed
+    (SeedSequence hashing of each seed, cached: the probes of a sweep reuse
+    their seeds)."""
+    out = np.empty((len(seeds), 4), dtype=np.uint64)
     for i, s in enumerate(seeds):
-        st = np.random.PCG64(int(s)).state["state"]
-        state, inc = int(st["state"]), int(st["inc"])
-        out[i] = (state >> 64, state & m, inc >> 64, inc & m)
+        out[i] = _seed_word(int(s))
     return out
 
 
