@@ -305,6 +305,20 @@ int mgt_coarse_apply(const int dims[4], const int block[4], int nv,
 int mgt_coarse_apply_c32(const int dims[4], const int block[4], int nv,
                          const void *C32_dev, const void *xc_dev, void *yc_dev,
                          int n_rhs, void *stream);
+/* One BiCGStab iteration on (C + i tau g5_c) for n_rhs independent native
+ * coarse systems (the inner solves of coarse Davidson / Algorithm 2,
+ * multigrid.coarse_bicgstab; the reference runs GCR on C through
+ * LatticeOperator.apply, krylov.py:52-118 / multigrid.py:228-243).  C is the
+ * fp64 operator, or its fp32 copy when c_fp32 != 0.  Vectors (n_rhs, Nc)
+ * complex128 on the device: x, r, p, v, s, t updated in place, rhat read.
+ * state: n_rhs rows of 12 doubles [rho re, im, alpha re, im, omega re, im,
+ * beta re, im, |r|^2, active, tol^2, converged], read and written on the
+ * device (the caller seeds rho, active, tol^2 and reads |r|^2 / converged). */
+int mgt_coarse_bicgstab_iter(const int dims[4], const int block[4], int nv,
+                             const void *C_dev, int c_fp32, double tau,
+                             int n_rhs, void *x, void *r, const void *rhat,
+                             void *p, void *v, void *s, void *t,
+                             double *state, void *stream);
 
 /* ---- deflation projection (trace.py:161-188, :266-267; eigen.py:79-86) --- */
 /* H (k x s, column major, complex128) = V^H X;  V: (k, len) row-major

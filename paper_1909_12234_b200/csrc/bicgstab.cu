@@ -1256,14 +1256,16 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
   X.R = make_eo_roles(P);
   LinkField<double, RECON> le{reinterpret_cast<const double2 *>(h->links_cb), Vs};
   LinkField<double, RECON> lo{reinterpret_cast<const double2 *>((const char *)h->links_cb + h->link_bytes / 2), Vs};
-  LinkField<float, RECON> le32{reinterpret_cast<const float2 *>(h->links_cb32), Vs};
-  LinkField<float, RECON> lo32{reinterpret_cast<const float2 *>((const char *)h->links_cb32 + h->link_bytes / 4), Vs};
+  // fp32 links: the handle's storage narrowed, or (MGT_MIXED_L18) full 3x3
+  constexpr int R32 = MGT_MIXED_L18 ? 18 : RECON;
+  LinkField<float, R32> le32{reinterpret_cast<const float2 *>(h->links_cb32), Vs};
+  LinkField<float, R32> lo32{reinterpret_cast<const float2 *>(h->links_cb32) + (R32 / 2) * 4 * Vs, Vs};
   static int g_str = 0, g_e1 = 0, g_e2 = 0, g_f1 = 0, g_f2 = 0;  // resident grids, per template instance
   if (!g_str) g_str = resident_grid(bi_k4<NR>, kRedBlock, (int64_t)1 << 40);
   if (!g_e1) g_e1 = resident_grid(bi_eo_first<NR, RECON>, kRedBlock, (int64_t)1 << 40);
   if (!g_e2) g_e2 = resident_grid(bi_k1_eo<NR, RECON>, kRedBlock, (int64_t)1 << 40);
-  if (!g_f1) g_f1 = resident_grid(bi_eo_first<NR, RECON, float>, kRedBlock, (int64_t)1 << 40);
-  if (!g_f2) g_f2 = resident_grid(bi_k1_eo<NR, RECON, float>, kRedBlock, (int64_t)1 << 40);
+  if (!g_f1) g_f1 = resident_grid(bi_eo_first<NR, R32, float>, kRedBlock, (int64_t)1 << 40);
+  if (!g_f2) g_f2 = resident_grid(bi_k1_eo<NR, R32, float>, kRedBlock, (int64_t)1 << 40);
   const int64_t need = (Vs + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
   auto per_group = [&](int resident) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, std::max(1, resident / G)));
@@ -1290,7 +1292,7 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
       MGT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
       cudaGraph_t graph;
       MGT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-      launch_chunk_eo<NR, RECON, float>(X, le32, lo32, w32, fd, f1, grid, cap);
+      launch_chunk_eo<NR, R32, float>(X, le32, lo32, w32, fd, f1, grid, cap);
       cudaError_t e = cudaStreamEndCapture(cap, &graph);
       cudaStreamDestroy(cap);
       if (e != cudaSuccess) return cuda_fail(e, "mixed bicgstab graph capture");

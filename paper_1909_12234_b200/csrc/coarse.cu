@@ -16,6 +16,7 @@
 // blocks, nc = 2 nv), b in native coarse order; block dir couples b to
 // nbr(b, dir) (dir 0: b itself).  The antiperiodic phase lives in the hops.
 #include <algorithm>
+#include <type_traits>
 
 #include "handle.cuh"
 #include "reduce.cuh"
@@ -33,16 +34,23 @@ __device__ __forceinline__ int64_t coarse_nbr(const CoarseGeom &cg, int64_t b, i
   if (dir == 0) return b;
   const int mu = (dir - 1) >> 1;
   const int sgn = ((dir - 1) & 1) ? -1 : 1;
-  int c[4];
+  // scalar coordinates (no local array: keeps the kernels off the stack)
   int64_t r = b;
-  c[2] = (int)(r % cg.Cd[2]);
+  int c2 = (int)(r % cg.Cd[2]);
   r /= cg.Cd[2];
-  c[1] = (int)(r % cg.Cd[1]);
+  int c1 = (int)(r % cg.Cd[1]);
   r /= cg.Cd[1];
-  c[0] = (int)(r % cg.Cd[0]);
-  c[3] = (int)(r / cg.Cd[0]);
-  c[mu] = (c[mu] + sgn + cg.Cd[mu]) % cg.Cd[mu];
-  return (((int64_t)c[3] * cg.Cd[0] + c[0]) * cg.Cd[1] + c[1]) * cg.Cd[2] + c[2];
+  int c0 = (int)(r % cg.Cd[0]);
+  int c3 = (int)(r / cg.Cd[0]);
+  if (mu == 0)
+    c0 = (c0 + sgn + cg.Cd[0]) % cg.Cd[0];
+  else if (mu == 1)
+    c1 = (c1 + sgn + cg.Cd[1]) % cg.Cd[1];
+  else if (mu == 2)
+    c2 = (c2 + sgn + cg.Cd[2]) % cg.Cd[2];
+  else
+    c3 = (c3 + sgn + cg.Cd[3]) % cg.Cd[3];
+  return (((int64_t)c3 * cg.Cd[0] + c0) * cg.Cd[1] + c1) * cg.Cd[2] + c2;
 }
 
 // 9-way split apply (fp64).  out: 9 native fields back to back.
@@ -138,10 +146,13 @@ __global__ void __launch_bounds__(256) coarse_apply_kernel(CoarseGeom cg, int G,
   double2 *sx = sm;                    // [9][nc][NR]
   double2 *part = sm + 9 * nc * NR;    // [G][NR][nc]
   const int64_t b = blockIdx.x;
+  __shared__ int64_t nbr[9];
+  if (threadIdx.x < 9) nbr[threadIdx.x] = coarse_nbr(cg, b, threadIdx.x);
+  __syncthreads();
   for (int i = threadIdx.x; i < 9 * nc * NR; i += blockDim.x) {
     const int r = i % NR, q = i / NR;
     const int dir = q / nc, col = q % nc;
-    sx[i] = x[((int64_t)r * cg.nb + coarse_nbr(cg, b, dir)) * nc + col];
+    sx[i] = x[((int64_t)r * cg.nb + nbr[dir]) * nc + col];
   }
   __syncthreads();
   const int row = threadIdx.x % nc, grp = threadIdx.x / nc;
@@ -175,9 +186,104 @@ __global__ void __launch_bounds__(256) coarse_apply_kernel(CoarseGeom cg, int G,
   }
 }
 
+// The same product with one thread per (dir, row): 9 nc threads per
+// aggregate, each streaming one block row-slice of C (48 columns, loads
+// issued 8 at a time so ~8 x 16 B per thread are in flight) against the
+// staged neighbour vectors; the 9 direction partials are then summed in
+// direction order through shared memory (the staging buffer, reused).
+// Every rhs sees the same arithmetic whatever NR is (bitwise-stable across
+// batchings).  For nc <= 49 (9 nc <= 448 threads, two CTAs per SM).
+constexpr int kCoarseDirThreads = 448;
+template <int NR, typename CT = double2>
+__global__ void __launch_bounds__(kCoarseDirThreads, 2)
+    coarse_apply_dir_kernel(CoarseGeom cg, const CT *__restrict__ Cm, const double2 *__restrict__ x,
+                            double2 *__restrict__ y) {
+  extern __shared__ double2 sm[];  // [9][nc][NR], then [9][NR][nc]
+  __shared__ int64_t nbr[9];
+  const int nc = cg.nc;
+  const int64_t b = blockIdx.x;
+  // the 9 neighbour aggregates once per CTA (64-bit div/mod is not cheap)
+  if (threadIdx.x < 9) nbr[threadIdx.x] = coarse_nbr(cg, b, threadIdx.x);
+  __syncthreads();
+  // arithmetic type: fp64 with the fp64 C; fp32 with its fp32 copy (loose
+  // inner solves only: ~1e-7 relative per product, well inside tol >= 1e-5)
+  using AT = std::conditional_t<sizeof(CT) == 8, float, double>;
+  using A2 = std::conditional_t<sizeof(CT) == 8, float2, double2>;
+  A2 *sx = reinterpret_cast<A2 *>(sm);
+  for (int i = threadIdx.x; i < 9 * nc * NR; i += blockDim.x) {
+    const int col = i % nc, q = i / nc;
+    const int r = q % NR, dir = q / NR;
+    const double2 xv = x[((int64_t)r * cg.nb + nbr[dir]) * nc + col];
+    A2 a;
+    a.x = (AT)xv.x;
+    a.y = (AT)xv.y;
+    sx[(dir * nc + col) * NR + r] = a;
+  }
+  __syncthreads();
+  const int dir = threadIdx.x / nc, row = threadIdx.x - dir * nc;
+  const bool on = dir < 9;
+  C<AT> acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = C<AT>(AT(0), AT(0));
+  if (on) {
+    const CT *Cb = Cm + (b * 9 + dir) * (int64_t)nc * nc + row;
+    const A2 *xs = sx + dir * nc * NR;
+    // loads in flight per thread: 8 (4 for 8 fp64 rhs, register budget)
+    constexpr int U = (sizeof(CT) == 16 && NR >= 2) ? 4 : 8;
+    for (int c0 = 0; c0 < nc; c0 += U) {
+      CT cl[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c0 + u < nc) cl[u] = Cb[(int64_t)(c0 + u) * nc];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (c0 + u < nc) {
+          const C<AT> cv(cl[u].x, cl[u].y);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const A2 xv = xs[(c0 + u) * NR + r];
+            acc[r] = cfma(cv, C<AT>(xv.x, xv.y), acc[r]);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (on) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) sm[(dir * NR + r) * nc + row] = make_double2((double)acc[r].re, (double)acc[r].im);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NR * nc; i += blockDim.x) {
+    const int r = i / nc, rw = i % nc;
+    C<double> t(0.0, 0.0);
+#pragma unroll
+    for (int d = 0; d < 9; ++d) {
+      const double2 v = sm[(d * NR + r) * nc + rw];
+      t = t + C<double>(v.x, v.y);
+    }
+    y[((int64_t)r * cg.nb + b) * nc + rw] = make_double2(t.re, t.im);
+  }
+}
+
 template <int NR, typename CT = double2>
 static int launch_coarse_apply(const CoarseGeom &cg, const CT *C, const double2 *x, double2 *y,
                                cudaStream_t st) {
+  if (9 * cg.nc <= kCoarseDirThreads) {
+    const int block = ((9 * cg.nc + 31) / 32) * 32;
+    const size_t smem = (size_t)9 * cg.nc * NR * sizeof(double2);
+    if (smem > 48 * 1024) {
+      static size_t set = 0;
+      if (smem > set) {
+        MGT_CUDA(cudaFuncSetAttribute(coarse_apply_dir_kernel<NR, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        set = smem;
+      }
+    }
+    coarse_apply_dir_kernel<NR, CT><<<(unsigned)cg.nb, block, smem, st>>>(cg, C, x, y);
+    MGT_LAUNCH_CHECK("coarse_apply_dir_kernel");
+    return MGT_OK;
+  }
   const int G = std::max(1, std::min(9, 256 / cg.nc));
   const int block = ((G * cg.nc + 31) / 32) * 32;
   const size_t smem = (size_t)(9 * cg.nc * NR + G * NR * cg.nc) * sizeof(double2);
@@ -275,10 +381,14 @@ static int coarse_apply_impl(const int dims[4], const int block[4], int nv, cons
   int r = 0;
   while (r < n_rhs) {
     const int left = n_rhs - r;
-    const int nr = left >= 4 ? 4 : (left >= 2 ? 2 : 1);
-    rc = nr == 4 ? launch_coarse_apply<4, CT>(cg, Cp, xp + r * stride, yp + r * stride, st)
-                 : (nr == 2 ? launch_coarse_apply<2, CT>(cg, Cp, xp + r * stride, yp + r * stride, st)
-                            : launch_coarse_apply<1, CT>(cg, Cp, xp + r * stride, yp + r * stride, st));
+    // up to 8 rhs per launch where the per-(dir, row) kernel applies (its
+    // staging buffer is 9 nc NR complex; the older group kernel stops at 4)
+    const bool dirk = 9 * cg.nc <= kCoarseDirThreads;
+    const int nr = (left >= 8 && dirk) ? 8 : (left >= 4 ? 4 : (left >= 2 ? 2 : 1));
+    rc = nr == 8   ? launch_coarse_apply<8, CT>(cg, Cp, xp + r * stride, yp + r * stride, st)
+         : nr == 4 ? launch_coarse_apply<4, CT>(cg, Cp, xp + r * stride, yp + r * stride, st)
+         : nr == 2 ? launch_coarse_apply<2, CT>(cg, Cp, xp + r * stride, yp + r * stride, st)
+                   : launch_coarse_apply<1, CT>(cg, Cp, xp + r * stride, yp + r * stride, st);
     if (rc) return rc;
     r += nr;
   }
@@ -286,7 +396,209 @@ static int coarse_apply_impl(const int dims[4], const int block[4], int nv, cons
 }
 }  // namespace mgt
 
+namespace mgt {
+
+// ---------------------------------------------------------------------------
+// One BiCGStab iteration on the coarse operator (C + i tau g5_c) for n
+// independent rhs, every vector op fused and every scalar kept on the
+// device (multigrid.coarse_bicgstab drives the loop and the explicit-residual
+// confirmations).  Per-rhs state row (doubles):
+//   [rho re, im, alpha re, im, omega re, im, beta re, im, r2, active, tol2, conv]
+// Reductions: per-block partials in a fixed grid, summed in block order by a
+// one-warp finisher per rhs (deterministic).
+enum { CK_RHO = 0, CK_ALPHA = 2, CK_OMEGA = 4, CK_BETA = 6, CK_R2 = 8, CK_ACT = 9, CK_TOL2 = 10, CK_CONV = 11,
+       CK_W = 12 };
+constexpr int kCkBlock = 256;
+
+__device__ __forceinline__ C<double> cdiv(C<double> a, C<double> b) {
+  const double d = b.re * b.re + b.im * b.im;
+  return C<double>((a.re * b.re + a.im * b.im) / d, (a.im * b.re - a.re * b.im) / d);
+}
+
+// sum v[NV] over the block; thread 0 writes part[(rhs * nblk + blk) * NV ..]
+template <int NV>
+__device__ __forceinline__ void ck_publish(double (&v)[NV], double *part) {
+  __shared__ double sm[kCkBlock / 32][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    if (lane == 0) sm[warp][k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kCkBlock / 32; ++w) t += sm[w][threadIdx.x];
+    part[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NV + threadIdx.x] = t;
+  }
+}
+
+// g5_c of element e of a (nb, nc) field: -1 on the second nv columns
+__device__ __forceinline__ double ck_g5(int64_t e, int nc, int nv) { return (int)(e % nc) >= nv ? -1.0 : 1.0; }
+
+// KIND 1: v += i tau g5 p ; sigma = <rhat, v>
+// KIND 3: t += i tau g5 s ; <t, t>, <t, s>
+template <int KIND>
+__global__ void __launch_bounds__(kCkBlock) ck_dots(int64_t L, int nc, int nv, double tau, double2 *__restrict__ a,
+                                                    const double2 *__restrict__ b, const double2 *__restrict__ c,
+                                                    double *part) {
+  const int64_t off = (int64_t)blockIdx.y * L;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t e = blockIdx.x * (int64_t)kCkBlock + threadIdx.x; e < L; e += (int64_t)gridDim.x * kCkBlock) {
+    C<double> y = ldc(a + off + e);
+    const C<double> q = ldc(b + off + e);  // the applied vector (p or s)
+    if (tau != 0.0) {
+      const double g = tau * ck_g5(e, nc, nv);
+      y = C<double>(y.re - g * q.im, y.im + g * q.re);
+      stc(a + off + e, y);
+    }
+    if (KIND == 1) {
+      const C<double> rh = ldc(c + off + e);
+      acc[0] += rh.re * y.re + rh.im * y.im;
+      acc[1] += rh.re * y.im - rh.im * y.re;
+    } else {
+      acc[0] += y.re * y.re + y.im * y.im;
+      acc[1] += y.re * q.re + y.im * q.im;
+      acc[2] += y.re * q.im - y.im * q.re;
+    }
+  }
+  ck_publish<3>(acc, part);
+}
+
+// s = r - alpha v
+__global__ void __launch_bounds__(kCkBlock) ck_sub(int64_t L, const double *__restrict__ st,
+                                                   const double2 *__restrict__ r, const double2 *__restrict__ v,
+                                                   double2 *__restrict__ s) {
+  const int64_t off = (int64_t)blockIdx.y * L;
+  const double *S = st + blockIdx.y * CK_W;
+  const C<double> al(S[CK_ALPHA], S[CK_ALPHA + 1]);
+  for (int64_t e = blockIdx.x * (int64_t)kCkBlock + threadIdx.x; e < L; e += (int64_t)gridDim.x * kCkBlock)
+    stc(s + off + e, ldc(r + off + e) - al * ldc(v + off + e));
+}
+
+// x += alpha p + omega s ; r = s - omega t ; <rhat, r>, <r, r>
+__global__ void __launch_bounds__(kCkBlock) ck_update(int64_t L, const double *__restrict__ st,
+                                                      double2 *__restrict__ x, double2 *__restrict__ r,
+                                                      const double2 *__restrict__ rhat, const double2 *__restrict__ p,
+                                                      const double2 *__restrict__ s, const double2 *__restrict__ t,
+                                                      double *part) {
+  const int64_t off = (int64_t)blockIdx.y * L;
+  const double *S = st + blockIdx.y * CK_W;
+  const C<double> al(S[CK_ALPHA], S[CK_ALPHA + 1]), om(S[CK_OMEGA], S[CK_OMEGA + 1]);
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t e = blockIdx.x * (int64_t)kCkBlock + threadIdx.x; e < L; e += (int64_t)gridDim.x * kCkBlock) {
+    const C<double> ss = ldc(s + off + e);
+    stc(x + off + e, ldc(x + off + e) + al * ldc(p + off + e) + om * ss);
+    const C<double> rr = ss - om * ldc(t + off + e);
+    stc(r + off + e, rr);
+    const C<double> rh = ldc(rhat + off + e);
+    acc[0] += rh.re * rr.re + rh.im * rr.im;
+    acc[1] += rh.re * rr.im - rh.im * rr.re;
+    acc[2] += rr.re * rr.re + rr.im * rr.im;
+  }
+  ck_publish<3>(acc, part);
+}
+
+// p = r + beta (p - omega v)
+__global__ void __launch_bounds__(kCkBlock) ck_dir(int64_t L, const double *__restrict__ st,
+                                                   const double2 *__restrict__ r, double2 *__restrict__ p,
+                                                   const double2 *__restrict__ v) {
+  const int64_t off = (int64_t)blockIdx.y * L;
+  const double *S = st + blockIdx.y * CK_W;
+  const C<double> be(S[CK_BETA], S[CK_BETA + 1]), om(S[CK_OMEGA], S[CK_OMEGA + 1]);
+  for (int64_t e = blockIdx.x * (int64_t)kCkBlock + threadIdx.x; e < L; e += (int64_t)gridDim.x * kCkBlock)
+    stc(p + off + e, ldc(r + off + e) + be * (ldc(p + off + e) - om * ldc(v + off + e)));
+}
+
+// scalar recurrences, one warp per rhs (blockIdx.x = rhs); same guards as the
+// torch formulation (zero denominators freeze the rhs' step)
+template <int KIND>
+__global__ void ck_finish(int nblk, const double *__restrict__ part, double *__restrict__ st) {
+  const int rhs = blockIdx.x, lane = threadIdx.x;
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int b = lane; b < nblk; b += 32)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[k] += part[((int64_t)rhs * nblk + b) * 3 + k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+  if (lane) return;
+  double *S = st + rhs * CK_W;
+  const bool act = S[CK_ACT] != 0.0;
+  const C<double> rho(S[CK_RHO], S[CK_RHO + 1]);
+  if (KIND == 1) {
+    const C<double> sig(v[0], v[1]);
+    const bool ok = act && (sig.re != 0.0 || sig.im != 0.0);
+    const C<double> al = ok ? cdiv(rho, sig) : C<double>(0.0, 0.0);
+    S[CK_ALPHA] = al.re, S[CK_ALPHA + 1] = al.im;
+  } else if (KIND == 3) {
+    const double tt = v[0];
+    const C<double> om = (act && tt > 0.0) ? C<double>(v[1] / tt, v[2] / tt) : C<double>(0.0, 0.0);
+    S[CK_OMEGA] = om.re, S[CK_OMEGA + 1] = om.im;
+  } else {
+    const C<double> rn(v[0], v[1]);
+    const C<double> om(S[CK_OMEGA], S[CK_OMEGA + 1]), al(S[CK_ALPHA], S[CK_ALPHA + 1]);
+    const bool rz = rho.re == 0.0 && rho.im == 0.0, oz = om.re == 0.0 && om.im == 0.0;
+    const C<double> be = (act && !rz && !oz) ? cdiv(rn, rho) * cdiv(al, om) : C<double>(0.0, 0.0);
+    S[CK_BETA] = be.re, S[CK_BETA + 1] = be.im;
+    S[CK_RHO] = rn.re, S[CK_RHO + 1] = rn.im;
+    S[CK_R2] = v[2];
+    const bool nz = rn.re == 0.0 && rn.im == 0.0;
+    S[CK_CONV] = (act && (v[2] <= S[CK_TOL2] || oz || nz)) ? 1.0 : 0.0;
+  }
+}
+
+template <typename CT>
+static int coarse_bicg_iter_impl(const int dims[4], const int block[4], int nv, const void *C_dev, double tau,
+                                 int n, double2 *x, double2 *r, const double2 *rhat, double2 *p, double2 *v,
+                                 double2 *s, double2 *t, double *st_dev, cudaStream_t st) {
+  CoarseGeom cg;
+  int rc = make_cg(dims, block, nv, cg);
+  if (rc) return rc;
+  const int64_t L = cg.nb * cg.nc;
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((L + 4 * kCkBlock - 1) / (4 * kCkBlock),
+                                                               std::max(1, 4 * kNumSMs / n)));
+  double *part = nullptr;
+  MGT_CUDA(scratch_alloc((void **)&part, (size_t)n * nblk * 3 * sizeof(double), st));
+  const dim3 grid(nblk, n);
+  rc = coarse_apply_impl<CT>(dims, block, nv, C_dev, p, v, n, st);
+  if (rc) return rc;
+  ck_dots<1><<<grid, kCkBlock, 0, st>>>(L, cg.nc, nv, tau, v, p, rhat, part);
+  ck_finish<1><<<n, 32, 0, st>>>(nblk, part, st_dev);
+  ck_sub<<<grid, kCkBlock, 0, st>>>(L, st_dev, r, v, s);
+  rc = coarse_apply_impl<CT>(dims, block, nv, C_dev, s, t, n, st);
+  if (rc) return rc;
+  ck_dots<3><<<grid, kCkBlock, 0, st>>>(L, cg.nc, nv, tau, t, s, nullptr, part);
+  ck_finish<3><<<n, 32, 0, st>>>(nblk, part, st_dev);
+  ck_update<<<grid, kCkBlock, 0, st>>>(L, st_dev, x, r, rhat, p, s, t, part);
+  ck_finish<4><<<n, 32, 0, st>>>(nblk, part, st_dev);
+  ck_dir<<<grid, kCkBlock, 0, st>>>(L, st_dev, r, p, v);
+  note_launch(8);
+  MGT_LAUNCH_CHECK("coarse bicgstab iteration");
+  MGT_CUDA(cudaFreeAsync(part, st));
+  return MGT_OK;
+}
+
+}  // namespace mgt
+
 extern "C" {
+
+int mgt_coarse_bicgstab_iter(const int dims[4], const int block[4], int nv, const void *C_dev, int c_fp32,
+                             double tau, int n_rhs, void *x, void *r, const void *rhat, void *p, void *v, void *s,
+                             void *t, double *state, void *stream) {
+  if (!dims || !block || !C_dev || !x || !r || !rhat || !p || !v || !s || !t || !state || n_rhs < 1)
+    return fail(MGT_ERR_INVALID, "mgt_coarse_bicgstab_iter: bad argument");
+  cudaStream_t st = as_stream(stream);
+  auto D = [](const void *q) { return (double2 *)q; };
+  return c_fp32 ? coarse_bicg_iter_impl<float2>(dims, block, nv, C_dev, tau, n_rhs, D(x), D(r), D(rhat), D(p), D(v), D(s),
+                                                D(t), state, st)
+                : coarse_bicg_iter_impl<double2>(dims, block, nv, C_dev, tau, n_rhs, D(x), D(r), D(rhat), D(p), D(v),
+                                                 D(s), D(t), state, st);
+}
 
 int mgt_coarse_apply(const int dims[4], const int block[4], int nv, const void *C_dev, const void *xc_dev,
                      void *yc_dev, int n_rhs, void *stream) {

@@ -59,6 +59,11 @@ __device__ __forceinline__ void bdag_mul(C<R> w0, C<R> w1, C<R> &o2, C<R> &o3) {
 #ifndef MGT_LINK_PAIRS
 #define MGT_LINK_PAIRS 1
 #endif
+// Mixed-precision solves: fp32 per-parity links stored as full 3x3 (no
+// third-row reconstruction in the fp32 hops) when 1.
+#ifndef MGT_MIXED_L18
+#define MGT_MIXED_L18 0
+#endif
 // With MGT_LINK_PAIRS the 12-real links are stored as 3 element pairs per
 // (mu, site), ((mu*3 + e/2)*V + site)*2 + (e & 1): one 256-bit (fp64) /
 // 128-bit (fp32) load per pair.

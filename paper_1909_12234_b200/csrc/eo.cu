@@ -112,6 +112,29 @@ __global__ void narrow_kernel(const double2 *__restrict__ in, float2 *__restrict
   }
 }
 
+// fp32 per-parity links of the mixed solver, full 3x3 (18 reals): built from
+// the fp64 per-parity links (either storage), third row reconstructed once
+// here in fp64 instead of in every fp32 hop.  Layout ((mu*9 + e)*Vh + c) per
+// parity, parities back to back.
+template <int RECON>
+__global__ void narrow_full_kernel(const double2 *__restrict__ cb, float2 *__restrict__ out, int64_t Vh,
+                                   size_t parity_bytes) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * 4 * Vh;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int par = (int)(i / (4 * Vh));
+    const int64_t j = i - (int64_t)par * 4 * Vh;
+    const int mu = (int)(j / Vh);
+    const int64_t c = j - (int64_t)mu * Vh;
+    LinkField<double, RECON> L{reinterpret_cast<const double2 *>((const char *)cb + par * parity_bytes), Vh};
+    C<double> u[3][3];
+    L.load(mu, c, u);
+    float2 *o = out + (int64_t)par * 4 * 9 * Vh;
+#pragma unroll
+    for (int e = 0; e < 9; ++e)
+      o[((int64_t)mu * 9 + e) * Vh + c] = make_float2((float)u[e / 3][e % 3].re, (float)u[e / 3][e % 3].im);
+  }
+}
+
 int eo_prepare_mixed(mgt_wilson_s *h, cudaStream_t st) {
   if (h->prec != 64) return fail(MGT_ERR_INVALID, "mixed-precision solve needs a complex128 operator");
   int rc = eo_prepare(h, st);
@@ -119,11 +142,24 @@ int eo_prepare_mixed(mgt_wilson_s *h, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(h->eo_mu);
   if (h->links_cb32) return MGT_OK;
   void *p = nullptr;
+#if MGT_MIXED_L18
+  const int64_t Vh = h->g.V / 2;
+  MGT_CUDA(cudaMalloc(&p, (size_t)2 * 4 * 9 * Vh * sizeof(float2)));
+  h->links_cb32 = p;
+  if (h->recon == 12)
+    narrow_full_kernel<12><<<grid_for(8 * Vh, 256, 8), 256, 0, st>>>((const double2 *)h->links_cb, (float2 *)p, Vh,
+                                                                     h->link_bytes / 2);
+  else
+    narrow_full_kernel<18><<<grid_for(8 * Vh, 256, 8), 256, 0, st>>>((const double2 *)h->links_cb, (float2 *)p, Vh,
+                                                                     h->link_bytes / 2);
+  MGT_LAUNCH_CHECK("narrow_full_kernel (fp32 links)");
+#else
   MGT_CUDA(cudaMalloc(&p, h->link_bytes / 2));
   h->links_cb32 = p;
   const int64_t n = (int64_t)(h->link_bytes / sizeof(double2));
   narrow_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>((const double2 *)h->links_cb, (float2 *)p, n);
   MGT_LAUNCH_CHECK("narrow_kernel (fp32 links)");
+#endif
   MGT_CUDA(cudaStreamSynchronize(st));
   return MGT_OK;
 }

@@ -146,7 +146,10 @@ __global__ void vhx_reduce_kernel(const double2 *__restrict__ part, int nblk, in
   }
 }
 
-// X[j] -= sum_i V[i] H[i, j] for j in a 16-wide tile (grid.y)
+// X[j] -= sum_i V[i] H[i, j] for j in a TJ-wide tile (grid.y); TJ follows s
+// (1, 2, 4, 8) so no accumulator or H load is wasted on absent columns, and
+// the V loads are issued 8 vectors at a time (independent, in flight
+// together) ahead of their FMAs.
 template <int TJ>
 __global__ void __launch_bounds__(256) proj_sub_kernel(const double2 *__restrict__ V, const double2 *__restrict__ H,
                                                        double2 *__restrict__ X, int64_t len, int k, int s) {
@@ -157,14 +160,26 @@ __global__ void __launch_bounds__(256) proj_sub_kernel(const double2 *__restrict
     sH[q] = (j0 + j < s) ? H[(int64_t)(j0 + j) * k + i] : make_double2(0.0, 0.0);
   }
   __syncthreads();
+  constexpr int U = 8;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
     C<double> acc[TJ];
 #pragma unroll
     for (int j = 0; j < TJ; ++j) acc[j] = C<double>(0.0, 0.0);
-    for (int i = 0; i < k; ++i) {
-      const C<double> v = ldc(V + (int64_t)i * len + e);
+    for (int i0 = 0; i0 < k; i0 += U) {
+      C<double> v[U];
 #pragma unroll
-      for (int j = 0; j < TJ; ++j) acc[j] = cfma(v, C<double>(sH[i * TJ + j].x, sH[i * TJ + j].y), acc[j]);
+      for (int u = 0; u < U; ++u)
+        if (i0 + u < k) v[u] = ldc(V + (int64_t)(i0 + u) * len + e);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u < k) {
+#pragma unroll
+          for (int j = 0; j < TJ; ++j) {
+            const double2 hv = sH[(i0 + u) * TJ + j];
+            acc[j] = cfma(v[u], C<double>(hv.x, hv.y), acc[j]);
+          }
+        }
+      }
     }
 #pragma unroll
     for (int j = 0; j < TJ; ++j) {
@@ -231,14 +246,26 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
 int mgt_proj_sub(const void *V_dev, const void *H_dev, void *X_dev, int64_t len, int k, int s, void *stream) {
   if (!V_dev || !X_dev || !H_dev || len < 0 || k < 1 || s < 1) return fail(MGT_ERR_INVALID, "mgt_proj_sub: bad argument");
   cudaStream_t st = as_stream(stream);
-  constexpr int TJ = 8;
+  const int TJ = s >= 8 ? 8 : (s >= 4 ? 4 : (s >= 2 ? 2 : 1));
   dim3 grid(grid_for(len, 256, 4), (s + TJ - 1) / TJ);
   const size_t smem = (size_t)k * TJ * sizeof(double2);
   if (smem > 200 * 1024) return fail(MGT_ERR_INVALID, "mgt_proj_sub: k too large");
-  if (smem > 48 * 1024)
-    MGT_CUDA(cudaFuncSetAttribute(proj_sub_kernel<TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  proj_sub_kernel<TJ><<<grid, 256, smem, st>>>((const double2 *)V_dev, (const double2 *)H_dev, (double2 *)X_dev, len,
-                                               k, s);
+#define MGT_PSUB(T)                                                                                                \
+  do {                                                                                                             \
+    if (smem > 48 * 1024)                                                                                          \
+      MGT_CUDA(cudaFuncSetAttribute(proj_sub_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    proj_sub_kernel<T><<<grid, 256, smem, st>>>((const double2 *)V_dev, (const double2 *)H_dev, (double2 *)X_dev, \
+                                                len, k, s);                                                        \
+  } while (0)
+  if (TJ == 8)
+    MGT_PSUB(8);
+  else if (TJ == 4)
+    MGT_PSUB(4);
+  else if (TJ == 2)
+    MGT_PSUB(2);
+  else
+    MGT_PSUB(1);
+#undef MGT_PSUB
   MGT_LAUNCH_CHECK("proj_sub_kernel");
   return MGT_OK;
 }

@@ -525,41 +525,42 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
     def dot(u, v):
         return torch.sum(u.conj() * v, dim=(1, 2))
 
+    # the iteration itself (2 stencil applies, fused vector updates and
+    # reductions, device-side scalars) is one C-ABI call per step
+    pr = coarse.prolongator
+    d, bk = pr._dims()
+    if low and getattr(coarse, "_c32", None) is None:
+        coarse._c32 = coarse.C.to(torch.complex64)
+    Cm = coarse._c32 if low else coarse.C
     n = b.shape[0]
+    b = b.contiguous()
     x = torch.zeros_like(b)
     r = b.clone()
     b2 = dot(b, b).real
     tol2 = (tol * tol) * b2
     rhat = r.clone()
     p = r.clone()
+    v, s, t = torch.empty_like(b), torch.empty_like(b), torch.empty_like(b)
     rho = dot(rhat, r)
     its = np.zeros(n, dtype=int)
     mv = np.zeros(n, dtype=int)
     done = (b2 == 0).cpu().numpy().copy()
-    active = torch.as_tensor(~done, device=b.device)
+    state = torch.zeros((n, 12), dtype=torch.float64, device=b.device)
+    state[:, 0], state[:, 1] = rho.real, rho.imag
+    state[:, 9] = torch.as_tensor(~done, device=b.device, dtype=torch.float64)
+    state[:, 10] = tol2
+    lib = _lib.lib()
     for it in range(max_iter):
         if done.all():
             break
-        v = A(p)
-        sigma = dot(rhat, v)
-        alpha = torch.where(active & (sigma.abs() > 0), rho / torch.where(sigma.abs() > 0, sigma, 1), 0)
-        s = r - alpha[:, None, None] * v
-        t = A(s)
-        tt = dot(t, t).real
-        omega = torch.where(active & (tt > 0), dot(t, s) / torch.where(tt > 0, tt, 1), 0)
-        x = x + alpha[:, None, None] * p + omega[:, None, None] * s
-        r = s - omega[:, None, None] * t
-        rho_new = dot(rhat, r)
-        beta = torch.where(active & (rho.abs() > 0) & (omega.abs() > 0),
-                           (rho_new / torch.where(rho.abs() > 0, rho, 1)) * (alpha / torch.where(omega.abs() > 0, omega, 1)),
-                           0)
-        p = r + beta[:, None, None] * (p - omega[:, None, None] * v)
-        rho = rho_new
-        r2 = dot(r, r).real
-        act = active.cpu().numpy()
+        _lib.check(lib.mgt_coarse_bicgstab_iter(d, bk, nv, ptr(Cm), 1 if low else 0, float(tau), n, ptr(x), ptr(r),
+                                                ptr(rhat), ptr(p), ptr(v), ptr(s), ptr(t), ptr(state), stream_ptr()),
+                   "coarse bicgstab iteration")
+        st = state.cpu().numpy()
+        act = st[:, 9] != 0
         its[act] += 1
         mv[act] += 2
-        conv = ((r2 <= tol2) | (omega.abs() == 0) | (rho.abs() == 0)).cpu().numpy() & act
+        conv = (st[:, 11] != 0) & act
         if conv.any():
             # confirm on the explicit residual; restart the ones that drifted
             rt = b - A(x, exact=True)
@@ -569,12 +570,13 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
             done |= ok
             again = conv & ~ok
             if again.any():
-                ag = torch.as_tensor(again, device=b.device)
-                r = torch.where(ag[:, None, None], rt, r)
-                rhat = torch.where(ag[:, None, None], rt, rhat)
-                p = torch.where(ag[:, None, None], rt, p)
-                rho = torch.where(ag, dot(rt, rt), rho)
-            active = torch.as_tensor(~done, device=b.device)
+                ag = torch.as_tensor(np.flatnonzero(again), device=b.device)
+                r[ag] = rt[ag]
+                rhat[ag] = rt[ag]
+                p[ag] = rt[ag]
+                rr = dot(rt[ag], rt[ag])
+                state[ag, 0], state[ag, 1] = rr.real, rr.imag
+            state[:, 9] = torch.as_tensor(~done, device=b.device, dtype=torch.float64)
     rt = b - A(x, exact=True)
     rel = (dot(rt, rt).real / torch.where(b2 > 0, b2, 1)).sqrt().cpu().numpy()
     reps = [(int(its[i]), float(rel[i]), bool(rel[i] <= tol or float(b2[i]) == 0.0), int(mv[i] + 1))
