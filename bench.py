@@ -302,6 +302,8 @@ def run_ours(args):
             probes3 = probes_config3(M, rank, world)
             if world == 1 and not args.skip_eigen:
                 probes4 = probes_config4(M, rank, world)
+    from paper_1909_12234_b200.krylov import release_solvers
+    release_solvers()  # the 16^4 configs' cached solver workspaces
     torch.cuda.empty_cache()
     probes5 = probes_config5(M, rank, world) if not (args.skip_probes or args.skip_config5) else None
     dsolve = None

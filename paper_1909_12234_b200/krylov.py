@@ -143,6 +143,13 @@ def _solver_for(op):
     return s[1]
 
 
+def release_solvers():
+    """Drop every cached solver workspace (and its operator reference);
+    the next solve per (operator, thread) allocates afresh."""
+    with _SOLVERS_LOCK:
+        _SOLVERS.clear()
+
+
 def bicgstab_solve(op, b, config):
     """Solver plugin `callable(op, b, config) -> (x, SolveReport)`
     (krylov.py:200-229).  b: reference-layout vector (numpy or CUDA tensor)."""
@@ -188,21 +195,57 @@ class TruncatedInverse:
         self._account(rep)
         return x
 
-    def solve_native(self, b, want_dot=False):
-        """Batched native-layout application (the estimators' fast path)."""
-        solver = _solver_for(self.op)
-        xs, reps, dots = [], [], []
-        for r0 in range(0, b.shape[0], solver.max_rhs):
-            x, rr, d = solver.solve_native(b[r0:r0 + solver.max_rhs], self.config.tol,
-                                           self.config.max_iter, want_dot=want_dot,
-                                           **solve_options(self.config))
-            xs.append(x)
+    def solve_native(self, b, want_dot=False, streams=None):
+        """Batched native-layout application (the estimators' fast path).
+        More rhs than one solver call takes are split into calls that run
+        on `streams` concurrent CUDA streams (default: trace.default_streams
+        for the volume); each call's result is a pure function of its rhs,
+        so the split does not change any value."""
+        base = _base_operator(self.op)[0]
+        max_rhs = solve_batch(base.volume)
+        n = b.shape[0]
+        chunks = [(r0, min(n, r0 + max_rhs)) for r0 in range(0, n, max_rhs)]
+        if streams is None:
+            from .trace import default_streams
+            streams = default_streams(base.volume, max_rhs)
+        ns = max(1, min(int(streams), len(chunks)))
+        if threading.current_thread().name.startswith("mgt-solve"):
+            ns = 1  # already on a worker stream: never wait on the pool from inside it
+        opts = solve_options(self.config)
+        if ns == 1:
+            solver = _solver_for(self.op)  # (only the calling thread's workspace is allocated)
+            results = [solver.solve_native(b[r0:r1], self.config.tol, self.config.max_iter, want_dot=want_dot, **opts)
+                       for r0, r1 in chunks]
+            xs = [res[0] for res in results]
+            x = torch.cat(xs) if len(xs) > 1 else xs[0]
+        else:
+            from .trace import _worker_pool
+            b = b.contiguous()
+            x = torch.empty_like(b)
+            torch.cuda.current_stream().synchronize()  # b is ready for the worker streams
+            dev = torch.cuda.current_device()
+            pool, local = _worker_pool(ns)
+
+            def run(r0, r1):
+                if getattr(local, "device", None) != dev:
+                    torch.cuda.set_device(dev)
+                    local.device = dev
+                    local.stream = torch.cuda.Stream()
+                with torch.cuda.stream(local.stream):
+                    res = _solver_for(self.op).solve_native(b[r0:r1], self.config.tol, self.config.max_iter,
+                                                            x=x[r0:r1], want_dot=want_dot, **opts)
+                    local.stream.synchronize()
+                return res
+
+            futs = [pool.submit(run, r0, r1) for r0, r1 in chunks]
+            results = [f.result() for f in futs]
+        reps, dots = [], []
+        for _, rr, d in results:
             reps.extend(rr)
             if want_dot:
                 dots.append(d)
         for rep in reps:
             self._account(rep)
-        x = torch.cat(xs) if len(xs) > 1 else xs[0]
         return x, reps, (np.concatenate(dots) if want_dot else None)
 
 

@@ -152,12 +152,19 @@ def default_streams(volume, batch=4):
     sites exposes batch V/2 stencil threads per kernel; ~32 resident waves
     of 148 SMs x 384 threads in flight hide the per-kernel launch/tail gaps
     and the host-side status polls (measured on B200, tools/batch_sweep.sh:
-    16^4 best at 16 rhs x 4 streams, 8^4 at 32 rhs x 1)."""
+    16^4 best at 16 rhs x 4 streams, 8^4 at 32 rhs x 1).  Where one solve
+    already fills the GPU (32^4, 32^3 x 64) two solves still pay: one's
+    latency-bound stencil kernels overlap the other's HBM-bound vector
+    kernels (tools/streams_probe.py: +17-18 % probes/s); above 2^22 sites
+    the second workspace is not worth its memory."""
     import os
     if os.environ.get("MGT_SOLVE_STREAMS"):
         return max(1, int(os.environ["MGT_SOLVE_STREAMS"]))
     want = 32 * 148 * 384
-    return int(max(1, min(8, -(-want // (batch * max(1, volume // 2))))))
+    n = int(max(1, min(8, -(-want // (batch * max(1, volume // 2))))))
+    if n == 1 and volume <= (1 << 22):
+        n = 2
+    return n
 
 
 def group_samples_gpu(inv_op, probes, batch=None, correction=None, streams=None, deferred=None, guess=None):
@@ -414,9 +421,13 @@ def _oblique_setup(op, inv_op, pr, coarse_triplets, rank):
         ubn = pr.coarse_from_ref(ub.reshape(rank, pr.n_blocks, pr.nc))
     wu = pr.prolong_native(ubn)  # W Ubar, (r, 12, V)
     g_cols = op.apply_native(wu)  # A W Ubar
-    g5 = torch.ones(12, device=dev, dtype=torch.float64)
-    g5[6:] = -1.0
-    s_small = torch.einsum("ics,jcs->ij", wu.conj(), g5[None, :, None] * g_cols).cpu().numpy()
+    # S = (W Ubar)^H g5 (A W Ubar) with the projection kernel; g5 flips the
+    # sign of comps 6..11 in place (exact) and back, so no r-field temporary
+    from .linalg import vhx
+    g_cols[:, 6:].neg_()
+    s_small = vhx(wu, g_cols).cpu().numpy()
+    g_cols[:, 6:].neg_()
+    del wu  # r fine fields (25.8 GB at 32^3 x 64, r = 64): not needed past S
     g5c = pr.coarse_gamma5
     t_small = ubar.conj().T @ (g5c[:, None] * ubar)
     lam, uhat, t0 = factorize_small(s_small, t_small)
