@@ -132,6 +132,37 @@ def test_coarse_bicgstab_solves(gold, setup):
             assert np.linalg.norm(xr[i] - exact) / np.linalg.norm(exact) < 1e-9
 
 
+def test_coarse_bicgstab_loose_fp32_path_and_edge_cases(gold, setup):
+    """tol >= 1e-5 iterates with the fp32 copy of C (fp32 stencil
+    arithmetic, fused device-side iteration); the contract stays the
+    reference's explicit fp64 residual.  9 rhs (one 8-rhs launch + 1), one of
+    them zero; a rhs at max_iter=1 reports not converged."""
+    M, MG, geo, op, A, Pg = setup
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    C = MG.build_coarse_operator(op, pro)
+    G = gold["C_dense"]
+    g5c = gold["coarse_gamma5"]
+    rng = np.random.default_rng(9)
+    bh = rng.normal(size=(9, C.dim)) + 1j * rng.normal(size=(9, C.dim))
+    bh[4] = 0.0
+    b = pro.coarse_from_ref(torch.as_tensor(bh, device="cuda").reshape(9, pro.n_blocks, pro.nc))
+    for tol, tau in ((1e-3, 0.0), (1e-5, 0.2)):
+        x, reps = MG.coarse_bicgstab(C, b, tol, 500, tau)
+        xr = pro.coarse_to_ref(x).reshape(9, -1).cpu().numpy()
+        Gt = G + 1j * tau * np.diag(g5c)
+        for i in range(9):
+            its, rel, conv, mv = reps[i]
+            assert conv
+            if i == 4:
+                assert its == 0 and np.all(xr[i] == 0)
+                continue
+            true_rel = np.linalg.norm(bh[i] - Gt @ xr[i]) / np.linalg.norm(bh[i])
+            assert true_rel <= tol and abs(true_rel - rel) <= 1e-3 * tol
+    _, reps = MG.coarse_bicgstab(C, b[:2], 1e-12, 1, 0.0)
+    assert all(not r[2] and r[0] == 1 for r in reps)
+
+
 def test_coarse_davidson_and_rank_r_oblique_deflation(gold, setup):
     M, MG, geo, op, A, Pg = setup
     from paper_1909_12234_b200 import trace as TR
