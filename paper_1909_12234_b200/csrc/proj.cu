@@ -29,8 +29,8 @@ constexpr int warp_vecs() {
 
 // S: compile-time column capacity, s <= S the actual column count
 template <int S>
-__global__ void __launch_bounds__(256) vhx_small_kernel(const double2 *__restrict__ V, const double2 *__restrict__ X,
-                                                        int64_t len, int k, int s, double2 *__restrict__ part) {
+__global__ void __launch_bounds__(256, 2) vhx_small_kernel(const double2 *__restrict__ V, const double2 *__restrict__ X,
+                                                           int64_t len, int k, int s, double2 *__restrict__ part) {
   constexpr int kWarpVecs = warp_vecs<S>();
   constexpr int kBlockVecs = 8 * kWarpVecs;
   __shared__ double2 red[8][kWarpVecs * S];
@@ -74,25 +74,32 @@ __global__ void __launch_bounds__(256) vhx_small_kernel(const double2 *__restric
   }
 }
 
-// 64 x 64 tile of V^H X over an e-chunk range; part: [block.x][k][s]
-__global__ void __launch_bounds__(256) vhx_tile_kernel(const double2 *__restrict__ V, const double2 *__restrict__ X,
-                                                       int64_t len, int k, int s, double2 *__restrict__ part) {
-  constexpr int T = 64, E = 8;
+// 64 x TJ tile of V^H X over an e-chunk range; part: [block.x][k][s].
+// 16 x (TJ/4) threads, a 4 x 4 complex register micro-tile each; TJ follows
+// s (16, 32 or 64) so skinny column counts do not run mostly-empty tiles.
+template <int TJ>
+__global__ void __launch_bounds__(16 * (TJ / 4)) vhx_tile_kernel(const double2 *__restrict__ V,
+                                                                const double2 *__restrict__ X, int64_t len, int k,
+                                                                int s, double2 *__restrict__ part) {
+  constexpr int T = 64, E = 8, NT = 16 * (TJ / 4);
   __shared__ double2 sV[E][T + 1];
-  __shared__ double2 sX[E][T + 1];
-  const int ti = threadIdx.x / 16, tj = threadIdx.x % 16;  // 16 x 16 threads, 4 x 4 each
-  const int i0 = blockIdx.y * T, j0 = blockIdx.z * T;
+  __shared__ double2 sX[E][TJ + 1];
+  const int ti = threadIdx.x / (TJ / 4), tj = threadIdx.x % (TJ / 4);
+  const int i0 = blockIdx.y * T, j0 = blockIdx.z * TJ;
   C<double> acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = C<double>(0.0, 0.0);
   for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < len; e0 += (int64_t)gridDim.x * E) {
-    // stage: 256 threads load 64 x 8 of V and of X (2 each)
-    for (int q = threadIdx.x; q < T * E; q += 256) {
+    for (int q = threadIdx.x; q < T * E; q += NT) {
       const int r = q / E, c = q % E;
       const int64_t e = e0 + c;
       sV[c][r] = (i0 + r < k && e < len) ? V[(int64_t)(i0 + r) * len + e] : make_double2(0.0, 0.0);
+    }
+    for (int q = threadIdx.x; q < TJ * E; q += NT) {
+      const int r = q / E, c = q % E;
+      const int64_t e = e0 + c;
       sX[c][r] = (j0 + r < s && e < len) ? X[(int64_t)(j0 + r) * len + e] : make_double2(0.0, 0.0);
     }
     __syncthreads();
@@ -228,11 +235,19 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
 #undef MGT_VHX
     MGT_LAUNCH_CHECK("vhx_small_kernel");
   } else {
-    const int gy = (k + 63) / 64, gz = (s + 63) / 64;
-    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, (int64_t)kNumSMs * 4 / (gy * gz) + 1));
+    const int tj = s <= 16 ? 16 : (s <= 32 ? 32 : 64);
+    const int gy = (k + 63) / 64, gz = (s + tj - 1) / tj;
+    // ~16 resident 64-thread tiles (4 of 256 threads) per SM
+    const int per_sm = 4 * 64 / tj;
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, (int64_t)kNumSMs * per_sm / (gy * gz) + 1));
     MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy, gz);
-    vhx_tile_kernel<<<grid, 256, 0, st>>>(V, X, len, k, s, part);
+    if (tj == 16)
+      vhx_tile_kernel<16><<<grid, 64, 0, st>>>(V, X, len, k, s, part);
+    else if (tj == 32)
+      vhx_tile_kernel<32><<<grid, 128, 0, st>>>(V, X, len, k, s, part);
+    else
+      vhx_tile_kernel<64><<<grid, 256, 0, st>>>(V, X, len, k, s, part);
     MGT_LAUNCH_CHECK("vhx_tile_kernel");
   }
   // the reduction reads part as [blk][rows][cols]: swapped, rows = s and cols = k
