@@ -550,9 +550,12 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
     state[:, 9] = torch.as_tensor(~done, device=b.device, dtype=torch.float64)
     state[:, 10] = tol2
     lib = _lib.lib()
+    tol2_h = tol2.cpu().numpy()
+    rt = None  # explicit residual of the current x (valid until the next step)
     for it in range(max_iter):
         if done.all():
             break
+        rt = None
         _lib.check(lib.mgt_coarse_bicgstab_iter(d, bk, nv, ptr(Cm), 1 if low else 0, float(tau), n, ptr(x), ptr(r),
                                                 ptr(rhat), ptr(p), ptr(v), ptr(s), ptr(t), ptr(state), stream_ptr()),
                    "coarse bicgstab iteration")
@@ -566,7 +569,7 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
             rt = b - A(x, exact=True)
             mv[act] += 1
             rt2 = dot(rt, rt).real.cpu().numpy()
-            ok = conv & (rt2 <= tol2.cpu().numpy())
+            ok = conv & (rt2 <= tol2_h)
             done |= ok
             again = conv & ~ok
             if again.any():
@@ -577,7 +580,8 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
                 rr = dot(rt[ag], rt[ag])
                 state[ag, 0], state[ag, 1] = rr.real, rr.imag
             state[:, 9] = torch.as_tensor(~done, device=b.device, dtype=torch.float64)
-    rt = b - A(x, exact=True)
+    if rt is None:  # (else: the last confirmation already holds b - A x for this x)
+        rt = b - A(x, exact=True)
     rel = (dot(rt, rt).real / torch.where(b2 > 0, b2, 1)).sqrt().cpu().numpy()
     reps = [(int(its[i]), float(rel[i]), bool(rel[i] <= tol or float(b2[i]) == 0.0), int(mv[i] + 1))
             for i in range(n)]
