@@ -659,8 +659,8 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_rhs(BiEo X, LinkField<doub
 
 // first half of S: tmp = Dg^-1 H_oe (G_in f), f = p / s / x (mode 0: rhs
 // still iterating, mode 1: rhs whose true residual is due)
-template <int NR, int RECON, typename R = double>
-__global__ void __launch_bounds__(kRedBlock, eo_minb<R>()) bi_eo_first(BiEo X, LinkField<R, RECON> le,
+template <int NR, int RECON, typename R = double, int MINB = eo_minb<R>()>
+__global__ void __launch_bounds__(kRedBlock, MINB) bi_eo_first(BiEo X, LinkField<R, RECON> le,
                                                             LinkField<R, RECON> lo, const cplx<R> *f, BiWST<R> w_,
                                                             int mode) {
   const BiWST<R> w = w_.at(blockIdx.y);
@@ -689,8 +689,8 @@ __global__ void __launch_bounds__(kRedBlock, eo_minb<R>()) bi_eo_first(BiEo X, L
 }
 
 // K1 (eo): v = S p = G_out [ Dg G_in p - 1/4 H_eo tmp ] ; sigma = (rhat, v)
-template <int NR, int RECON, typename R = double>
-__global__ void __launch_bounds__(kRedBlock, eo_minb<R>()) bi_k1_eo(BiEo X, LinkField<R, RECON> le,
+template <int NR, int RECON, typename R = double, int MINB = eo_minb<R>()>
+__global__ void __launch_bounds__(kRedBlock, MINB) bi_k1_eo(BiEo X, LinkField<R, RECON> le,
                                                          LinkField<R, RECON> lo, BiWST<R> w_) {
   const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
@@ -722,8 +722,8 @@ __global__ void __launch_bounds__(kRedBlock, eo_minb<R>()) bi_k1_eo(BiEo X, Link
 }
 
 // K3 (eo): t = S s ; (t, s), |t|^2
-template <int NR, int RECON, typename R = double>
-__global__ void __launch_bounds__(kRedBlock, eo_minb<R>()) bi_k3_eo(BiEo X, LinkField<R, RECON> le,
+template <int NR, int RECON, typename R = double, int MINB = eo_minb<R>()>
+__global__ void __launch_bounds__(kRedBlock, MINB) bi_k3_eo(BiEo X, LinkField<R, RECON> le,
                                                          LinkField<R, RECON> lo, BiWST<R> w_) {
   const BiWST<R> w = w_.at(blockIdx.y);
   if (!any_status<NR>(w.st, ST_RUN)) return;
@@ -959,16 +959,16 @@ static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &l
   return MGT_OK;
 }
 
-template <int NR, int RECON, typename R = double>
+template <int NR, int RECON, typename R = double, int MINB = eo_minb<R>()>
 static int launch_chunk_eo(const BiEo &X, const LinkField<R, RECON> &le, const LinkField<R, RECON> &lo,
                            const BiWST<R> &w, dim3 gd, dim3 g1, dim3 grid, cudaStream_t st) {
   const int64_t Vh = X.E.Vh;
   for (int it = 0; it < kChunk; ++it) {
-    bi_eo_first<NR, RECON, R><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
-    bi_k1_eo<NR, RECON, R><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    bi_eo_first<NR, RECON, R, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
+    bi_k1_eo<NR, RECON, R, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
     bi_k2<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
-    bi_eo_first<NR, RECON, R><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w, 0);
-    bi_k3_eo<NR, RECON, R><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    bi_eo_first<NR, RECON, R, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w, 0);
+    bi_k3_eo<NR, RECON, R, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
     bi_k4<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
     bi_k5<NR, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
   }
@@ -1237,7 +1237,12 @@ __global__ void mx_next(BiWS w_, int cycle, int max_cycles) {
   }
 }
 
-template <int NR, int RECON>
+// MINB32: resident blocks per SM of the fp32 stencil kernels (their launch
+// bounds).  Small lattices run at 4 (128 registers, 16 warps/SM: at 8^4 the
+// 2,048 rhs-warps of a 32-rhs stencil pass fit one wave instead of 1.15;
+// config-1 probes/s +10 %); large ones at 3 (168 registers, no spills, the
+// better choice once the pass is many waves long).
+template <int NR, int RECON, int MINB32 = eo_minb<float>()>
 static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b,
                              double2 *x, char *ws, const WSLayout &Lw, double tol, int max_iter, int64_t *report,
                              double *relres, double *dot_out, int G, cudaStream_t st) {
@@ -1264,8 +1269,8 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
   if (!g_str) g_str = resident_grid(bi_k4<NR>, kRedBlock, (int64_t)1 << 40);
   if (!g_e1) g_e1 = resident_grid(bi_eo_first<NR, RECON>, kRedBlock, (int64_t)1 << 40);
   if (!g_e2) g_e2 = resident_grid(bi_k1_eo<NR, RECON>, kRedBlock, (int64_t)1 << 40);
-  if (!g_f1) g_f1 = resident_grid(bi_eo_first<NR, R32, float>, kRedBlock, (int64_t)1 << 40);
-  if (!g_f2) g_f2 = resident_grid(bi_k1_eo<NR, R32, float>, kRedBlock, (int64_t)1 << 40);
+  if (!g_f1) g_f1 = resident_grid(bi_eo_first<NR, R32, float, MINB32>, kRedBlock, (int64_t)1 << 40);
+  if (!g_f2) g_f2 = resident_grid(bi_k1_eo<NR, R32, float, MINB32>, kRedBlock, (int64_t)1 << 40);
   const int64_t need = (Vs + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
   auto per_group = [&](int resident) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, std::max(1, resident / G)));
@@ -1292,7 +1297,7 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
       MGT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
       cudaGraph_t graph;
       MGT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-      launch_chunk_eo<NR, R32, float>(X, le32, lo32, w32, fd, f1, grid, cap);
+      launch_chunk_eo<NR, R32, float, MINB32>(X, le32, lo32, w32, fd, f1, grid, cap);
       cudaError_t e = cudaStreamEndCapture(cap, &graph);
       cudaStreamDestroy(cap);
       if (e != cudaSuccess) return cuda_fail(e, "mixed bicgstab graph capture");
@@ -1364,6 +1369,20 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
       }
     }
   return MGT_OK;
+}
+
+// small lattices (at most 2^13 sites per parity: 8^4, 8^3 x 16) take the
+// 4-blocks-per-SM fp32 stencils
+constexpr int64_t kSmallMixedVh = 8192;
+template <int NR, int RECON>
+static int solve_group_mixed_any(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b,
+                                 double2 *x, char *ws, const WSLayout &Lw, double tol, int max_iter,
+                                 int64_t *report, double *relres, double *dot_out, int G, cudaStream_t st) {
+  if (h->g.V / 2 <= kSmallMixedVh)
+    return solve_group_mixed<NR, RECON, 4>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report, relres, dot_out,
+                                           G, st);
+  return solve_group_mixed<NR, RECON>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report, relres, dot_out, G,
+                                      st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1561,10 +1580,10 @@ static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, i
     char *ws = (char *)workspace_dev;
     int rc;
 #define MGT_SOLVE(NR, GG)                                                                                       \
-  (mixed ? (h->recon == 18 ? solve_group_mixed<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter,          \
-                                                       report_out + 4 * r0, relres_out + r0, dot, GG, st)      \
-                           : solve_group_mixed<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter,          \
-                                                       report_out + 4 * r0, relres_out + r0, dot, GG, st))     \
+  (mixed ? (h->recon == 18 ? solve_group_mixed_any<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter,      \
+                                                           report_out + 4 * r0, relres_out + r0, dot, GG, st)  \
+                           : solve_group_mixed_any<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter,      \
+                                                           report_out + 4 * r0, relres_out + r0, dot, GG, st)) \
    : (h->recon == 18 ? solve_group<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,  \
                                             relres_out + r0, dot, eo, GG, st)                                    \
                      : solve_group<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,  \
