@@ -92,15 +92,13 @@ __global__ void __launch_bounds__(16 * (TJ / 4)) vhx_tile_kernel(const double2 *
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = C<double>(0.0, 0.0);
   for (int64_t e0 = (int64_t)blockIdx.x * E; e0 < len; e0 += (int64_t)gridDim.x * E) {
+    // one staging loop for both tiles (their loads in flight together)
     for (int q = threadIdx.x; q < T * E; q += NT) {
       const int r = q / E, c = q % E;
       const int64_t e = e0 + c;
-      sV[c][r] = (i0 + r < k && e < len) ? V[(int64_t)(i0 + r) * len + e] : make_double2(0.0, 0.0);
-    }
-    for (int q = threadIdx.x; q < TJ * E; q += NT) {
-      const int r = q / E, c = q % E;
-      const int64_t e = e0 + c;
-      sX[c][r] = (j0 + r < s && e < len) ? X[(int64_t)(j0 + r) * len + e] : make_double2(0.0, 0.0);
+      const double2 vv = (i0 + r < k && e < len) ? V[(int64_t)(i0 + r) * len + e] : make_double2(0.0, 0.0);
+      if (r < TJ) sX[c][r] = (j0 + r < s && e < len) ? X[(int64_t)(j0 + r) * len + e] : make_double2(0.0, 0.0);
+      sV[c][r] = vv;
     }
     __syncthreads();
 #pragma unroll

@@ -14,13 +14,27 @@ def _flat(t):
     return t, t.reshape(t.shape[0], -1).shape[1]
 
 
-def vhx(V, X):
-    """H = V^H X, shape (k, s)."""
+# From this many columns (with more than 8 vectors) V^H X is a plain
+# GEMM: cuBLAS ZGEMM on the FP64 tensor cores (DMMA: fp64 products, so the
+# fp64 tolerance holds) beats the FP64-pipe tile kernel 1.6-2.8x
+# (tools/proj_probe.py: k = 64, s = 32 / 128: 0.82 vs 1.35 ms, 1.74 vs
+# 4.82 ms); below it the projection kernels win (s <= 16: they stream V at
+# up to 70 % of HBM).
+GEMM_MIN_COLS = 32
+
+
+def vhx(V, X, gemm=None):
+    """H = V^H X, shape (k, s).  gemm: None = by shape (cuBLAS for k > 8,
+    s >= GEMM_MIN_COLS), False = always the projection kernels (C ABI)."""
     V, n = _flat(V)
     X, n2 = _flat(X)
     if n != n2:
         raise ValueError(f"dimension mismatch: {n} != {n2}")
     k, s = V.shape[0], X.shape[0]
+    if gemm is None:
+        gemm = k > 8 and s >= GEMM_MIN_COLS
+    if gemm:
+        return V.reshape(k, n).conj() @ X.reshape(s, n).transpose(0, 1)
     H = torch.empty((s, k), dtype=torch.complex128, device=V.device)  # column major k x s
     _lib.check(_lib.lib().mgt_proj_vhx(ptr(V), ptr(X), n, k, s, ptr(H), stream_ptr()), "proj_vhx")
     return H.transpose(0, 1)

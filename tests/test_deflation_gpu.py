@@ -30,7 +30,8 @@ def setup(gold):
 
 
 @pytest.mark.parametrize("k,s,n", [(64, 1, 49152), (64, 4, 49152), (64, 128, 20000), (5, 3, 1001), (70, 9, 777),
-                                   (208, 8, 49152), (70, 6, 777), (8, 136, 49152), (3, 20, 1001), (1, 9, 513)])
+                                   (208, 8, 49152), (70, 6, 777), (8, 136, 49152), (3, 20, 1001), (1, 9, 513),
+                                   (64, 16, 49152), (144, 16, 7777), (40, 32, 3001), (64, 33, 2049)])
 def test_projection_kernels_vs_numpy(cuda, k, s, n):
     from paper_1909_12234_b200 import linalg as LA
     rng = np.random.default_rng(k + s)
@@ -40,6 +41,11 @@ def test_projection_kernels_vs_numpy(cuda, k, s, n):
     H = LA.vhx(Vd, Xd).cpu().numpy()
     Hr = V.conj() @ X.T
     assert np.linalg.norm(H - Hr) / np.linalg.norm(Hr) < 1e-13
+    # the C-ABI projection kernels themselves at every shape (vhx hands
+    # k > 8, s >= 32 to cuBLAS by default); deterministic
+    Hk = LA.vhx(Vd, Xd, gemm=False)
+    assert np.linalg.norm(Hk.cpu().numpy() - Hr) / np.linalg.norm(Hr) < 1e-13
+    assert torch.equal(Hk, LA.vhx(Vd, Xd, gemm=False))
     LA.sub_vh(Vd, torch.as_tensor(Hr, device=cuda), Xd)
     Xr = X - (V.T @ Hr).T
     assert np.linalg.norm(Xd.cpu().numpy() - Xr) / np.linalg.norm(Xr) < 1e-13

@@ -18,7 +18,7 @@ def main():
     n = 12 * 16 ** 4
     for k in (64, 144):
         V = torch.randn((k, n), dtype=torch.complex128, device="cuda")
-        for s in (1, 2, 4, 8, 16):
+        for s in ((1, 2, 4, 8, 16, 32, 128) if k == 64 else (1, 8, 16)):
             X = torch.randn((s, n), dtype=torch.complex128, device="cuda")
             t = timeit(lambda: LA.vhx(V, X), steps=20)
             b = 16 * n * (k + s)
