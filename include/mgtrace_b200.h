@@ -239,6 +239,18 @@ size_t mgt_gcr_workspace_bytes(mgt_wilson_t h, int m);
 int mgt_gcr_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m,
                   int max_iter, double tol, void *workspace_dev,
                   int64_t *report_out, double *relres_out, void *stream);
+/* Restarted GMRES(m) from x0 = 0 on the operator variant (flags, tau) of
+ * mgt_wilson_apply: Arnoldi (modified Gram-Schmidt) on the device, Givens /
+ * least squares on the host, explicit residual b - A x between cycles and
+ * as the stopping test (the reference's contract, krylov.py:78-85, 113-118;
+ * the north star's GPU-resident "BiCGStab/GMRES", SURVEY 8(b) solve_gmres).
+ * max_iter counts Arnoldi steps over all cycles; report as above
+ * (reason 2 = Arnoldi breakdown before convergence). */
+size_t mgt_gmres_workspace_bytes(mgt_wilson_t h, int m);
+int mgt_gmres_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m,
+                    int max_iter, double tol, int flags, double tau,
+                    void *workspace_dev, int64_t *report_out,
+                    double *relres_out, void *stream);
 
 /* ---- probes -------------------------------------------------------------- */
 /* Bit-exact numpy PCG64 noise (probing.py:94-107): field j of n_fields is

@@ -1,4 +1,6 @@
-// Restarted GCR(m) on the GPU (reference: gcr_solve, krylov.py:52-118) -- the
+// Restarted GCR(m) and GMRES(m) on the GPU.
+//
+// GCR(m) (reference: gcr_solve, krylov.py:52-118) -- the
 // relaxation used by generate_null_vectors (multigrid.py:87-95, with
 // restart = max_iter) and the GCR smoother (krylov.py:236-252).
 //
@@ -9,6 +11,7 @@
 // path, not the per-probe hot loop).  Modified Gram-Schmidt against the
 // stored (z_j, q_j) pairs, in the reference's order.
 #include <cmath>
+#include <complex>
 #include <vector>
 
 #include "handle.cuh"
@@ -180,6 +183,146 @@ int mgt_gcr_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m, int max
   rel = rn / bn;
   const bool ok = rel <= tol;
   report_out[0] = it, report_out[1] = matvecs, report_out[2] = ok ? 1 : 0, report_out[3] = ok ? 0 : reason;
+  relres_out[0] = rel;
+  return MGT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Restarted GMRES(m) (the north star's "BiCGStab/GMRES"; SURVEY 8(b)
+// solve_gmres): Arnoldi with modified Gram-Schmidt on the device (fp64
+// dot/axpy kernels), Givens rotations and the (m+1) x m least-squares
+// problem on the host, x += V y at the end of each cycle, then the
+// explicit residual b - A x restarts the next cycle -- the same
+// explicit-residual contract (||b - A x|| <= tol ||b||) as gcr_solve.
+// Operator variant by flags / tau as mgt_wilson_apply.  Breakdown: the
+// Arnoldi vector vanishes (||w|| <= 1e-14 ||A v_j||) before convergence.
+size_t mgt_gmres_workspace_bytes(mgt_wilson_t h, int m) {
+  if (!h || m < 1) return 0;
+  return (size_t)(m + 3) * 12 * h->g.V * sizeof(double2) + 256;
+}
+
+int mgt_gmres_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m, int max_iter, double tol, int flags,
+                    double tau, void *workspace_dev, int64_t *report_out, double *relres_out, void *stream) {
+  if (!h || !b_dev || !x_dev || !workspace_dev || !report_out || !relres_out)
+    return fail(MGT_ERR_INVALID, "mgt_gmres_solve: null argument");
+  if (h->prec != 64) return fail(MGT_ERR_INVALID, "mgt_gmres_solve: needs a complex128 operator");
+  if (m < 1 || max_iter < 1) return fail(MGT_ERR_INVALID, "mgt_gmres_solve: restart and max_iter must be >= 1");
+  Gcr g;
+  g.h = h;
+  g.st = as_stream(stream);
+  g.n = 12 * h->g.V;
+  const double2 *b = (const double2 *)b_dev;
+  double2 *x = (double2 *)x_dev;
+  double2 *base = (double2 *)workspace_dev;
+  double2 *r = base, *w = base + g.n, *Vb = base + 2 * g.n;  // Vb: m + 1 basis vectors
+  g.dbuf = (double *)(Vb + (size_t)(m + 1) * g.n);
+  static thread_local double *hb = nullptr;
+  if (!hb) MGT_CUDA(cudaMallocHost((void **)&hb, 4 * sizeof(double)));
+  g.hbuf = hb;
+  const int64_t nb = g.n * sizeof(double2);
+  auto apply = [&](const double2 *in, double2 *out) { return wilson_apply_native(h, in, out, 1, flags, tau, g.st); };
+  auto resid = [&]() -> int {  // r = b - A x
+    int rc = apply(x, w);
+    if (rc) return rc;
+    sub_kernel<<<grid_for(g.n, 256, 8), 256, 0, g.st>>>(g.n, b, w, r);
+    MGT_LAUNCH_CHECK("sub_kernel");
+    return MGT_OK;
+  };
+  using cd = std::complex<double>;
+  int rc;
+  int64_t matvecs = 0;
+  double bn;
+  if ((rc = g.norm(b, bn))) return rc;
+  MGT_CUDA(cudaMemsetAsync(x, 0, nb, g.st));
+  if (bn == 0.0) {
+    report_out[0] = 0, report_out[1] = 0, report_out[2] = 1, report_out[3] = 0;
+    relres_out[0] = 0.0;
+    return MGT_OK;
+  }
+  MGT_CUDA(cudaMemcpyAsync(r, b, nb, cudaMemcpyDeviceToDevice, g.st));
+  double beta = bn, rel = 1.0;
+  int it = 0, reason = 1;  // 1 max_iter, 2 breakdown
+  std::vector<cd> H((size_t)(m + 1) * m), gv(m + 1), cs(m), sn(m), y(m);
+  auto Hij = [&](int i, int j) -> cd & { return H[(size_t)j * (m + 1) + i]; };
+  bool broke = false;
+  while (it < max_iter && !broke) {
+    // v_0 = r / beta
+    MGT_CUDA(cudaMemcpyAsync(Vb, r, nb, cudaMemcpyDeviceToDevice, g.st));
+    scale2_kernel<<<grid_for(g.n, 256, 8), 256, 0, g.st>>>(g.n, 1.0 / beta, Vb, r);  // (r scaled too; rebuilt below)
+    MGT_LAUNCH_CHECK("scale2_kernel");
+    std::fill(gv.begin(), gv.end(), cd(0.0));
+    gv[0] = cd(beta);
+    int k = 0;
+    for (int j = 0; j < m && it < max_iter; ++j) {
+      double2 *vj = Vb + (size_t)j * g.n;
+      if ((rc = apply(vj, w))) return rc;
+      ++matvecs;
+      double w0;
+      if ((rc = g.norm(w, w0))) return rc;
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+        C<double> hij;
+        const double2 *vi = Vb + (size_t)i * g.n;
+        if ((rc = g.dot(vi, w, hij))) return rc;
+        Hij(i, j) = cd(hij.re, hij.im);
+        if ((rc = g.axpy2(C<double>(-hij.re, -hij.im), vi, w))) return rc;
+      }
+      double hn;
+      if ((rc = g.norm(w, hn))) return rc;
+      Hij(j + 1, j) = cd(hn);
+      for (int i = 0; i < j; ++i) {  // previous rotations
+        const cd a = Hij(i, j), c2 = Hij(i + 1, j);
+        Hij(i, j) = std::conj(cs[i]) * a + std::conj(sn[i]) * c2;
+        Hij(i + 1, j) = -sn[i] * a + cs[i] * c2;
+      }
+      const cd a = Hij(j, j), c2 = Hij(j + 1, j);
+      const double den = std::sqrt(std::norm(a) + std::norm(c2));
+      if (den == 0.0) {
+        cs[j] = cd(1.0), sn[j] = cd(0.0);
+      } else {
+        cs[j] = a / den;
+        sn[j] = c2 / den;
+      }
+      Hij(j, j) = std::conj(cs[j]) * a + std::conj(sn[j]) * c2;
+      Hij(j + 1, j) = cd(0.0);
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = std::conj(cs[j]) * gv[j];
+      ++it;
+      k = j + 1;
+      rel = std::abs(gv[j + 1]) / bn;
+      if (hn <= 1e-14 * std::max(w0, 1e-300)) {  // invariant subspace / breakdown
+        broke = rel > tol;
+        break;
+      }
+      if (rel <= tol) break;
+      if (j + 1 < m) {
+        double2 *vn = Vb + (size_t)(j + 1) * g.n;
+        MGT_CUDA(cudaMemcpyAsync(vn, w, nb, cudaMemcpyDeviceToDevice, g.st));
+        scale2_kernel<<<grid_for(g.n, 256, 8), 256, 0, g.st>>>(g.n, 1.0 / hn, vn, w);
+        MGT_LAUNCH_CHECK("scale2_kernel");
+      }
+    }
+    // y = R^-1 g ; x += V y
+    for (int i = k - 1; i >= 0; --i) {
+      cd t = gv[i];
+      for (int l = i + 1; l < k; ++l) t -= Hij(i, l) * y[l];
+      y[i] = Hij(i, i) == cd(0.0) ? cd(0.0) : t / Hij(i, i);
+    }
+    for (int i = 0; i < k; ++i)
+      if ((rc = g.axpy2(C<double>(y[i].real(), y[i].imag()), Vb + (size_t)i * g.n, x))) return rc;
+    if ((rc = resid())) return rc;
+    ++matvecs;
+    double rn;
+    if ((rc = g.norm(r, rn))) return rc;
+    rel = rn / bn;
+    beta = rn;
+    if (rel <= tol) {
+      report_out[0] = it, report_out[1] = matvecs, report_out[2] = 1, report_out[3] = 0;
+      relres_out[0] = rel;
+      return MGT_OK;
+    }
+    if (broke) reason = 2;
+  }
+  report_out[0] = it, report_out[1] = matvecs, report_out[2] = 0, report_out[3] = reason;
   relres_out[0] = rel;
   return MGT_OK;
 }

@@ -32,7 +32,7 @@ class SolveConfig:
     tol: float = 1e-8
     max_iter: int = 2000
     restart: int = 32
-    kind: str = "bicgstab"  # bicgstab (GPU default) | gcr
+    kind: str = "bicgstab"  # bicgstab (GPU default) | gmres (restarted GMRES(restart)) | gcr (GCR(restart))
     # BiCGStab on the even-odd Schur complement (same full-residual stopping
     # test; about half the iterations).  False solves the full system.
     even_odd: bool = True
@@ -47,6 +47,8 @@ class SolveConfig:
             raise ValueError(f"tol must be in (0,1), got {self.tol}")
         if self.max_iter < 1:
             raise ValueError("max_iter must be >= 1")
+        if self.kind not in ("bicgstab", "gmres", "gcr"):
+            raise ValueError(f"unknown solver kind {self.kind!r}")
 
 
 @dataclass
@@ -150,6 +152,45 @@ def release_solvers():
         _SOLVERS.clear()
 
 
+_KRYLOV_WS = {}
+
+
+def restarted_solve_native(op, b, config, want_dot=False):
+    """GMRES(restart) / GCR(restart) on native fields b (n, 12, V), one rhs
+    at a time (C ABI `mgt_gmres_solve` / `mgt_gcr_solve`; zero start,
+    explicit-residual stopping test as krylov.py:78-85, 113-118).  Returns
+    (x, [SolveReport], dots or None) like BiCGStab.solve_native."""
+    base, flags, tau = _base_operator(op)
+    kind, m = config.kind, int(config.restart)
+    if kind == "gcr" and (flags or tau):
+        raise ValueError("the GPU GCR solves the plain operator only (use kind='gmres' for forms of it)")
+    key = (id(base), kind, m, threading.get_ident())  # one workspace per host thread (concurrent streams)
+    ws = _KRYLOV_WS.get(key)
+    if ws is None or ws[0] is not base:
+        fn = _lib.lib().mgt_gmres_workspace_bytes if kind == "gmres" else _lib.lib().mgt_gcr_workspace_bytes
+        ws = (base, torch.empty(int(fn(base.handle, m)), dtype=torch.uint8, device=device()))
+        _KRYLOV_WS[key] = ws
+    b = b.contiguous()
+    x = torch.empty_like(b)
+    reports, dots = [], []
+    for r in range(b.shape[0]):
+        rep = (ct.c_int64 * 4)()
+        rel = (ct.c_double * 1)()
+        if kind == "gmres":
+            rc = _lib.lib().mgt_gmres_solve(base.handle, ptr(b[r]), ptr(x[r]), m, int(config.max_iter),
+                                            float(config.tol), int(flags), float(tau), ptr(ws[1]), rep, rel,
+                                            stream_ptr())
+        else:
+            rc = _lib.lib().mgt_gcr_solve(base.handle, ptr(b[r]), ptr(x[r]), m, int(config.max_iter),
+                                          float(config.tol), ptr(ws[1]), rep, rel, stream_ptr())
+        _lib.check(rc, kind)
+        it, mv, conv, reason = (int(v) for v in rep)
+        reports.append(SolveReport(it, float(rel[0]), bool(conv), mv, "" if conv else REASONS.get(reason, "max_iter")))
+        if want_dot:
+            dots.append(complex(torch.vdot(b[r].reshape(-1), x[r].reshape(-1)).item()))
+    return x, reports, (np.array(dots) if want_dot else None)
+
+
 def bicgstab_solve(op, b, config):
     """Solver plugin `callable(op, b, config) -> (x, SolveReport)`
     (krylov.py:200-229).  b: reference-layout vector (numpy or CUDA tensor)."""
@@ -158,9 +199,12 @@ def bicgstab_solve(op, b, config):
     bd = to_device_c128(b)
     if bd.shape[0] != base.dim:
         raise ValueError(f"dimension mismatch: {bd.shape[0]} != {base.dim}")
-    solver = _solver_for(op)
     bn = base.to_native(bd.unsqueeze(0))
-    x, reps, _ = solver.solve_native(bn, config.tol, config.max_iter, **solve_options(config))
+    if getattr(config, "kind", "bicgstab") != "bicgstab":
+        x, reps, _ = restarted_solve_native(op, bn, config)
+    else:
+        solver = _solver_for(op)
+        x, reps, _ = solver.solve_native(bn, config.tol, config.max_iter, **solve_options(config))
     xr = base.from_native(x)[0]
     return (xr.cpu().numpy() if host else xr), reps[0]
 
@@ -201,6 +245,11 @@ class TruncatedInverse:
         on `streams` concurrent CUDA streams (default: trace.default_streams
         for the volume); each call's result is a pure function of its rhs,
         so the split does not change any value."""
+        if getattr(self.config, "kind", "bicgstab") != "bicgstab":
+            x, reps, dots = restarted_solve_native(self.op, b, self.config, want_dot=want_dot)
+            for rep in reps:
+                self._account(rep)
+            return x, reps, dots
         base = _base_operator(self.op)[0]
         max_rhs = solve_batch(base.volume)
         n = b.shape[0]

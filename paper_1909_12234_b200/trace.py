@@ -91,12 +91,22 @@ def _solve_batches_concurrently(inv_op, probes, batches, correction, streams, gu
     absolute residual bound tol ||z||) and post(e) gives the slots' values."""
     import torch
 
-    from .krylov import _solver_for, solve_options
+    import dataclasses
+
+    from .krylov import _solver_for, restarted_solve_native, solve_options
+
+    restarted = getattr(inv_op.config, "kind", "bicgstab") != "bicgstab"
+
+    class _Restarted:  # SolveConfig.kind = gmres / gcr: the restarted C-ABI solvers, one rhs at a time
+        @staticmethod
+        def solve_native(b, tol, max_iter, want_dot=False, **_):
+            cfg = dataclasses.replace(inv_op.config, tol=tol, max_iter=max_iter)
+            return restarted_solve_native(inv_op.op, b, cfg, want_dot=want_dot)
 
     def work(j0, j1, stream):
         with torch.cuda.stream(stream):
             z = probes.noise_native(j0, j1)
-            solver = _solver_for(inv_op.op)
+            solver = _Restarted if restarted else _solver_for(inv_op.op)
             tol = inv_op.config.tol
             if guess is not None:
                 r0, post = guess(j0, z)

@@ -207,3 +207,61 @@ def test_mixed_hutchinson_within_tolerance(cuda):
     exact = np.array([np.vdot(z, lu.solve(z)) for z in
                       (P.rademacher_numpy(op.dim, 23 + j) for j in range(s))])
     assert np.max(np.abs(est.samples - exact) / np.abs(exact)) < 1e-9
+
+
+@pytest.mark.parametrize("restart", [8, 32])
+def test_gmres_exact_solution_and_contract(cuda, restart):
+    """Restarted GMRES(m) (C ABI mgt_gmres_solve): explicit residual within
+    tol, x vs the oracle's sparse LU, counters (one matvec per Arnoldi step
+    plus one explicit residual per cycle)."""
+    M, geo, op, A = _setup((4, 4, 4, 8))
+    rng = np.random.default_rng(11)
+    b = rng.normal(size=op.dim) + 1j * rng.normal(size=op.dim)
+    cfg = M.SolveConfig(tol=1e-10, kind="gmres", restart=restart)
+    x, rep = M.bicgstab_solve(op, b, cfg)
+    assert rep.converged and rep.final_relres <= 1e-10
+    assert np.linalg.norm(b - A @ x) <= 1.01e-10 * np.linalg.norm(b)
+    xe = spla.spsolve(A.tocsc(), b)
+    assert np.linalg.norm(x - xe) / np.linalg.norm(xe) < 1e-8
+    cycles = -(-rep.iterations // restart)
+    assert rep.matvecs == rep.iterations + cycles
+
+
+@pytest.mark.parametrize("flags,tau", [(0, 0.5), (3, -0.2), (4, 0.0)])
+def test_gmres_operator_variants(cuda, flags, tau):
+    from paper_1909_12234_b200.lattice import FormOperator
+    M, geo, op, A = _setup((4, 4, 4, 8), eps=0.3)
+    form = FormOperator(op, flags, tau, "t")
+    rng = np.random.default_rng(12)
+    b = rng.normal(size=op.dim) + 1j * rng.normal(size=op.dim)
+    x, rep = M.bicgstab_solve(form, b, M.SolveConfig(tol=1e-10, kind="gmres", restart=16))
+    assert rep.converged
+    assert np.linalg.norm(b - form.apply(x)) <= 1.01e-10 * np.linalg.norm(b)
+
+
+def test_gmres_and_gcr_edge_cases_and_estimator(cuda):
+    """zero rhs, max_iter, the GCR kind, and Hutchinson through
+    TruncatedInverse(kind='gmres') vs the exact quadratic forms."""
+    import torch
+    M, geo, op, A = _setup((4, 4, 4, 4))
+    x, rep = M.bicgstab_solve(op, np.zeros(op.dim, dtype=complex), M.SolveConfig(kind="gmres"))
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+    b = np.ones(op.dim, dtype=complex)
+    x, rep = M.bicgstab_solve(op, b, M.SolveConfig(tol=1e-14, max_iter=5, kind="gmres", restart=4))
+    assert not rep.converged and rep.reason == "max_iter" and rep.iterations == 5
+    x, rep = M.bicgstab_solve(op, b, M.SolveConfig(tol=1e-10, kind="gcr", restart=16))
+    assert rep.converged and np.linalg.norm(b - A @ x) <= 1.01e-10 * np.linalg.norm(b)
+    with pytest.raises(ValueError):
+        M.SolveConfig(kind="cg")
+    inv = M.TruncatedInverse(op, M.SolveConfig(tol=1e-10, kind="gmres", restart=16))
+    probes = M.build_probe_set(geo, 12, 3, hp_count=1, dilution=False, kind="rademacher", seed=5)
+    est = M.hutchinson(inv, probes)
+    lu = spla.splu(A.tocsc())
+    for j, s in enumerate(est.samples):
+        z = P.rademacher_numpy(op.dim, 5 + j)
+        q = np.vdot(z, lu.solve(z.astype(complex)))
+        assert abs(s - q) <= 1e-8 * abs(q)
+    assert inv.n_solves == 3 and inv.n_failed == 0
+    zn = op.to_native(torch.as_tensor(np.stack([P.rademacher_numpy(op.dim, 5)])).cuda())
+    xb, reps, dq = inv.solve_native(zn, want_dot=True)
+    assert reps[0].converged and abs(dq[0] - est.samples[0]) <= 1e-9 * abs(est.samples[0])
