@@ -110,6 +110,15 @@ int mgt_wilson_info(mgt_wilson_t h, int dims[4], int *prec, int *recon,
 int mgt_wilson_apply(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rhs,
                      int flags, double tau, void *stream);
 
+/* Fused y = A' x and dot_out[2r..2r+1] = vdot(u_r, y_r) (re, im; device
+ * doubles) for n_rhs native fields: the (rhat, A p) / Arnoldi dot of an
+ * external Krylov loop on the stencil's epilogue (SURVEY 8(b) fused
+ * apply+dot; LatticeOperator.apply + numpy vdot, lattice.py:214-217).
+ * complex128 handles; flags / tau as mgt_wilson_apply. */
+int mgt_wilson_apply_dot(mgt_wilson_t h, const void *x_dev, void *y_dev,
+                         const void *u_dev, int n_rhs, int flags, double tau,
+                         double *dot_out_dev, void *stream);
+
 /* The same operator on n_rhs rhs-interleaved fields ((comp*V + site)*n_rhs +
  * rhs), n_rhs in {1, 2, 4, 8, 12}: one pass over the links for all rhs
  * (LatticeOperator.apply on an (N, k) block, lattice.py:214-217). */

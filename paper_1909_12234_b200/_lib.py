@@ -75,6 +75,7 @@ _SIGNATURES = {
                                          vp, ct.c_size_t, c_i64_p, c_dbl_p, c_dbl_p, vp]),
     "mgt_gcr_workspace_bytes": (ct.c_size_t, [vp, ct.c_int]),
     "mgt_gcr_solve": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp, c_i64_p, c_dbl_p, vp]),
+    "mgt_wilson_apply_dot": (ct.c_int, [vp, vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp, vp]),
     "mgt_gmres_workspace_bytes": (ct.c_size_t, [vp, ct.c_int]),
     "mgt_gmres_solve": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, ct.c_int, ct.c_double, vp, c_i64_p,
                                    c_dbl_p, vp]),

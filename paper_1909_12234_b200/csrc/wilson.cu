@@ -6,6 +6,7 @@
 #include <string>
 
 #include "handle.cuh"
+#include "reduce.cuh"
 
 namespace mgt {
 
@@ -245,6 +246,72 @@ int wilson_apply_native(const mgt_wilson_s *h, const void *x, void *y, int n_rhs
   return apply_groups<float, 12>(h, P, x, y, n_rhs, st);
 }
 
+// ---------------------------------------------------------------------------
+// Fused y = A' x and d = (u, y) (numpy vdot) for an external Krylov loop
+// (SURVEY 8(b) "fused wd_apply_axpy_dot": the sigma = (rhat, A p) step of
+// BiCGStab or the first Arnoldi dot): the dot rides on the stencil's
+// epilogue instead of re-reading y.  fp64; dynamically scheduled chunks
+// publish per-chunk partials, summed in chunk order by the last block
+// (deterministic).
+template <int RECON>
+__global__ void __launch_bounds__(128, 3)
+    wilson_apply_dot_kernel(WilsonParams P, const double2 *__restrict__ in, double2 *__restrict__ out,
+                            const double2 *__restrict__ u, LinkField<double, RECON> links, unsigned long long *ctr,
+                            unsigned *ticket, double *partials, double *dot_out) {
+  const int64_t V = P.g.V;
+  const int64_t nch = (V + 127) / 128;
+  for (int64_t chunk = next_chunk(ctr); chunk < nch; chunk = next_chunk(ctr)) {
+    const int64_t o = chunk * 128 + threadIdx.x;
+    double acc[2] = {0.0, 0.0};
+    if (o < V) {
+      const int64_t site = sched_site(P.sched, o);
+      C<double> y[4][3], xc[4][3];
+      wilson_eval<double, RECON>(P, in, links, site, y, xc);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int64_t q = (int64_t)(a * 3 + c) * V + site;
+          stc(out + q, y[a][c]);
+          const C<double> uu = ldc(u + q);
+          acc[0] += uu.re * y[a][c].re + uu.im * y[a][c].im;
+          acc[1] += uu.re * y[a][c].im - uu.im * y[a][c].re;
+        }
+    }
+    chunk_publish<1, 2>(acc, partials + chunk * 2);
+  }
+  if (last_block(ticket)) {
+    double r[2];
+    reduce_finish_n<2>(partials, nch, ticket, r);
+    if (threadIdx.x == 0) {
+      dot_out[0] = r[0];
+      dot_out[1] = r[1];
+    }
+  }
+}
+
+template <int RECON>
+static int apply_dot(const mgt_wilson_s *h, const WilsonParams &P, const double2 *x, double2 *y, const double2 *u,
+                     int n_rhs, double *dot_dev, cudaStream_t st) {
+  LinkField<double, RECON> lf{reinterpret_cast<const double2 *>(h->links), h->g.V};
+  const int64_t V = h->g.V, nch = (V + 127) / 128;
+  static int grid_cache = 0;
+  if (!grid_cache) grid_cache = resident_grid(wilson_apply_dot_kernel<RECON>, 128, (int64_t)1 << 40);
+  const int grid = (int)std::min<int64_t>(grid_cache, nch);
+  char *scr = nullptr;
+  MGT_CUDA(scratch_alloc((void **)&scr, 256 + (size_t)nch * 2 * sizeof(double), st));
+  for (int r = 0; r < n_rhs; ++r) {
+    MGT_CUDA(cudaMemsetAsync(scr, 0, 256, st));
+    wilson_apply_dot_kernel<RECON><<<grid, 128, 0, st>>>(
+        P, x + (int64_t)r * 12 * V, y + (int64_t)r * 12 * V, u + (int64_t)r * 12 * V, lf,
+        reinterpret_cast<unsigned long long *>(scr + 8), reinterpret_cast<unsigned *>(scr),
+        reinterpret_cast<double *>(scr + 256), dot_dev + 2 * r);
+    MGT_LAUNCH_CHECK("wilson_apply_dot_kernel");
+  }
+  MGT_CUDA(cudaFreeAsync(scr, st));
+  return MGT_OK;
+}
+
 }  // namespace mgt
 
 using namespace mgt;
@@ -364,6 +431,22 @@ int mgt_wilson_apply_il(mgt_wilson_t h, const void *x_dev, void *y_dev, int n_rh
   if (x_dev == y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply_il: in-place apply is not supported");
   if (h->slab) return fail(MGT_ERR_INVALID, "mgt_wilson_apply_il: slab handles are not supported");
   return wilson_apply_il_native(h, x_dev, y_dev, n_rhs, flags, tau, as_stream(stream));
+}
+
+int mgt_wilson_apply_dot(mgt_wilson_t h, const void *x_dev, void *y_dev, const void *u_dev, int n_rhs, int flags,
+                         double tau, double *dot_out_dev, void *stream) {
+  if (!h || !x_dev || !y_dev || !u_dev || !dot_out_dev || n_rhs < 1)
+    return fail(MGT_ERR_INVALID, "mgt_wilson_apply_dot: bad argument");
+  if (h->prec != 64) return fail(MGT_ERR_INVALID, "mgt_wilson_apply_dot: needs a complex128 operator");
+  if (h->slab) return fail(MGT_ERR_INVALID, "mgt_wilson_apply_dot: slab handles use mgt_wilson_apply_slab");
+  if (x_dev == y_dev) return fail(MGT_ERR_INVALID, "mgt_wilson_apply_dot: in-place apply is not supported");
+  const WilsonParams P = make_params(h, flags, tau);
+  cudaStream_t st = as_stream(stream);
+  const double2 *x = (const double2 *)x_dev, *u = (const double2 *)u_dev;
+  double2 *y = (double2 *)y_dev;
+  note_launch(n_rhs);
+  return h->recon == 18 ? apply_dot<18>(h, P, x, y, u, n_rhs, dot_out_dev, st)
+                        : apply_dot<12>(h, P, x, y, u, n_rhs, dot_out_dev, st);
 }
 
 }  // extern "C"

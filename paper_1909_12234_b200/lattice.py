@@ -188,6 +188,20 @@ class WilsonOperator:
                                                 float(tau), stream_ptr()), "apply")
         return out
 
+    def apply_dot_native(self, x, u, out=None, flags=0, tau=0.0):
+        """(out, d): out = variant(A) x and d[r] = vdot(u_r, out_r) from one
+        fused pass (C ABI `mgt_wilson_apply_dot`, complex128 operators)."""
+        if x.dim() != 3 or x.shape[1] != DOF or x.shape[2] != self.volume or u.shape != x.shape:
+            raise ValueError(f"dimension mismatch: native field shapes {tuple(x.shape)}, {tuple(u.shape)}")
+        if x.dtype != self.dtype or u.dtype != self.dtype:
+            raise ValueError(f"field dtype {x.dtype} / {u.dtype} != operator dtype {self.dtype}")
+        x, u = x.contiguous(), u.contiguous()
+        out = torch.empty_like(x) if out is None else out
+        d = torch.empty((x.shape[0], 2), dtype=torch.float64, device=x.device)
+        _lib.check(_lib.lib().mgt_wilson_apply_dot(self._handle, ptr(x), ptr(out), ptr(u), x.shape[0], int(flags),
+                                                    float(tau), ptr(d), stream_ptr()), "apply_dot")
+        return out, torch.complex(d[:, 0], d[:, 1])
+
     def apply_interleaved(self, x, out=None, flags=0, tau=0.0):
         """out = variant(A) x on rhs-interleaved fields (12, V, n), n in
         {1, 2, 4, 8, 12}: the n rhs of a site share every link load (the

@@ -159,3 +159,23 @@ def test_dense_guard(cuda):
     D = op2.dense()
     A = W.build_wilson4d_csr(links2, (2, 2, 2, 4), 0.1).toarray()
     assert np.abs(D - A).max() < 1e-13
+
+
+@pytest.mark.parametrize("recon,flags,tau", [(12, 0, 0.0), (18, 3, 0.25), (12, 4, -0.1)])
+def test_apply_dot_fused(cuda, recon, flags, tau):
+    """mgt_wilson_apply_dot: y bitwise equal to the plain apply, d = vdot(u, y)
+    to 1e-13, deterministic, 3 rhs."""
+    import torch
+    import paper_1909_12234_b200 as M
+    geo = M.LatticeGeometry((4, 6, 8, 10), "antiperiodic")
+    op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.3, seed=2), 0.1, recon=recon)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn((3, 12, geo.site_count), dtype=torch.complex128, device="cuda", generator=g)
+    u = torch.randn((3, 12, geo.site_count), dtype=torch.complex128, device="cuda", generator=g)
+    y, d = op.apply_dot_native(x, u, flags=flags, tau=tau)
+    y0 = op.apply_native(x, flags=flags, tau=tau)
+    assert torch.equal(y, y0)
+    dr = torch.sum(u.conj() * y0, dim=(1, 2))
+    assert ((d - dr).abs() / dr.abs()).max().item() < 1e-13
+    y2, d2 = op.apply_dot_native(x, u, flags=flags, tau=tau)
+    assert torch.equal(d, d2)
