@@ -63,6 +63,45 @@ def sharded_estimate(local_estimator, n_total, group=None, device=None, t0=None)
     return finish(t0v, samples, int(inv.item()))
 
 
+def _local_vhx(V, X):
+    from .linalg import vhx
+    return vhx(V, X)
+
+
+def _local_sub(V, H, X):
+    from .linalg import sub_vh
+    return sub_vh(V, H, X)
+
+
+def slab_vhx(V, X, group=None, local=None):
+    """t-sharded H = V^H X (the deflation projection on t-slab
+    fields): each rank forms its slab's k x s partial with the projection
+    kernels, the partials are all-gathered and summed in rank order on every
+    rank -- bitwise identical on all ranks and independent of the
+    collective's own reduction order (k x s is small next to the slabs).
+    V: (k, ...) and X: (s, ...) this rank's slab fields; returns (k, s)."""
+    H = (local or _local_vhx)(V, X)
+    world = dist.get_world_size(group)
+    if world == 1:
+        return H
+    Hr = torch.view_as_real(H.contiguous()).contiguous()
+    parts = [torch.empty_like(Hr) for _ in range(world)]
+    dist.all_gather(parts, Hr, group=group)
+    out = parts[0].clone()
+    for p in parts[1:]:
+        out += p
+    return torch.view_as_complex(out)
+
+
+def slab_project_out(V, X, group=None, local_vhx=None, local_sub=None):
+    """t-sharded X <- X - V (V^H X) in place on this rank's slab (the
+    orthogonal deflation / CGS2 step, trace.py:182-183, eigen.py:79-86);
+    returns the global H = V^H X."""
+    H = slab_vhx(V, X, group, local_vhx)
+    (local_sub or _local_sub)(V, H, X)
+    return H
+
+
 def exchange_halos(to_prev, to_next, group=None):
     """Ring exchange of the two t-faces: `to_prev` (this rank's first-slice
     face) goes to rank - 1, `to_next` (last-slice face) to rank + 1.

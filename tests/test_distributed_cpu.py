@@ -106,3 +106,41 @@ def test_halo_exchange_ring(world):
     for r, (from_next, from_prev) in enumerate(res):
         assert from_next == 10 * ((r + 1) % world) + 1  # next rank's first-slice face
         assert from_prev == 10 * ((r - 1) % world) + 2  # previous rank's last-slice face
+
+
+def _slab_proj(rank, world):
+    from paper_1909_12234_b200.distributed import shard_range, slab_project_out, slab_vhx
+    rng = np.random.default_rng(21)
+    k, s, n = 5, 3, 61
+    V = rng.normal(size=(k, n)) + 1j * rng.normal(size=(k, n))
+    X = rng.normal(size=(s, n)) + 1j * rng.normal(size=(s, n))
+    j0, j1 = shard_range(n, rank, world)
+    Vl = torch.as_tensor(V[:, j0:j1].copy())
+    Xl = torch.as_tensor(X[:, j0:j1].copy())
+
+    def local_vhx(a, b):
+        return a.conj() @ b.T
+
+    def local_sub(a, h, x):
+        x -= (a.T @ h).T
+        return x
+    H = slab_vhx(Vl, Xl, local=local_vhx)
+    H2 = slab_project_out(Vl, Xl, local_vhx=local_vhx, local_sub=local_sub)
+    return H.numpy(), H2.numpy(), Xl.numpy(), (j0, j1)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_projection_matches_global(world):
+    """t-sharded V^H X and X - V (V^H X): rank-ordered sum of slab partials
+    == the global product (1e-14), bitwise identical on every rank."""
+    rng = np.random.default_rng(21)
+    k, s, n = 5, 3, 61
+    V = rng.normal(size=(k, n)) + 1j * rng.normal(size=(k, n))
+    X = rng.normal(size=(s, n)) + 1j * rng.normal(size=(s, n))
+    Hg = V.conj() @ X.T
+    Xg = X - (V.T @ Hg).T
+    res = spawn(world, _slab_proj)
+    for H, H2, Xl, (j0, j1) in res:
+        assert np.abs(H - Hg).max() <= 1e-14 * np.abs(Hg).max()
+        assert np.array_equal(H, res[0][0]) and np.array_equal(H2, H)
+        assert np.abs(Xl - Xg[:, j0:j1]).max() <= 1e-13 * np.abs(Xg).max()
