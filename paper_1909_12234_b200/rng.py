@@ -42,6 +42,17 @@ def _pool():
         return _POOL
 
 
+_COPY_POOL = None
+
+
+def _copy_pool():
+    global _COPY_POOL
+    with _POOL_LOCK:
+        if _COPY_POOL is None:
+            _COPY_POOL = cf.ThreadPoolExecutor(max_workers=8, thread_name_prefix="mgt-rng-copy")
+        return _COPY_POOL
+
+
 class NormalStream:
     """Consecutive `standard_normal` draws of `rng` (a numpy Generator on
     PCG64), decoded in parallel.  `take(n, out=None)` returns the next n
@@ -131,14 +142,23 @@ class NormalStream:
                 break
             self._fill(n - ready)
         pos = 0
+        copies = []
         while pos < n:
             a = self._ready[0]
             m = min(len(a), n - pos)
-            out[pos:pos + m] = a[:m]
+            copies.append((pos, a[:m]))
             pos += m
             self._avail -= m
             if m == len(a):
                 self._ready.pop(0)
             else:
                 self._ready[0] = a[m:]
+        # the copies into `out` (a pinned staging buffer: ~200 MB per half
+        # vector at 32^3 x 64) are memory-bound; spread them over a few
+        # threads (numpy releases the GIL while copying)
+        if n >= (1 << 20) and len(copies) > 1:
+            list(_copy_pool().map(lambda pa: out.__setitem__(slice(pa[0], pa[0] + len(pa[1])), pa[1]), copies))
+        else:
+            for p0, a in copies:
+                out[p0:p0 + len(a)] = a
         return out
