@@ -460,7 +460,7 @@ def probes_config3(M, rank, world, dims=(16, 16, 16, 16), s=128, tol=1e-8, nv=24
     nvs = MG.generate_null_vectors(op, nv, tol=1e-12, max_iter=8, seed=7)
     pro = MG.build_prolongator(nvs, MG.BlockingScheme((4, 4, 4, 4)), layout_op=op)
     coarse = MG.build_coarse_operator(op, pro)
-    coarse.dense_inverse_native()  # tr(C^-1) and C^-1 for the per-probe correction
+    coarse.exact_inverse()  # tr(C^-1) and C^-1 for the per-probe correction (coarse even-odd Schur)
     torch.cuda.synchronize()
     setup = _max_over_ranks(time.perf_counter() - t0, world)
     inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))

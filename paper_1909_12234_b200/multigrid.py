@@ -481,6 +481,22 @@ class CoarseOperator:
             del D
         return self._dinv
 
+    def exact_inverse(self):
+        """Exact C^-1 for the full-prolongator deflation (BASELINE configs[2]):
+        returns an object with .t0 = tr(C^-1) and .apply_rows(H) = rows of
+        H C^-T (i.e. (C^-1 h)^T for every row h), cached.  With every coarse
+        extent even it is the coarse even-odd Schur factorisation
+        (`CoarseSchurInverse`: ~3x fewer flops than the dense inverse), else
+        the dense LU inverse."""
+        if getattr(self, "_exact_inv", None) is None:
+            pr = self.prolongator
+            cd = pr.blocking.coarse_dims(pr.geometry)
+            if all(c % 2 == 0 for c in cd):
+                self._exact_inv = CoarseSchurInverse(self)
+            else:
+                self._exact_inv = _DenseInverse(self.dense_inverse_native())
+        return self._exact_inv
+
     def dense(self):
         """Dense matrix in the reference coarse order (host numpy)."""
         pr = self.prolongator
@@ -491,6 +507,75 @@ class CoarseOperator:
         Dr = torch.empty_like(Dn)
         Dr[idx[:, None], idx[None, :]] = Dn
         return Dr.cpu().numpy()
+
+
+class _DenseInverse:
+    def __init__(self, Dinv):
+        self.Dinv = Dinv
+        self.t0 = complex(torch.diagonal(Dinv).sum().item())
+
+    def apply_rows(self, H):
+        return H @ self.Dinv.transpose(0, 1)
+
+
+class CoarseSchurInverse:
+    """C^-1 through the coarse checkerboard (every coarse extent even: the
+    9-point coarse stencil couples only opposite-parity aggregates, so C_oo
+    and C_ee are block diagonal -- one 2nv x 2nv block per aggregate):
+        S = C_ee - C_eo C_oo^-1 C_oe,   A = C_eo C_oo^-1,   B = C_oo^-1 C_oe,
+        tr(C^-1) = tr(S^-1) + tr(C_oo^-1) + tr(S^-1 A B),
+        y_e = S^-1 (h_e - A h_o),   y_o = C_oo^-1 h_o - B y_e.
+    The reference forms tr(C^-1) by a dense factorisation of the whole
+    Nc x Nc operator (trace.py:203-217); this does one dense inverse of
+    half the size plus two half-size GEMMs (~3x fewer flops), exact in
+    fp64 arithmetic (same t0 to rounding)."""
+
+    def __init__(self, coarse):
+        pr = coarse.prolongator
+        C0, C1, C2, C3 = pr.blocking.coarse_dims(pr.geometry)
+        nb, nc = pr.n_blocks, pr.nc
+        b = np.arange(nb)
+        par = ((b % C2) + (b // C2) % C1 + (b // (C2 * C1)) % C0 + b // (C2 * C1 * C0)) & 1
+        dev = device()
+        cols = np.arange(nc)
+        iE = torch.as_tensor((np.flatnonzero(par == 0)[:, None] * nc + cols).reshape(-1), device=dev)
+        iO = torch.as_tensor((np.flatnonzero(par == 1)[:, None] * nc + cols).reshape(-1), device=dev)
+        ne, no = len(iE) // nc, len(iO) // nc
+        D = coarse.dense_native()
+        Ceo = D[iE][:, iO]
+        Coe = D[iO][:, iE]
+        Cee = D[iE][:, iE]
+        Coo = D[iO][:, iO]
+        del D
+        Coo_b = Coo.reshape(no, nc, no, nc).diagonal(dim1=0, dim2=2).permute(2, 0, 1).contiguous()
+        off = Coo.reshape(no, nc, no, nc).abs().sum(dim=(1, 3))
+        off.fill_diagonal_(0.0)
+        if off.max().item() > 0.0:
+            raise RuntimeError("coarse operator: odd-odd block is not block diagonal")
+        del Coo
+        self.Cooinv = torch.linalg.inv(Coo_b)  # (no, nc, nc)
+        A = torch.einsum("rja,jab->rjb", Ceo.reshape(ne * nc, no, nc), self.Cooinv).reshape(ne * nc, no * nc)
+        B = torch.einsum("jab,jbc->jac", self.Cooinv, Coe.reshape(no, nc, ne * nc)).reshape(no * nc, ne * nc)
+        del Ceo
+        S = Cee - A @ Coe
+        del Cee, Coe
+        self.Sinv = torch.linalg.inv(S)
+        del S
+        tr_sab = torch.sum((self.Sinv @ A) * B.transpose(0, 1))
+        self.t0 = complex((torch.diagonal(self.Sinv).sum() + torch.diagonal(self.Cooinv, dim1=1, dim2=2).sum()
+                           + tr_sab).item())
+        self.A, self.B, self.iE, self.iO, self.no, self.nc = A, B, iE, iO, no, nc
+
+    def apply_rows(self, H):
+        """rows (C^-1 h)^T for the rows h of H (n, Nc), native coarse order."""
+        He, Ho = H[:, self.iE], H[:, self.iO]
+        Ye = (He - Ho @ self.A.transpose(0, 1)) @ self.Sinv.transpose(0, 1)
+        Yo = torch.einsum("jab,njb->nja", self.Cooinv, Ho.reshape(H.shape[0], self.no, self.nc)).reshape(Ho.shape) \
+            - Ye @ self.B.transpose(0, 1)
+        Y = torch.empty_like(H)
+        Y[:, self.iE] = Ye
+        Y[:, self.iO] = Yo
+        return Y
 
 
 def coarse_gamma5(x, nv):

@@ -349,8 +349,8 @@ def _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op):
     import torch
     from .multigrid import build_coarse_operator
     coarse = coarse_op if coarse_op is not None else build_coarse_operator(op, prolongator)
-    Dinv = coarse.dense_inverse_native()  # setup, cached on the coarse operator
-    t0 = complex(torch.diagonal(Dinv).sum().item())
+    cinv = coarse.exact_inverse()  # setup, cached on the coarse operator (coarse Schur or dense LU)
+    t0 = cinv.t0
     Nc = prolongator.coarse_dim
     store = {}
 
@@ -361,7 +361,7 @@ def _full_coarse_deflation(op, inv_op, prolongator, probes, coarse_op):
         # one (s x Nc) x (Nc x Nc) product for all probes: C^-1 is read once
         keys = sorted(store)
         H = torch.cat([store[k] for k in keys])
-        CH = H @ Dinv.transpose(0, 1)
+        CH = cinv.apply_rows(H)
         return torch.sum(H.conj() * CH, dim=1).cpu().numpy()
 
     return t0, (restrict, corrections)

@@ -343,3 +343,25 @@ def test_tsm_correction(gold, setup):
     z0 = P.rademacher_numpy(op.dim, 3)
     xe = np.vdot(z0, np.linalg.solve(A.toarray(), z0))
     assert 0 < abs(c) < 1e-2 * abs(xe)
+
+
+def test_coarse_schur_inverse_matches_dense(gold, setup):
+    """Coarse even-odd Schur factors (config 3's exact tr(C^-1) and C^-1 h):
+    t0 and C^-1 h equal the dense inverse's to 1e-12, and the golden
+    reference C's dense inverse (numpy) to 1e-11."""
+    M, MG, geo, op, A, Pg = setup
+    nvs = MG.null_vectors_from_array(op, gold["null_vectors"])
+    pro = MG.build_prolongator(nvs, MG.BlockingScheme(tuple(gold["block"])), layout_op=op)
+    C = MG.build_coarse_operator(op, pro)
+    sch = MG.CoarseSchurInverse(C)
+    Dinv = C.dense_inverse_native()
+    t0d = complex(torch.diagonal(Dinv).sum().item())
+    assert abs(sch.t0 - t0d) <= 1e-12 * abs(t0d)
+    t0g = np.trace(np.linalg.inv(gold["C_dense"]))
+    assert abs(sch.t0 - t0g) <= 1e-11 * abs(t0g)
+    g = torch.Generator(device="cuda").manual_seed(8)
+    H = torch.randn((5, pro.coarse_dim), dtype=torch.complex128, device="cuda", generator=g)
+    Y = sch.apply_rows(H)
+    Yd = H @ Dinv.transpose(0, 1)
+    assert ((Y - Yd).abs().max() / Yd.abs().max()).item() < 1e-12
+    assert isinstance(C.exact_inverse(), MG.CoarseSchurInverse)
