@@ -1374,11 +1374,19 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
 // small lattices (at most 2^13 sites per parity: 8^4, 8^3 x 16) take the
 // 4-blocks-per-SM fp32 stencils
 constexpr int64_t kSmallMixedVh = 8192;
+static int64_t small_mixed_vh() {  // MGT_SMALL_VH overrides (A/B)
+  static int64_t v = -1;
+  if (v < 0) {
+    const char *e = getenv("MGT_SMALL_VH");
+    v = e ? atoll(e) : kSmallMixedVh;
+  }
+  return v;
+}
 template <int NR, int RECON>
 static int solve_group_mixed_any(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b,
                                  double2 *x, char *ws, const WSLayout &Lw, double tol, int max_iter,
                                  int64_t *report, double *relres, double *dot_out, int G, cudaStream_t st) {
-  if (h->g.V / 2 <= kSmallMixedVh)
+  if (h->g.V / 2 <= small_mixed_vh())
     return solve_group_mixed<NR, RECON, 4>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report, relres, dot_out,
                                            G, st);
   return solve_group_mixed<NR, RECON>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report, relres, dot_out, G,
