@@ -65,8 +65,17 @@ __global__ void links_from_ref_kernel(Geom g, const double2 *__restrict__ ref, c
 // ---------------------------------------------------------------------------
 // plain apply: one thread per (site, rhs-in-group of NR), links shared by the
 // NR threads of a site through L1 broadcast.
+// resident blocks per SM of the plain apply (tools/f32_apply_ab.sh): fp32
+// at 5 (102 registers) -- 8.5 % faster than 4 at 32^4 and 48^3 x 96 (3, 6:
+// slower); fp64 at 3 (168 registers, no spills)
+#ifndef MGT_F32_APPLY_MINB
+#define MGT_F32_APPLY_MINB 5
+#endif
+#ifndef MGT_F64_APPLY_MINB
+#define MGT_F64_APPLY_MINB 3
+#endif
 template <typename R, int RECON, int NR>
-__global__ void __launch_bounds__(128, (sizeof(R) == 8 ? 3 : 4))
+__global__ void __launch_bounds__(128, (sizeof(R) == 8 ? MGT_F64_APPLY_MINB : MGT_F32_APPLY_MINB))
     wilson_apply_kernel(WilsonParams P, const cplx<R> *__restrict__ in, cplx<R> *__restrict__ out,
                         LinkField<R, RECON> links, unsigned long long *ctr) {
   // warp w of the block serves rhs w % NR on 32 consecutive sites: every load
