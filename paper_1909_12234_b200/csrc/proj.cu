@@ -27,12 +27,25 @@ constexpr int warp_vecs() {
   return S <= 2 ? 8 : (S <= 4 ? 4 : 2);
 }
 
+// e-elements per lane per loop trip: their V and X loads are issued together
+// ahead of the FMAs (more bytes in flight per SM for the HBM-bound few-column
+// shapes; 1 at S = 8 where the accumulators already fill the registers).
+template <int S>
+constexpr int vhx_unroll() {
+#ifdef MGT_VHX_NO_UNROLL
+  return 1;
+#else
+  return S <= 2 ? 4 : (S <= 4 ? 2 : 1);
+#endif
+}
+
 // S: compile-time column capacity, s <= S the actual column count
 template <int S>
 __global__ void __launch_bounds__(256, 2) vhx_small_kernel(const double2 *__restrict__ V, const double2 *__restrict__ X,
                                                            int64_t len, int k, int s, double2 *__restrict__ part) {
   constexpr int kWarpVecs = warp_vecs<S>();
   constexpr int kBlockVecs = 8 * kWarpVecs;
+  constexpr int U = vhx_unroll<S>();
   __shared__ double2 red[8][kWarpVecs * S];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i0 = blockIdx.y * kBlockVecs + warp * kWarpVecs;
@@ -41,18 +54,26 @@ __global__ void __launch_bounds__(256, 2) vhx_small_kernel(const double2 *__rest
   for (int a = 0; a < kWarpVecs; ++a)
 #pragma unroll
     for (int j = 0; j < S; ++j) acc[a][j] = C<double>(0.0, 0.0);
-  for (int64_t e = blockIdx.x * 32 + lane; e < len; e += (int64_t)gridDim.x * 32) {
-    C<double> xv[S];
+  const int64_t stride = (int64_t)gridDim.x * 32;
+  for (int64_t e = blockIdx.x * 32 + lane; e < len; e += stride * U) {
+    // element u of this trip: e + u * stride (absent ones load zeros)
+    C<double> xv[U][S], v[U][kWarpVecs];
 #pragma unroll
-    for (int j = 0; j < S; ++j) xv[j] = j < s ? ldc(X + (int64_t)j * len + e) : C<double>(0.0, 0.0);
+    for (int u = 0; u < U; ++u) {
+      const int64_t eu = e + u * stride;
+      const bool in = eu < len;
 #pragma unroll
-    for (int a = 0; a < kWarpVecs; ++a) {
-      if (i0 + a < k) {
-        C<double> v = ldc(V + (int64_t)(i0 + a) * len + e);
+      for (int j = 0; j < S; ++j) xv[u][j] = (j < s && in) ? ldc(X + (int64_t)j * len + eu) : C<double>(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < S; ++j) acc[a][j] = cfma_conj(v, xv[j], acc[a][j]);
-      }
+      for (int a = 0; a < kWarpVecs; ++a)
+        v[u][a] = (i0 + a < k && in) ? ldc(V + (int64_t)(i0 + a) * len + eu) : C<double>(0.0, 0.0);
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int a = 0; a < kWarpVecs; ++a)
+#pragma unroll
+        for (int j = 0; j < S; ++j) acc[a][j] = cfma_conj(v[u][a], xv[u][j], acc[a][j]);
   }
   // warp reduce, then each warp writes its own 8 x S values (distinct i)
 #pragma unroll
