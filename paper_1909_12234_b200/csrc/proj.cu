@@ -237,7 +237,13 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
     const int kk = swapped ? s : k, ss = swapped ? k : s;
     const int bv = 8 * (ss <= 2 ? warp_vecs<1>() : (ss <= 4 ? warp_vecs<4>() : warp_vecs<8>()));
     const int gy = (kk + bv - 1) / bv;
+#ifdef MGT_VHX_OLD_GRID
     nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, (int64_t)kNumSMs * 6 / gy + 1));
+#else
+    // one full wave of the 2 resident blocks per SM (grid-stride over len):
+    // no partial tail wave, and fewer partials for the final reduction
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, std::max(1, kNumSMs * 2 / gy)));
+#endif
     MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy);
 #define MGT_VHX(SS) vhx_small_kernel<SS><<<grid, 256, 0, st>>>(Vv, Xv, len, kk, ss, part)
@@ -257,8 +263,21 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
     const int tj = s <= 16 ? 16 : (s <= 32 ? 32 : 64);
     const int gy = (k + 63) / 64, gz = (s + tj - 1) / tj;
     // ~16 resident 64-thread tiles (4 of 256 threads) per SM
+#ifdef MGT_VHX_OLD_GRID
     const int per_sm = 4 * 64 / tj;
     nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, (int64_t)kNumSMs * per_sm / (gy * gz) + 1));
+#else
+    // one full wave of resident tiles (occupancy-queried), no partial tail
+    int per_sm = 1;
+    if (tj == 16)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vhx_tile_kernel<16>, 64, 0);
+    else if (tj == 32)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vhx_tile_kernel<32>, 128, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vhx_tile_kernel<64>, 256, 0);
+    per_sm = std::max(per_sm, 1);
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, std::max(1, kNumSMs * per_sm / (gy * gz))));
+#endif
     MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy, gz);
     if (tj == 16)
@@ -281,13 +300,27 @@ int mgt_proj_sub(const void *V_dev, const void *H_dev, void *X_dev, int64_t len,
   if (!V_dev || !X_dev || !H_dev || len < 0 || k < 1 || s < 1) return fail(MGT_ERR_INVALID, "mgt_proj_sub: bad argument");
   cudaStream_t st = as_stream(stream);
   const int TJ = s >= 8 ? 8 : (s >= 4 ? 4 : (s >= 2 ? 2 : 1));
-  dim3 grid(grid_for(len, 256, 4), (s + TJ - 1) / TJ);
+  const int gy = (s + TJ - 1) / TJ;
+  dim3 grid(grid_for(len, 256, 4), gy);
   const size_t smem = (size_t)k * TJ * sizeof(double2);
   if (smem > 200 * 1024) return fail(MGT_ERR_INVALID, "mgt_proj_sub: k too large");
+  // MGT_PSUB: one full wave of resident blocks over (len, column tiles)
+#ifdef MGT_VHX_OLD_GRID
+#define MGT_PSUB_GRID(T)
+#else
+#define MGT_PSUB_GRID(T)                                                                                 \
+  do {                                                                                                   \
+    int per_sm = 1;                                                                                      \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, proj_sub_kernel<T>, 256, smem);               \
+    grid.x = (unsigned)std::max<int64_t>(                                                                \
+        1, std::min<int64_t>((len + 255) / 256, std::max(1, kNumSMs * std::max(per_sm, 1) / gy)));      \
+  } while (0)
+#endif
 #define MGT_PSUB(T)                                                                                                \
   do {                                                                                                             \
     if (smem > 48 * 1024)                                                                                          \
       MGT_CUDA(cudaFuncSetAttribute(proj_sub_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    MGT_PSUB_GRID(T);                                                                                              \
     proj_sub_kernel<T><<<grid, 256, smem, st>>>((const double2 *)V_dev, (const double2 *)H_dev, (double2 *)X_dev, \
                                                 len, k, s);                                                        \
   } while (0)
@@ -300,6 +333,7 @@ int mgt_proj_sub(const void *V_dev, const void *H_dev, void *X_dev, int64_t len,
   else
     MGT_PSUB(1);
 #undef MGT_PSUB
+#undef MGT_PSUB_GRID
   MGT_LAUNCH_CHECK("proj_sub_kernel");
   return MGT_OK;
 }
