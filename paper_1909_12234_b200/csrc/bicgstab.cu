@@ -854,7 +854,7 @@ static WSLayout ws_layout(int64_t V, int groups = 1) {
   L.field = align_up((size_t)groups * kMaxGroup * 12 * V * sizeof(double2), 512);
   // static-grid kernels: one NR*NV slot per block; dynamic kernels: one per
   // chunk of 128 / NR sites (NR = 4 is the largest)
-  const size_t per_block = (size_t)kNumSMs * 16 * kMaxGroup * 4;
+  const size_t per_block = (size_t)num_sms() * 16 * kMaxGroup * 4;
   const size_t per_chunk = (size_t)((V + 31) / 32) * kMaxGroup * 3;
   L.gpart = align_up(std::max(per_block, per_chunk), 32);
   L.partials = align_up((size_t)groups * L.gpart * sizeof(double), 256);

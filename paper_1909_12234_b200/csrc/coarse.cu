@@ -561,7 +561,7 @@ static int coarse_bicg_iter_impl(const int dims[4], const int block[4], int nv, 
   if (rc) return rc;
   const int64_t L = cg.nb * cg.nc;
   const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((L + 4 * kCkBlock - 1) / (4 * kCkBlock),
-                                                               std::max(1, 4 * kNumSMs / n)));
+                                                               std::max(1, 4 * num_sms() / n)));
   double *part = nullptr;
   MGT_CUDA(scratch_alloc((void **)&part, (size_t)n * nblk * 3 * sizeof(double), st));
   const dim3 grid(nblk, n);

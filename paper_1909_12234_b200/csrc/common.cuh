@@ -37,7 +37,14 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 // cached instead of being unmapped at every synchronisation.
 cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st);
 
-constexpr int kNumSMs = 148;
+// SM count of the current device (cudaDevAttrMultiProcessorCount), queried
+// once per device: grids sized in multiples of it follow the device (148 on
+// a B200, fewer on a MIG slice) instead of a hard-coded constant.
+int num_sms();
+// Resident blocks per SM of `kernel` at (block, dynamic smem) from the
+// occupancy calculator, cached per (device, kernel, block, smem); -1 if the
+// query fails (the error message is recorded).
+int blocks_per_sm(const void *kernel, int block, size_t smem = 0);
 
 // ---- complex arithmetic on double2 / float2 ------------------------------
 template <typename R> struct cplx_t;
@@ -195,18 +202,17 @@ __device__ __forceinline__ int64_t next_chunk(unsigned long long *ctr) {
 // schedule instead of scattering a block's iterations across the lattice.
 template <typename K>
 inline int resident_grid(K kernel, int block, int64_t work_items) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
+  int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kernel), block, 0);
+  if (per_sm < 1) per_sm = 1;  // a kernel that cannot launch fails at its launch check
   int64_t need = (work_items + block - 1) / block;
-  int64_t g = (int64_t)kNumSMs * per_sm;
+  int64_t g = (int64_t)num_sms() * per_sm;
   if (g > need) g = need;
   return (int)(g < 1 ? 1 : g);
 }
 
 inline int grid_for(int64_t n, int block, int max_blocks_per_sm = 16) {
   int64_t b = (n + block - 1) / block;
-  int64_t cap = (int64_t)kNumSMs * max_blocks_per_sm;
+  int64_t cap = (int64_t)num_sms() * max_blocks_per_sm;
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   return (int)b;

@@ -238,11 +238,11 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
     const int bv = 8 * (ss <= 2 ? warp_vecs<1>() : (ss <= 4 ? warp_vecs<4>() : warp_vecs<8>()));
     const int gy = (kk + bv - 1) / bv;
 #ifdef MGT_VHX_OLD_GRID
-    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, (int64_t)kNumSMs * 6 / gy + 1));
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, (int64_t)num_sms() * 6 / gy + 1));
 #else
     // one full wave of the 2 resident blocks per SM (grid-stride over len):
     // no partial tail wave, and fewer partials for the final reduction
-    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, std::max(1, kNumSMs * 2 / gy)));
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 31) / 32, std::max(1, num_sms() * 2 / gy)));
 #endif
     MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy);
@@ -265,18 +265,14 @@ int mgt_proj_vhx(const void *V_dev, const void *X_dev, int64_t len, int k, int s
     // ~16 resident 64-thread tiles (4 of 256 threads) per SM
 #ifdef MGT_VHX_OLD_GRID
     const int per_sm = 4 * 64 / tj;
-    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, (int64_t)kNumSMs * per_sm / (gy * gz) + 1));
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, (int64_t)num_sms() * per_sm / (gy * gz) + 1));
 #else
     // one full wave of resident tiles (occupancy-queried), no partial tail
-    int per_sm = 1;
-    if (tj == 16)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vhx_tile_kernel<16>, 64, 0);
-    else if (tj == 32)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vhx_tile_kernel<32>, 128, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vhx_tile_kernel<64>, 256, 0);
-    per_sm = std::max(per_sm, 1);
-    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, std::max(1, kNumSMs * per_sm / (gy * gz))));
+    const int per_sm = tj == 16 ? blocks_per_sm((const void *)vhx_tile_kernel<16>, 64)
+                       : tj == 32 ? blocks_per_sm((const void *)vhx_tile_kernel<32>, 128)
+                                  : blocks_per_sm((const void *)vhx_tile_kernel<64>, 256);
+    if (per_sm < 1) return per_sm < 0 ? MGT_ERR_CUDA : fail(MGT_ERR_CUDA, "vhx_tile_kernel cannot be resident");
+    nblk = (int)std::max<int64_t>(1, std::min<int64_t>((len + 7) / 8, std::max(1, num_sms() * per_sm / (gy * gz))));
 #endif
     MGT_CUDA(scratch_alloc((void **)&part, (size_t)nblk * k * s * sizeof(double2), st));
     dim3 grid(nblk, gy, gz);
@@ -310,10 +306,10 @@ int mgt_proj_sub(const void *V_dev, const void *H_dev, void *X_dev, int64_t len,
 #else
 #define MGT_PSUB_GRID(T)                                                                                 \
   do {                                                                                                   \
-    int per_sm = 1;                                                                                      \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, proj_sub_kernel<T>, 256, smem);               \
+    const int per_sm = blocks_per_sm((const void *)proj_sub_kernel<T>, 256, smem);                     \
+    if (per_sm < 1) return per_sm < 0 ? MGT_ERR_CUDA : fail(MGT_ERR_CUDA, "proj_sub_kernel cannot be resident"); \
     grid.x = (unsigned)std::max<int64_t>(                                                                \
-        1, std::min<int64_t>((len + 255) / 256, std::max(1, kNumSMs * std::max(per_sm, 1) / gy)));      \
+        1, std::min<int64_t>((len + 255) / 256, std::max(1, num_sms() * per_sm / gy)));                 \
   } while (0)
 #endif
 #define MGT_PSUB(T)                                                                                                \

@@ -3,7 +3,10 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "handle.cuh"
 #include "reduce.cuh"
@@ -37,6 +40,43 @@ cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st) {
     pool_dev = dev;
   }
   return cudaMallocAsync(p, bytes, st);
+}
+
+int num_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1) {
+    cudaGetLastError();
+    return 148;  // B200; only reached without a usable device (no launch can follow)
+  }
+  cache[dev].store(v, std::memory_order_relaxed);
+  return v;
+}
+
+int blocks_per_sm(const void *kernel, int block, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void *, int, size_t>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, kernel, block, smem);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int per_sm = 0;
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    return -1;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = per_sm;
+  return per_sm;
 }
 
 // ---------------------------------------------------------------------------
