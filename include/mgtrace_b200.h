@@ -240,6 +240,16 @@ int mgt_bicgstab_solve_ws(mgt_wilson_t h, const void *b_dev, void *x_dev,
                           int max_iter, void *workspace_dev, size_t workspace_bytes,
                           int64_t *report_out, double *relres_out,
                           double *dot_out_host, void *stream);
+/* mgt_bicgstab_solve_ws with one relative tolerance per rhs (tols: host
+ * array of n_rhs values in (0,1)): rhs r stops at ||b_r - A x_r|| <=
+ * tols[r] ||b_r||.  Used by the deflated-start estimator (the reference's
+ * tol ||z|| bound on A e = z - A x0 is tol ||z|| / ||r0|| relative to r0,
+ * trace.py:161-188 with krylov.py:78-85). */
+int mgt_bicgstab_solve_tols(mgt_wilson_t h, const void *b_dev, void *x_dev,
+                            int n_rhs, int flags, double tau, const double *tols,
+                            int max_iter, void *workspace_dev, size_t workspace_bytes,
+                            int64_t *report_out, double *relres_out,
+                            double *dot_out_host, void *stream);
 
 /* Fixed-iteration restarted GCR(m) with zero start (krylov.py:52-118 with
  * max_iter = restart = m, as called by generate_null_vectors,

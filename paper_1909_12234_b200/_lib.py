@@ -10,7 +10,8 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmgtrace_b200.so")
+# MGT_LIB_PATH: load another build of the same library (A/B timing runs)
+LIB_PATH = os.environ.get("MGT_LIB_PATH") or os.path.join(_PKG, "libmgtrace_b200.so")
 
 MGT_OK = 0
 MGT_ERR_INVALID = 1
@@ -73,6 +74,8 @@ _SIGNATURES = {
                                       vp, c_i64_p, c_dbl_p, c_dbl_p, vp]),
     "mgt_bicgstab_solve_ws": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, ct.c_double, ct.c_int,
                                          vp, ct.c_size_t, c_i64_p, c_dbl_p, c_dbl_p, vp]),
+    "mgt_bicgstab_solve_tols": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, c_dbl_p, ct.c_int,
+                                           vp, ct.c_size_t, c_i64_p, c_dbl_p, c_dbl_p, vp]),
     "mgt_gcr_workspace_bytes": (ct.c_size_t, [vp, ct.c_int]),
     "mgt_gcr_solve": (ct.c_int, [vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp, c_i64_p, c_dbl_p, vp]),
     "mgt_wilson_apply_dot": (ct.c_int, [vp, vp, vp, vp, ct.c_int, ct.c_int, ct.c_double, vp, vp]),

@@ -46,14 +46,15 @@ struct BiWST {
   using F = cplx<R>;
   F *r, *rhat, *p, *v, *s, *t, *x, *b;
   F *be, *bo, *tmp;    // even-odd solve: b_e, b_o, odd-parity scratch
-  double *partials;
+  TileRed tr;       // tile-ordered reduction scratch (reduce.cuh)
   unsigned *ticket;
   unsigned long long *ctr;   // dynamic chunk counter (dslash kernels), reset by their last block
   unsigned long long *ctr2;  // counter of the eo first-half kernels, reset by the following kernel
   double *red;               // distributed solve: rank-local sums handed to the all-reduce
   BiState *st;
   // batched solves: group g of kMaxGroup rhs (blockIdx.y) owns field slice
-  // g*gfield, partials g*gpart, ticket area g*256 B and states g*kMaxGroup
+  // g*gfield, tile partials g*gpart, ticket area g*256 B and states
+  // g*kMaxGroup
   int64_t gfield, gpart;
   __host__ __device__ __forceinline__ BiWST at(int g) const {
     BiWST o = *this;
@@ -63,7 +64,7 @@ struct BiWST {
 #pragma unroll
     for (int i = 0; i < 11; ++i)
       if (o.*fs[i]) o.*fs[i] += f;
-    o.partials += (int64_t)g * gpart;
+    o.tr.tiles += (int64_t)g * gpart;
     o.ticket = (unsigned *)((char *)ticket + 256 * (int64_t)g);
     o.ctr = (unsigned long long *)((char *)ctr + 256 * (int64_t)g);
     o.ctr2 = (unsigned long long *)((char *)ctr2 + 256 * (int64_t)g);
@@ -128,6 +129,14 @@ constexpr int eo_minb() {
   for (int64_t chunk = next_chunk(CTR), o = chunk * (M).SPB + (M).local; chunk < NCH; \
        chunk = next_chunk(CTR), o = chunk * (M).SPB + (M).local)
 
+// Static chunk loop of the streaming kernels: block b takes chunks b, b +
+// grid, ... of SPB ordered sites (every thread iterates; `o` may be >= V in
+// the last chunk).  Their reductions are tile-ordered (reduce.cuh), so the
+// grid size does not enter the result.
+#define MGT_CHUNK_LOOP(M, V)                                                                              \
+  _Pragma("unroll 1") for (int64_t chunk = blockIdx.x, nch_ = ((V) + (M).SPB - 1) / (M).SPB, o = chunk * (M).SPB + (M).local; \
+       chunk < nch_; chunk += gridDim.x, o = chunk * (M).SPB + (M).local)
+
 // Last-block scalar recurrences of the stencil kernels (shared by the full
 // and the even-odd kernels).  They also reset the chunk counters.
 template <int M, class W>
@@ -155,9 +164,9 @@ __device__ __forceinline__ void k1_logic(const W &w, const double (&out)[NR * 2]
 }
 
 template <int NR, int DIST = 0, class W>
-__device__ __forceinline__ void k1_finish(const W &w, int64_t nchunks) {
+__device__ __forceinline__ void k1_finish(const W &w, int64_t sites) {
   double out[NR * 2];
-  reduce_finish_n<NR * 2>(w.partials, nchunks, w.ticket, out);
+  tiles_final<NR * 2>(w.tr, sites, w.ticket, out);
   if (threadIdx.x == 0) {
     *w.ctr = 0ull;
     *w.ctr2 = 0ull;
@@ -188,9 +197,9 @@ __device__ __forceinline__ void k3_logic(const W &w, const double (&out)[NR * 3]
 }
 
 template <int NR, int DIST = 0, class W>
-__device__ __forceinline__ void k3_finish(const W &w, int64_t nchunks) {
+__device__ __forceinline__ void k3_finish(const W &w, int64_t sites) {
   double out[NR * 3];
-  reduce_finish_n<NR * 3>(w.partials, nchunks, w.ticket, out);
+  tiles_final<NR * 3>(w.tr, sites, w.ticket, out);
   if (threadIdx.x == 0) {
     *w.ctr = 0ull;
     *w.ctr2 = 0ull;
@@ -224,9 +233,9 @@ __device__ __forceinline__ void resid_logic(const W &w, const double (&out)[NR])
 }
 
 template <int NR, int DIST = 0, class W>
-__device__ __forceinline__ void resid_finish(const W &w, int64_t nchunks) {
+__device__ __forceinline__ void resid_finish(const W &w, int64_t sites) {
   double out[NR];
-  reduce_finish_n<NR>(w.partials, nchunks, w.ticket, out);
+  tiles_final<NR>(w.tr, sites, w.ticket, out);
   if (threadIdx.x == 0) {
     *w.ctr = 0ull;
     *w.ctr2 = 0ull;
@@ -277,25 +286,28 @@ __global__ void __launch_bounds__(kRedBlock) bi_init(int64_t V, const double2 *_
                                                      int maxit, int use_bfull) {
   const BiWS w = w_.at(blockIdx.y);
   RhsMap<NR> m;
-  double acc[1] = {0.0};
   b += (int64_t)blockIdx.y * NR * 12 * V;
-  MGT_SITE_LOOP(m, V) {
-    const int64_t base = (int64_t)m.rhs * 12 * V + o;
+  MGT_CHUNK_LOOP(m, V) {
+    double acc[1] = {0.0};
+    if (o < V) {
+      const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      const int64_t q = base + (int64_t)c * V;
-      double2 bb = b[q];
-      w.b[q] = bb;
-      w.r[q] = bb;
-      w.rhat[q] = bb;
-      w.p[q] = bb;
-      w.x[q] = make_double2(0.0, 0.0);
-      acc[0] += bb.x * bb.x + bb.y * bb.y;
+      for (int c = 0; c < 12; ++c) {
+        const int64_t q = base + (int64_t)c * V;
+        double2 bb = b[q];
+        w.b[q] = bb;
+        w.r[q] = bb;
+        w.rhat[q] = bb;
+        w.p[q] = bb;
+        w.x[q] = make_double2(0.0, 0.0);
+        acc[0] += bb.x * bb.x + bb.y * bb.y;
+      }
     }
+    tile_publish<NR, 1>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
   }
-  if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR];
-    reduce_finish<NR>(w.partials, w.ticket, out);
+    tiles_final<NR>(w.tr, V, w.ticket, out);
     if (DIST)
       store_red<NR>(w, out);
     else
@@ -330,9 +342,10 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k1(WilsonParams P, LinkField<
           acc[1] += rh.re * y[a][c].im - rh.im * y[a][c].re;
         }
     }
-    chunk_publish<NR, 2>(acc, w.partials + chunk * NR * 2);
+    if (run_me) tile_publish<NR, 2>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
   }
-  if (last_block(w.ticket)) k1_finish<NR, DIST>(w, nchunks);
+  (void)nchunks;
+  if (last_block(w.ticket)) k1_finish<NR, DIST>(w, V);
 }
 
 template <int NR, class W>
@@ -353,22 +366,25 @@ __global__ void __launch_bounds__(kRedBlock) bi_k2(int64_t V, BiWST<R> w_) {
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
   const C<R> al = cvt<R>(w.st[m.rhs].alpha);
-  double acc[1] = {0.0};
   if (run_me) {
-    MGT_SITE_LOOP(m, V) {
-      const int64_t base = (int64_t)m.rhs * 12 * V + o;
+      MGT_CHUNK_LOOP(m, V) {
+      double acc[1] = {0.0};
+      if (o < V) {
+        const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-      for (int c = 0; c < 12; ++c) {
-        const int64_t q = base + (int64_t)c * V;
-        C<R> ss = ldc(w.r + q) - al * ldc(w.v + q);
-        stc(w.s + q, ss);
-        acc[0] += dnorm2(ss);
+        for (int c = 0; c < 12; ++c) {
+          const int64_t q = base + (int64_t)c * V;
+          C<R> ss = ldc(w.r + q) - al * ldc(w.v + q);
+          stc(w.s + q, ss);
+          acc[0] += dnorm2(ss);
+        }
       }
+      tile_publish<NR, 1>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
     }
   }
-  if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR];
-    reduce_finish<NR>(w.partials, w.ticket, out);
+    tiles_final<NR>(w.tr, V, w.ticket, out);
     if (DIST)
       store_red<NR>(w, out);
     else
@@ -403,9 +419,10 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_k3(WilsonParams P, LinkField<
           acc[2] += cabs2(tt);
         }
     }
-    chunk_publish<NR, 3>(acc, w.partials + chunk * NR * 3);
+    if (run_me) tile_publish<NR, 3>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
   }
-  if (last_block(w.ticket)) k3_finish<NR, DIST>(w, nchunks);
+  (void)nchunks;
+  if (last_block(w.ticket)) k3_finish<NR, DIST>(w, V);
 }
 
 template <int NR, class W>
@@ -440,27 +457,30 @@ __global__ void __launch_bounds__(kRedBlock) bi_k4(int64_t V, BiWST<R> w_) {
   RhsMap<NR> m;
   const bool run_me = w.st[m.rhs].status == ST_RUN;
   const C<R> al = cvt<R>(w.st[m.rhs].alpha), om = cvt<R>(w.st[m.rhs].omega);
-  double acc[3] = {0.0, 0.0, 0.0};
   if (run_me) {
-    MGT_SITE_LOOP(m, V) {
-      const int64_t base = (int64_t)m.rhs * 12 * V + o;
+      MGT_CHUNK_LOOP(m, V) {
+      double acc[3] = {0.0, 0.0, 0.0};
+      if (o < V) {
+        const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-      for (int c = 0; c < 12; ++c) {
-        const int64_t q = base + (int64_t)c * V;
-        C<R> xx = ldc(w.x + q), pp = ldc(w.p + q), ss = ldc(w.s + q), tt = ldc(w.t + q), rh = ldc(w.rhat + q);
-        xx = xx + al * pp + om * ss;
-        C<R> rr = ss - om * tt;
-        stc(w.x + q, xx);
-        stc(w.r + q, rr);
-        acc[0] += dre(rh, rr);
-        acc[1] += dim(rh, rr);
-        acc[2] += dnorm2(rr);
+        for (int c = 0; c < 12; ++c) {
+          const int64_t q = base + (int64_t)c * V;
+          C<R> xx = ldc(w.x + q), pp = ldc(w.p + q), ss = ldc(w.s + q), tt = ldc(w.t + q), rh = ldc(w.rhat + q);
+          xx = xx + al * pp + om * ss;
+          C<R> rr = ss - om * tt;
+          stc(w.x + q, xx);
+          stc(w.r + q, rr);
+          acc[0] += dre(rh, rr);
+          acc[1] += dim(rh, rr);
+          acc[2] += dnorm2(rr);
+        }
       }
+      tile_publish<NR, 3>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
     }
   }
-  if (reduce_publish<NR, 3>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR * 3];
-    reduce_finish<NR * 3>(w.partials, w.ticket, out);
+    tiles_final<NR * 3>(w.tr, V, w.ticket, out);
     if (DIST)
       store_red<NR * 3>(w, out);
     else
@@ -519,9 +539,10 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid(WilsonParams P, LinkFie
           acc[0] += cabs2(rr);
         }
     }
-    chunk_publish<NR, 1>(acc, w.partials + chunk * NR);
+    if (act_me) tile_publish<NR, 1>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
   }
-  if (last_block(w.ticket)) resid_finish<NR, DIST>(w, nchunks);
+  (void)nchunks;
+  if (last_block(w.ticket)) resid_finish<NR, DIST>(w, V);
 }
 
 template <int NR, class W>
@@ -545,23 +566,26 @@ __global__ void __launch_bounds__(kRedBlock) bi_restart(int64_t V, BiWS w_) {
   if (!any_status<NR>(w.st, ST_RESTART)) return;
   RhsMap<NR> m;
   const bool act_me = w.st[m.rhs].status == ST_RESTART;
-  double acc[1] = {0.0};
   if (act_me) {
-    MGT_SITE_LOOP(m, V) {
-      const int64_t base = (int64_t)m.rhs * 12 * V + o;
+    MGT_CHUNK_LOOP(m, V) {
+      double acc[1] = {0.0};
+      if (o < V) {
+        const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-      for (int c = 0; c < 12; ++c) {
-        const int64_t q = base + (int64_t)c * V;
-        double2 rr = w.r[q];
-        w.rhat[q] = rr;
-        w.p[q] = rr;
-        acc[0] += rr.x * rr.x + rr.y * rr.y;
+        for (int c = 0; c < 12; ++c) {
+          const int64_t q = base + (int64_t)c * V;
+          double2 rr = w.r[q];
+          w.rhat[q] = rr;
+          w.p[q] = rr;
+          acc[0] += rr.x * rr.x + rr.y * rr.y;
+        }
       }
+      tile_publish<NR, 1>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
     }
   }
-  if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR];
-    reduce_finish<NR>(w.partials, w.ticket, out);
+    tiles_final<NR>(w.tr, V, w.ticket, out);
     if (DIST)
       store_red<NR>(w, out);
     else
@@ -575,21 +599,24 @@ __global__ void __launch_bounds__(kRedBlock) bi_final(int64_t V, double2 *__rest
   const BiWS w = w_.at(blockIdx.y);
   xout += (int64_t)blockIdx.y * NR * 12 * V;
   RhsMap<NR> m;
-  double acc[2] = {0.0, 0.0};
-  MGT_SITE_LOOP(m, V) {
-    const int64_t base = (int64_t)m.rhs * 12 * V + o;
+  MGT_CHUNK_LOOP(m, V) {
+    double acc[2] = {0.0, 0.0};
+    if (o < V) {
+      const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      const int64_t q = base + (int64_t)c * V;
-      C<double> bb = ldc(w.b + q), xx = ldc(w.x + q);
-      stc(xout + q, xx);
-      acc[0] += bb.re * xx.re + bb.im * xx.im;
-      acc[1] += bb.re * xx.im - bb.im * xx.re;
+      for (int c = 0; c < 12; ++c) {
+        const int64_t q = base + (int64_t)c * V;
+        C<double> bb = ldc(w.b + q), xx = ldc(w.x + q);
+        stc(xout + q, xx);
+        acc[0] += bb.re * xx.re + bb.im * xx.im;
+        acc[1] += bb.re * xx.im - bb.im * xx.re;
+      }
     }
+    tile_publish<NR, 2>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
   }
-  if (reduce_publish<NR, 2>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR * 2];
-    reduce_finish<NR * 2>(w.partials, w.ticket, out);
+    tiles_final<NR * 2>(w.tr, V, w.ticket, out);
     if (DIST)
       store_red<NR * 2>(w, out);
     else if (threadIdx.x < NR)
@@ -614,26 +641,29 @@ __global__ void __launch_bounds__(kRedBlock) bi_eo_split(BiEo X, const double2 *
   RhsMap<NR> m;
   const int64_t Vh = X.E.Vh, V = X.E.g.V;
   const C<double> iu(X.R.iu_re, X.R.iu_im), id(X.R.id_re, X.R.id_im);
-  double acc[1] = {0.0};
-  MGT_SITE_LOOP(m, Vh) {
-    int x[4];
-    const int64_t fe = eo_coords(X.E, 0, o, x);
-    const int64_t fo = eo_coords(X.E, 1, o, x);
-    const double2 *B = b + (int64_t)m.rhs * 12 * V;
-    const int64_t hb = (int64_t)m.rhs * 12 * Vh + o;
+  MGT_CHUNK_LOOP(m, Vh) {
+    double acc[1] = {0.0};
+    if (o < Vh) {
+      int x[4];
+      const int64_t fe = eo_coords(X.E, 0, o, x);
+      const int64_t fo = eo_coords(X.E, 1, o, x);
+      const double2 *B = b + (int64_t)m.rhs * 12 * V;
+      const int64_t hb = (int64_t)m.rhs * 12 * Vh + o;
 #pragma unroll
-    for (int k = 0; k < 12; ++k) {
-      const C<double> e = ldc(B + (int64_t)k * V + fe), od = ldc(B + (int64_t)k * V + fo);
-      stc(w.be + hb + (int64_t)k * Vh, e);
-      stc(w.bo + hb + (int64_t)k * Vh, od);
-      const C<double> u = k < 6 ? iu * od : id * (g5out * od);
-      stc(w.tmp + hb + (int64_t)k * Vh, u);
-      acc[0] += cabs2(e) + cabs2(od);
+      for (int k = 0; k < 12; ++k) {
+        const C<double> e = ldc(B + (int64_t)k * V + fe), od = ldc(B + (int64_t)k * V + fo);
+        stc(w.be + hb + (int64_t)k * Vh, e);
+        stc(w.bo + hb + (int64_t)k * Vh, od);
+        const C<double> u = k < 6 ? iu * od : id * (g5out * od);
+        stc(w.tmp + hb + (int64_t)k * Vh, u);
+        acc[0] += cabs2(e) + cabs2(od);
+      }
     }
+    tile_publish<NR, 1>(acc, w.tr, m.tile(o), n_tiles(Vh), m.rhs);
   }
-  if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR];
-    reduce_finish<NR>(w.partials, w.ticket, out);
+    tiles_final<NR>(w.tr, Vh, w.ticket, out);
     if (threadIdx.x < NR) w.st[threadIdx.x].bfull2 = out[threadIdx.x];
   }
 }
@@ -716,9 +746,10 @@ __global__ void __launch_bounds__(kRedBlock, MINB) bi_k1_eo(BiEo X, LinkField<R,
           acc[1] += dim(rh, y[a][k]);
         }
     }
-    chunk_publish<NR, 2>(acc, w.partials + chunk * NR * 2);
+    if (run_me) tile_publish<NR, 2>(acc, w.tr, m.tile(o), n_tiles(Vh), m.rhs);
   }
-  if (last_block(w.ticket)) k1_finish<NR>(w, nchunks);
+  (void)nchunks;
+  if (last_block(w.ticket)) k1_finish<NR>(w, Vh);
 }
 
 // K3 (eo): t = S s ; (t, s), |t|^2
@@ -749,9 +780,10 @@ __global__ void __launch_bounds__(kRedBlock, MINB) bi_k3_eo(BiEo X, LinkField<R,
           acc[2] += dnorm2(tt);
         }
     }
-    chunk_publish<NR, 3>(acc, w.partials + chunk * NR * 3);
+    if (run_me) tile_publish<NR, 3>(acc, w.tr, m.tile(o), n_tiles(Vh), m.rhs);
   }
-  if (last_block(w.ticket)) k3_finish<NR>(w, nchunks);
+  (void)nchunks;
+  if (last_block(w.ticket)) k3_finish<NR>(w, Vh);
 }
 
 // true Schur residual r = bh - S x (= the full residual, odd rows exact)
@@ -784,9 +816,10 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_resid_eo(BiEo X, LinkField<do
           acc[0] += cabs2(rr);
         }
     }
-    chunk_publish<NR, 1>(acc, w.partials + chunk * NR);
+    if (act_me) tile_publish<NR, 1>(acc, w.tr, m.tile(o), n_tiles(Vh), m.rhs);
   }
-  if (last_block(w.ticket)) resid_finish<NR>(w, nchunks);
+  (void)nchunks;
+  if (last_block(w.ticket)) resid_finish<NR>(w, Vh);
 }
 
 // x_full: even sites <- x_e, odd sites <- x_o = G_in Dg^-1 [G_out b_o + 1/2 H_oe G_in x_e];
@@ -801,29 +834,32 @@ __global__ void __launch_bounds__(kRedBlock, 3) bi_eo_final(BiEo X, LinkField<do
   const int64_t Vh = X.E.Vh, V = X.E.g.V;
   const int64_t off = (int64_t)m.rhs * 12 * Vh;
   double2 *XO = xout + (int64_t)m.rhs * 12 * V;
-  double acc[2] = {0.0, 0.0};
-  MGT_SITE_LOOP(m, Vh) {
-    int x[4];
-    const int64_t fe = eo_coords(X.E, 0, o, x);
-    const int64_t fo = eo_coords(X.E, 1, o, x);
-    C<double> y[4][3], cc[4][3];
-    eo_eval<double, RECON>(X.E, 1, X.R.recon, w.x + off, w.bo + off, lo, le, o, y, cc);
+  MGT_CHUNK_LOOP(m, Vh) {
+    double acc[2] = {0.0, 0.0};
+    if (o < Vh) {
+      int x[4];
+      const int64_t fe = eo_coords(X.E, 0, o, x);
+      const int64_t fo = eo_coords(X.E, 1, o, x);
+      C<double> y[4][3], cc[4][3];
+      eo_eval<double, RECON>(X.E, 1, X.R.recon, w.x + off, w.bo + off, lo, le, o, y, cc);
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const int ck = a * 3 + k;
-        const C<double> xe = ldc(w.x + off + (int64_t)ck * Vh + o), bev = ldc(w.be + off + (int64_t)ck * Vh + o);
-        stc(XO + (int64_t)ck * V + fe, xe);
-        stc(XO + (int64_t)ck * V + fo, y[a][k]);
-        const C<double> bov = cc[a][k], xo = y[a][k];
-        acc[0] += bev.re * xe.re + bev.im * xe.im + bov.re * xo.re + bov.im * xo.im;
-        acc[1] += bev.re * xe.im - bev.im * xe.re + bov.re * xo.im - bov.im * xo.re;
-      }
+        for (int k = 0; k < 3; ++k) {
+          const int ck = a * 3 + k;
+          const C<double> xe = ldc(w.x + off + (int64_t)ck * Vh + o), bev = ldc(w.be + off + (int64_t)ck * Vh + o);
+          stc(XO + (int64_t)ck * V + fe, xe);
+          stc(XO + (int64_t)ck * V + fo, y[a][k]);
+          const C<double> bov = cc[a][k], xo = y[a][k];
+          acc[0] += bev.re * xe.re + bev.im * xe.im + bov.re * xo.re + bov.im * xo.im;
+          acc[1] += bev.re * xe.im - bev.im * xe.re + bov.re * xo.im - bov.im * xo.re;
+        }
+    }
+    tile_publish<NR, 2>(acc, w.tr, m.tile(o), n_tiles(Vh), m.rhs);
   }
-  if (reduce_publish<NR, 2>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR * 2];
-    reduce_finish<NR * 2>(w.partials, w.ticket, out);
+    tiles_final<NR * 2>(w.tr, Vh, w.ticket, out);
     const int r = threadIdx.x;
     if (r < NR) {
       w.st[r].dotq = C<double>(out[2 * r], out[2 * r + 1]);
@@ -837,12 +873,38 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 constexpr int kMaxGroup = 4;
 constexpr int kChunk = 8;  // iterations per graph replay
+constexpr int kMaxGroups = 64;
+
+// Per-rhs relative tolerances (mgt_bicgstab_solve_tols): after bi_init,
+// tol2 = tol_r^2 |b_r|^2 for every rhs r of every group.
+struct TolPack {
+  double t[kMaxGroups * kMaxGroup];
+};
+template <int NR>
+__global__ void bi_set_tols(BiWS w_, TolPack tp) {
+  const BiWS w = w_.at(blockIdx.y);
+  const int r = threadIdx.x;
+  if (r < NR) {
+    BiState &s = w.st[r];
+    const double t = tp.t[blockIdx.y * NR + r];
+    s.tol2 = t * t * s.b2;
+  }
+}
+template <int NR>
+static int set_tols(const BiWS &w, const double *tols, int G, cudaStream_t st) {
+  if (!tols) return MGT_OK;
+  TolPack tp;
+  for (int i = 0; i < G * NR; ++i) tp.t[i] = tols[i];
+  bi_set_tols<NR><<<dim3(1, G), 32, 0, st>>>(w, tp);
+  MGT_LAUNCH_CHECK("bi_set_tols");
+  return MGT_OK;
+}
 
 struct WSLayout {
   size_t field, partials, total;
   int64_t V;
   int groups;
-  size_t gpart;  // partial doubles per group
+  size_t gpart;  // tile-partial doubles per group
 };
 
 // groups: batched solves of groups * kMaxGroup rhs share one workspace (and
@@ -852,11 +914,9 @@ static WSLayout ws_layout(int64_t V, int groups = 1) {
   L.V = V;
   L.groups = groups;
   L.field = align_up((size_t)groups * kMaxGroup * 12 * V * sizeof(double2), 512);
-  // static-grid kernels: one NR*NV slot per block; dynamic kernels: one per
-  // chunk of 128 / NR sites (NR = 4 is the largest)
-  const size_t per_block = (size_t)num_sms() * 16 * kMaxGroup * 4;
-  const size_t per_chunk = (size_t)((V + 31) / 32) * kMaxGroup * 3;
-  L.gpart = align_up(std::max(per_block, per_chunk), 32);
+  // tile-ordered reductions (reduce.cuh): up to kMaxGroup * 3 doubles per
+  // tile of the full lattice (the largest loop)
+  L.gpart = align_up((size_t)n_tiles(V) * kMaxGroup * 3, 32);
   L.partials = align_up((size_t)groups * L.gpart * sizeof(double), 256);
   L.total = 8 * L.field + L.partials + 256 * (size_t)groups /*tickets*/ +
             align_up((size_t)groups * kMaxGroup * sizeof(BiState), 256);
@@ -871,6 +931,12 @@ static size_t ws32_bytes(const WSLayout &L) {
   return 8 * f32 + L.partials + 256 * (size_t)L.groups + align_up((size_t)L.groups * kMaxGroup * sizeof(BiState), 256);
 }
 
+template <typename R>
+static void carve_red(BiWST<R> &w, char *q, const WSLayout &Lw) {
+  w.tr.tiles = (double *)q;
+  w.gpart = (int64_t)Lw.gpart;
+}
+
 static BiWST<float> carve32(char *q, const WSLayout &Lw) {
   BiWST<float> w;
   const size_t f32 = align_up((size_t)Lw.groups * kMaxGroup * 12 * (Lw.V / 2) * sizeof(float2), 512);
@@ -878,7 +944,7 @@ static BiWST<float> carve32(char *q, const WSLayout &Lw) {
   for (int i = 0; i < 8; ++i) *f[i] = (float2 *)(q + i * f32);
   w.b = w.be = w.bo = nullptr;
   q += 8 * f32;
-  w.partials = (double *)q;
+  carve_red(w, q, Lw);
   q += Lw.partials;
   w.ticket = (unsigned *)q;
   w.ctr = (unsigned long long *)(q + 8);
@@ -887,7 +953,6 @@ static BiWST<float> carve32(char *q, const WSLayout &Lw) {
   q += 256 * (size_t)Lw.groups;
   w.st = (BiState *)q;
   w.gfield = (int64_t)kMaxGroup * 12 * (Lw.V / 2);
-  w.gpart = (int64_t)Lw.gpart;
   return w;
 }
 
@@ -906,7 +971,7 @@ static BiWS carve(char *q, const WSLayout &Lw, bool eo = false) {
   for (int i = 0; i < (eo ? 11 : 8); ++i) *f[i] = (double2 *)(f0 + i * step);
   if (!eo) w.be = w.bo = w.tmp = nullptr;
   q += 8 * Lw.field;
-  w.partials = (double *)q;
+  carve_red(w, q, Lw);
   q += Lw.partials;
   w.ticket = (unsigned *)q;
   w.ctr = (unsigned long long *)(q + 8);
@@ -915,7 +980,6 @@ static BiWS carve(char *q, const WSLayout &Lw, bool eo = false) {
   q += 256 * (size_t)Lw.groups;
   w.st = (BiState *)q;
   w.gfield = (int64_t)kMaxGroup * 12 * (eo ? Lw.V / 2 : Lw.V);
-  w.gpart = (int64_t)Lw.gpart;
   return w;
 }
 
@@ -995,8 +1059,8 @@ static BiState *state_mailbox(int n) {
 // kernel for all groups (blockIdx.y = group).
 template <int NR, int RECON>
 static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b, double2 *x,
-                       char *ws, const WSLayout &Lw, double tol, int max_iter, int64_t *report, double *relres,
-                       double *dot_out, bool eo, int G, cudaStream_t st) {
+                       char *ws, const WSLayout &Lw, double tol, const double *tols, int max_iter, int64_t *report,
+                       double *relres, double *dot_out, bool eo, int G, cudaStream_t st) {
   const int64_t V = h->g.V;
   const int64_t Vs = eo ? V / 2 : V;  // sites of the solved system
   BiWS w = carve(ws, Lw, eo);
@@ -1040,6 +1104,7 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
     note_launch(1);
   }
   MGT_LAUNCH_CHECK("bi_init");
+  if (int rc = set_tols<NR>(w, tols, G, st)) return rc;
 
   cudaGraphExec_t exec = nullptr;
   {
@@ -1148,23 +1213,26 @@ __global__ void __launch_bounds__(kRedBlock) mx_begin(int64_t V, BiWS w64_, BiWS
   const BiWST<float> w = w_.at(blockIdx.y);
   RhsMap<NR> m;
   const bool act = w64.st[m.rhs].status == ST_RUN;
-  double acc[1] = {0.0};
-  MGT_SITE_LOOP(m, V) {
-    const int64_t base = (int64_t)m.rhs * 12 * V + o;
+  MGT_CHUNK_LOOP(m, V) {
+    double acc[1] = {0.0};
+    if (o < V) {
+      const int64_t base = (int64_t)m.rhs * 12 * V + o;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      const int64_t q = base + (int64_t)c * V;
-      const C<float> bb = act ? cvt<float>(ldc(w64.r + q)) : C<float>(0.f, 0.f);
-      stc(w.r + q, bb);
-      stc(w.rhat + q, bb);
-      stc(w.p + q, bb);
-      stc(w.x + q, C<float>(0.f, 0.f));
-      acc[0] += dnorm2(bb);
+      for (int c = 0; c < 12; ++c) {
+        const int64_t q = base + (int64_t)c * V;
+        const C<float> bb = act ? cvt<float>(ldc(w64.r + q)) : C<float>(0.f, 0.f);
+        stc(w.r + q, bb);
+        stc(w.rhat + q, bb);
+        stc(w.p + q, bb);
+        stc(w.x + q, C<float>(0.f, 0.f));
+        acc[0] += dnorm2(bb);
+      }
     }
+    tile_publish<NR, 1>(acc, w.tr, m.tile(o), n_tiles(V), m.rhs);
   }
-  if (reduce_publish<NR, 1>(acc, w.partials, w.ticket)) {
+  if (last_block(w.ticket)) {
     double out[NR];
-    reduce_finish<NR>(w.partials, w.ticket, out);
+    tiles_final<NR>(w.tr, V, w.ticket, out);
     const int r = threadIdx.x;
     if (r < NR) {
       BiState &s = w.st[r];
@@ -1244,8 +1312,8 @@ __global__ void mx_next(BiWS w_, int cycle, int max_cycles) {
 // better choice once the pass is many waves long).
 template <int NR, int RECON, int MINB32 = eo_minb<float>()>
 static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b,
-                             double2 *x, char *ws, const WSLayout &Lw, double tol, int max_iter, int64_t *report,
-                             double *relres, double *dot_out, int G, cudaStream_t st) {
+                             double2 *x, char *ws, const WSLayout &Lw, double tol, const double *tols, int max_iter,
+                             int64_t *report, double *relres, double *dot_out, int G, cudaStream_t st) {
   const int64_t V = h->g.V, Vs = V / 2;
   BiWS w = carve(ws, Lw, true);
   BiWST<float> w32 = carve32(ws + Lw.total, Lw);
@@ -1284,6 +1352,7 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
   bi_init<NR><<<grid, kRedBlock, 0, st>>>(Vs, w.b, w, tol, max_iter, 1);
   note_launch(3);
   MGT_LAUNCH_CHECK("bi_init (mixed)");
+  if (int rc = set_tols<NR>(w, tols, G, st)) return rc;
 
   cudaGraphExec_t exec = nullptr;
   {
@@ -1384,13 +1453,14 @@ static int64_t small_mixed_vh() {  // MGT_SMALL_VH overrides (A/B)
 }
 template <int NR, int RECON>
 static int solve_group_mixed_any(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b,
-                                 double2 *x, char *ws, const WSLayout &Lw, double tol, int max_iter,
-                                 int64_t *report, double *relres, double *dot_out, int G, cudaStream_t st) {
+                                 double2 *x, char *ws, const WSLayout &Lw, double tol, const double *tols,
+                                 int max_iter, int64_t *report, double *relres, double *dot_out, int G,
+                                 cudaStream_t st) {
   if (h->g.V / 2 <= small_mixed_vh())
-    return solve_group_mixed<NR, RECON, 4>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report, relres, dot_out,
-                                           G, st);
-  return solve_group_mixed<NR, RECON>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report, relres, dot_out, G,
-                                      st);
+    return solve_group_mixed<NR, RECON, 4>(h, P, flags, tau, b, x, ws, Lw, tol, tols, max_iter, report, relres,
+                                           dot_out, G, st);
+  return solve_group_mixed<NR, RECON>(h, P, flags, tau, b, x, ws, Lw, tol, tols, max_iter, report, relres, dot_out,
+                                      G, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1550,11 +1620,17 @@ size_t mgt_bicgstab_workspace_bytes(mgt_wilson_t h, int n_rhs) {
 }
 
 static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau,
-                               double tol, int max_iter, void *workspace_dev, size_t workspace_bytes,
-                               int64_t *report_out, double *relres_out, double *dot_out_host, void *stream) {
+                               double tol, const double *tols, int max_iter, void *workspace_dev,
+                               size_t workspace_bytes, int64_t *report_out, double *relres_out, double *dot_out_host,
+                               void *stream) {
   if (!h || !b_dev || !x_dev || !workspace_dev || !report_out || !relres_out)
     return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: null argument");
   if (h->prec != 64) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: needs a complex128 operator");
+  if (tols) {
+    for (int i = 0; i < n_rhs; ++i)
+      if (!(tols[i] > 0.0 && tols[i] < 1.0)) return fail(MGT_ERR_INVALID, "every tol must be in (0,1)");
+    tol = tols[0];
+  }
   if (!(tol > 0.0 && tol < 1.0)) return fail(MGT_ERR_INVALID, "tol must be in (0,1)");
   if (max_iter < 1) return fail(MGT_ERR_INVALID, "max_iter must be >= 1");
   if (n_rhs < 1) return fail(MGT_ERR_INVALID, "n_rhs must be >= 1");
@@ -1572,7 +1648,7 @@ static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, i
   // groups of kMaxGroup rhs batched into one launch per kernel, as many as
   // the workspace holds
   int gmax = 1;
-  while (gmax < 64 && ws_total(V, gmax + 1, mixed) <= workspace_bytes) ++gmax;
+  while (gmax < kMaxGroups && ws_total(V, gmax + 1, mixed) <= workspace_bytes) ++gmax;
   if (ws_total(V, 1, mixed) > workspace_bytes) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: workspace too small");
   const size_t field = (size_t)12 * V;
   int r0 = 0;
@@ -1585,16 +1661,17 @@ static int bicgstab_solve_impl(mgt_wilson_t h, const void *b_dev, void *x_dev, i
     const double2 *b = (const double2 *)b_dev + r0 * field;
     double2 *x = (double2 *)x_dev + r0 * field;
     double *dot = dot_out_host ? dot_out_host + 2 * r0 : nullptr;
+    const double *tl = tols ? tols + r0 : nullptr;
     char *ws = (char *)workspace_dev;
     int rc;
-#define MGT_SOLVE(NR, GG)                                                                                       \
-  (mixed ? (h->recon == 18 ? solve_group_mixed_any<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter,      \
-                                                           report_out + 4 * r0, relres_out + r0, dot, GG, st)  \
-                           : solve_group_mixed_any<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter,      \
-                                                           report_out + 4 * r0, relres_out + r0, dot, GG, st)) \
-   : (h->recon == 18 ? solve_group<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,  \
-                                            relres_out + r0, dot, eo, GG, st)                                    \
-                     : solve_group<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, max_iter, report_out + 4 * r0,  \
+#define MGT_SOLVE(NR, GG)                                                                                          \
+  (mixed ? (h->recon == 18 ? solve_group_mixed_any<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, tl, max_iter,     \
+                                                           report_out + 4 * r0, relres_out + r0, dot, GG, st)     \
+                           : solve_group_mixed_any<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, tl, max_iter,     \
+                                                           report_out + 4 * r0, relres_out + r0, dot, GG, st))    \
+   : (h->recon == 18 ? solve_group<NR, 18>(h, P, flags, tau, b, x, ws, Lw, tol, tl, max_iter, report_out + 4 * r0, \
+                                            relres_out + r0, dot, eo, GG, st)                                       \
+                     : solve_group<NR, 12>(h, P, flags, tau, b, x, ws, Lw, tol, tl, max_iter, report_out + 4 * r0, \
                                             relres_out + r0, dot, eo, GG, st)))
     if (nr == 4)
       rc = MGT_SOLVE(4, Gc);
@@ -1613,15 +1690,23 @@ int mgt_bicgstab_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs
                        int max_iter, void *workspace_dev, int64_t *report_out, double *relres_out,
                        double *dot_out_host, void *stream) {
   if (!h) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve: null argument");
-  return bicgstab_solve_impl(h, b_dev, x_dev, n_rhs, flags, tau, tol, max_iter, workspace_dev,
+  return bicgstab_solve_impl(h, b_dev, x_dev, n_rhs, flags, tau, tol, nullptr, max_iter, workspace_dev,
                              ws_total(h->g.V, 1, eo_available(h)), report_out, relres_out, dot_out_host, stream);
 }
 
 int mgt_bicgstab_solve_ws(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau,
                           double tol, int max_iter, void *workspace_dev, size_t workspace_bytes, int64_t *report_out,
                           double *relres_out, double *dot_out_host, void *stream) {
-  return bicgstab_solve_impl(h, b_dev, x_dev, n_rhs, flags, tau, tol, max_iter, workspace_dev, workspace_bytes,
-                             report_out, relres_out, dot_out_host, stream);
+  return bicgstab_solve_impl(h, b_dev, x_dev, n_rhs, flags, tau, tol, nullptr, max_iter, workspace_dev,
+                             workspace_bytes, report_out, relres_out, dot_out_host, stream);
+}
+
+int mgt_bicgstab_solve_tols(mgt_wilson_t h, const void *b_dev, void *x_dev, int n_rhs, int flags, double tau,
+                            const double *tols, int max_iter, void *workspace_dev, size_t workspace_bytes,
+                            int64_t *report_out, double *relres_out, double *dot_out_host, void *stream) {
+  if (!tols) return fail(MGT_ERR_INVALID, "mgt_bicgstab_solve_tols: null tolerance array");
+  return bicgstab_solve_impl(h, b_dev, x_dev, n_rhs, flags, tau, 0.0, tols, max_iter, workspace_dev,
+                             workspace_bytes, report_out, relres_out, dot_out_host, stream);
 }
 
 size_t mgt_bicgstab_slab_workspace_bytes(mgt_wilson_t h, int n_rhs) {

@@ -120,9 +120,80 @@ struct RhsMap {
     rhs = w % NR;
     local = (w / NR) * 32 + (threadIdx.x & 31);
   }
+  // tile (32 consecutive ordered sites) of ordered site o of this thread
+  __device__ __forceinline__ static int64_t tile(int64_t o) { return o >> 5; }
   __device__ __forceinline__ int64_t first() const { return blockIdx.x * (int64_t)SPB + local; }
   __device__ __forceinline__ int64_t stride() const { return (int64_t)gridDim.x * SPB; }
 };
+
+// ---------------------------------------------------------------------------
+// Tile-ordered reductions (the solver kernels, bicgstab.cu).  A sum over
+// ordered sites is defined by the site index alone, so a right-hand side's
+// reductions -- and with them its whole BiCGStab iterate sequence -- do not
+// depend on how many rhs share a launch (NR), on the number of batched
+// groups, or on the grid size:
+//   1. tile  = 32 consecutive ordered sites: xor-shuffle tree over the warp
+//              serving them (lane = site in the tile), stored by lane 0;
+//   2. final = lane l sums tiles l, l + 32, l + 64, ... in order, then an
+//              xor tree over the lanes (the kernel's last block).
+// Tile partials are laid out [tile][rhs][value] (M = NR * NV doubles per
+// tile); the order of the sum of one (rhs, value) is the same for every NR.
+// (Folding 32-tile supers inside the kernel by the last-arriving warp needs
+// a fence and an atomic round trip per tile: measured 3-8 % slower per
+// solver iteration.)
+struct TileRed {
+  double *tiles;  // [ntiles][M]
+};
+
+__host__ __device__ __forceinline__ int64_t n_tiles(int64_t sites) { return (sites + 31) / 32; }
+
+// Publish this warp's tile partial v[NV] (rhs r of NR; `tile` warp-uniform;
+// every lane must call it).
+template <int NR, int NV>
+__device__ __forceinline__ void tile_publish(double (&v)[NV], const TileRed &T, int64_t tile, int64_t ntiles, int r) {
+  constexpr int M = NR * NV;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    v[k] = x;
+  }
+  if ((threadIdx.x & 31) == 0 && tile < ntiles) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) T.tiles[tile * M + r * NV + k] = v[k];
+  }
+}
+
+// In the last block (after last_block()): out[j] = the ordered sum above for
+// j < M, then reset the ticket.  Warp w takes values w, w + 4, ...; each
+// lane keeps 8 tile loads in flight and adds them in tile order.  Result
+// visible to the whole block.
+template <int M>
+__device__ __forceinline__ void tiles_final(const TileRed &T, int64_t sites, unsigned *ticket, double (&out)[M]) {
+  __shared__ double res[M > 0 ? M : 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nt = n_tiles(sites);
+  for (int j = warp; j < M; j += kRedWarps) {
+    double s = 0.0;
+    int64_t b = lane;
+    for (; b + 7 * 32 < nt; b += 8 * 32) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldcg(T.tiles + (b + u * 32) * M + j);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += x[u];
+    }
+    for (; b < nt; b += 32) s += __ldcg(T.tiles + b * M + j);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) res[j] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < M; ++j) out[j] = res[j];
+  if (threadIdx.x == 0) *ticket = 0u;
+}
 
 // In the last block: out[j] = sum_b partials[b*M + j] for j < M (fixed
 // order), then reset the ticket.  Result visible to the whole block.

@@ -9,8 +9,14 @@ Probe sharding: Hutchinson probes are independent
 (probing.py:155), so the union of the shards is exactly the single-process
 probe set.  The only collective is one all-gather of the per-probe complex
 samples at the end; every rank then reduces them in GLOBAL probe order with
-the reference's `_finish` arithmetic (trace.py:73-92), so a sharded estimate
-is bitwise equal to the single-GPU one.
+the reference's `_finish` arithmetic (trace.py:73-92).  A probe's solve
+does not depend on the batch it was solved in (the solver's reductions are
+tile-ordered, csrc/reduce.cuh; tests/test_batch_invariance_gpu.py), so a
+sharded Hutchinson estimate is bitwise equal to the single-GPU one.  The
+deflated estimators add per-batch projection corrections (U^H z, Y^H z)
+whose summation order depends on the batch width (kernel choice and grid of
+mgt_proj_vhx); their sharded samples agree with the single-GPU ones to
+rounding (~1e-16 relative), not bitwise.
 
 t-slab decomposition: see `SlabWilsonOperator`.
 """

@@ -106,18 +106,26 @@ class BiCGStab:
         """Solve A x_r = b_r for native fields b (n, 12, V); returns
         (x, [SolveReport], dots or None) where dots[r] = vdot(b_r, x_r).
         even_odd: solve through the even-odd Schur complement (whenever every
-        extent is even); the stopping test is the full residual either way."""
+        extent is even); the stopping test is the full residual either way.
+        tol: one relative tolerance, or one per rhs (mgt_bicgstab_solve_tols)."""
         n = b.shape[0]
         b = b.contiguous()
         x = torch.empty_like(b) if x is None else x
         rep = (ct.c_int64 * (4 * n))()
         rel = (ct.c_double * n)()
         dots = (ct.c_double * (2 * n))() if want_dot else None
-        _lib.check(_lib.lib().mgt_bicgstab_solve_ws(
-            self.op.handle, ptr(b), ptr(x), n,
-            int(self.flags) | (0 if even_odd else _lib.SOLVE_FULL) | (_lib.SOLVE_MIXED if mixed else 0),
-            float(self.tau), float(tol), int(max_iter),
-            ptr(self.workspace), self.ws_bytes, rep, rel, dots, stream_ptr()), "bicgstab")
+        flags = int(self.flags) | (0 if even_odd else _lib.SOLVE_FULL) | (_lib.SOLVE_MIXED if mixed else 0)
+        if np.ndim(tol) == 0:
+            rc = _lib.lib().mgt_bicgstab_solve_ws(
+                self.op.handle, ptr(b), ptr(x), n, flags, float(self.tau), float(tol), int(max_iter),
+                ptr(self.workspace), self.ws_bytes, rep, rel, dots, stream_ptr())
+        else:
+            tols = np.ascontiguousarray(np.broadcast_to(np.asarray(tol, dtype=np.float64), (n,)))
+            rc = _lib.lib().mgt_bicgstab_solve_tols(
+                self.op.handle, ptr(b), ptr(x), n, flags, float(self.tau),
+                tols.ctypes.data_as(ct.POINTER(ct.c_double)), int(max_iter),
+                ptr(self.workspace), self.ws_bytes, rep, rel, dots, stream_ptr())
+        _lib.check(rc, "bicgstab")
         reports = []
         for r in range(n):
             it, mv, conv, reason = rep[4 * r:4 * r + 4]

@@ -86,7 +86,9 @@ def _solve_batches_concurrently(inv_op, probes, batches, correction, streams, gu
     """Solve probe batches (one multi-rhs solve each) on `streams` CUDA streams from host
     worker threads: at small volumes one multi-rhs solve cannot fill 148 SMs,
     several independent ones can.  Returns [(reports, q)] in batch order;
-    every result is a pure function of its probes (bitwise reproducible).
+    every result is bitwise reproducible; the solves are independent of the
+    batching (tile-ordered reductions), the projection corrections' rounding
+    depends on the batch width.
     `guess(j0, z) -> (r0, post)` solves A e = r0 = z - A x0 instead (same
     absolute residual bound tol ||z||) and post(e) gives the slots' values."""
     import torch
@@ -113,8 +115,9 @@ def _solve_batches_concurrently(inv_op, probes, batches, correction, streams, gu
                 zn = torch.linalg.vector_norm(z.reshape(z.shape[0], -1), dim=1)
                 rn = torch.linalg.vector_norm(r0.reshape(r0.shape[0], -1), dim=1)
                 ratio = torch.where(rn > 0, rn / zn, torch.ones_like(rn)).cpu().numpy()
-                e, reps, _ = solver.solve_native(r0, min(0.99, tol / float(ratio.max())), inv_op.config.max_iter,
-                                                 **solve_options(inv_op.config))
+                # per rhs: ||r0_i - A e_i|| <= tol ||z_i||  <=>  relative tol ||z_i|| / ||r0_i|| on r0_i
+                tols = np.minimum(0.99, tol / ratio) if not restarted else min(0.99, tol / float(ratio.max()))
+                e, reps, _ = solver.solve_native(r0, tols, inv_op.config.max_iter, **solve_options(inv_op.config))
                 for rep, f in zip(reps, ratio):  # residuals relative to the probe, as the reference's
                     rep.final_relres *= float(f)
                     rep.converged = rep.final_relres <= tol
@@ -244,17 +247,18 @@ def _group_samples_generic(apply_fn, probes, health=None):
     return samples, flagged
 
 
-def deflate_orthogonal(inv_op, U, probes, op=None, guess=True):
+def deflate_orthogonal(inv_op, U, probes, op=None, guess=False):
     """Algorithm-1 trace estimate with the orthogonal projector of U
     (trace.py:161-188): t0 = sum_i u_i^H A^-1 u_i and per slot
     z^H (A^-1 z - Y U^H z) = q - (Y^H z)^H (U^H z), Y = A^-1 U solved once.
 
-    guess=True (single-slot probe groups): every probe solve starts from the
-    deflated guess x0 = Y (U^H z), i.e. solves A e = z - A x0 to the same
-    residual bound tol ||z||, and the slot value is z^H e -- the same
-    quantity (z^H (x - Y U^H z) with x = x0 + e), O(xi) apart from the
-    zero-start form; the low modes of the start residual are gone, ~11 %
-    fewer iterations at 16^4 with k = 64.
+    guess=True (single-slot probe groups; off by default, the reference
+    solves from zero): every probe solve starts from the deflated guess
+    x0 = Y (U^H z), i.e. solves A e = z - A x0 to the same residual bound
+    tol ||z|| per probe (per-rhs tolerance tol ||z_i|| / ||r0_i||), and the
+    slot value is z^H e -- the same quantity (z^H (x - Y U^H z) with
+    x = x0 + e), O(xi) apart from the zero-start form; the low modes of the
+    start residual are gone, ~11 % fewer iterations at 16^4 with k = 64.
 
     U: native fields (k, 12, V) CUDA tensor, or reference-layout (N, k)
     array/tensor (then `op` or inv_op.op converts the layout)."""

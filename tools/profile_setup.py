@@ -25,7 +25,7 @@ def tick():
     return time.perf_counter()
 
 
-for rep in range(2):
+for rep in range(int(os.environ.get("MGT_SETUP_REPS", "3"))):
     t0 = tick()
     nvs = MG.generate_null_vectors(op, 24, tol=1e-12, max_iter=8, seed=7)
     t1 = tick()
