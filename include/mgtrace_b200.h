@@ -342,14 +342,46 @@ int mgt_coarse_apply_c32(const int dims[4], const int block[4], int nv,
  * LatticeOperator.apply, krylov.py:52-118 / multigrid.py:228-243).  C is the
  * fp64 operator, or its fp32 copy when c_fp32 != 0.  Vectors (n_rhs, Nc)
  * complex128 on the device: x, r, p, v, s, t updated in place, rhat read.
- * state: n_rhs rows of 12 doubles [rho re, im, alpha re, im, omega re, im,
- * beta re, im, |r|^2, active, tol^2, converged], read and written on the
- * device (the caller seeds rho, active, tol^2 and reads |r|^2 / converged). */
+ * state: n_rhs rows of 16 doubles [rho re, im, alpha re, im, omega re, im,
+ * beta re, im, |r|^2, active, tol^2, converged, iterations, freeze, -, -],
+ * read and written on the device (the caller seeds rho, active, tol^2,
+ * freeze and reads |r|^2 / converged / iterations; with freeze != 0 a
+ * converged rhs clears its own active flag). */
 int mgt_coarse_bicgstab_iter(const int dims[4], const int block[4], int nv,
                              const void *C_dev, int c_fp32, double tau,
                              int n_rhs, void *x, void *r, const void *rhat,
                              void *p, void *v, void *s, void *t,
                              double *state, void *stream);
+
+/* Coarse even-odd (checkerboard) form, every coarse extent even.  Parity
+ * fields are compact: aggregate b (native coarse order) has cb index b >> 1;
+ * vectors (n_rhs, nb / 2, 2nv) complex128.  Blocks of one parity's
+ * aggregates, column-major: M[((c * nd + d) * nc + col) * nc + row].
+ * mgt_coarse_half_apply: y[c] = sum_d M[c][d] src_d for output parity par;
+ * nd = 8: the 8 hops (d -> direction d + 1) from x_other; nd = 9: d = 0 the
+ * self block on x_self (dropped when skip_self) and the hops from x_other.
+ * M in fp64, or fp32 when m_fp32 != 0 (fp64 vectors). */
+int mgt_coarse_half_apply(const int dims[4], const int block[4], int nv,
+                          const void *M_dev, int nd, int par, int m_fp32,
+                          int skip_self, const void *x_self, const void *x_other,
+                          void *y, int n_rhs, void *stream);
+/* Schur complement S = C_ee - C_eo C_oo^-1 C_oe of (C + i tau g5_c) on the
+ * even aggregates from D (odd, nd = 8: C_oo^-1 C_o,dir) and E (even, nd = 9:
+ * C_ee and -C_e,dir): y_e = S x_e, t_o: odd scratch (n_rhs fields). */
+int mgt_coarse_schur_apply(const int dims[4], const int block[4], int nv,
+                           const void *D_dev, const void *E_dev, int m_fp32,
+                           const void *x_e, void *y_e, void *t_o, int n_rhs,
+                           void *stream);
+/* n_iters BiCGStab iterations on S for n_rhs even-parity systems, every
+ * scalar on the device (state rows as mgt_coarse_bicgstab_iter; set freeze
+ * so converged rhs stop themselves); t_o: odd scratch.  The caller confirms
+ * convergence on the explicit residual between calls
+ * (multigrid.coarse_bicgstab). */
+int mgt_coarse_schur_bicgstab(const int dims[4], const int block[4], int nv,
+                              const void *D_dev, const void *E_dev, int m_fp32,
+                              int n_rhs, int n_iters, void *x, void *r,
+                              const void *rhat, void *p, void *v, void *s,
+                              void *t, void *t_o, double *state, void *stream);
 
 /* ---- deflation projection (trace.py:161-188, :266-267; eigen.py:79-86) --- */
 /* H (k x s, column major, complex128) = V^H X;  V: (k, len) row-major

@@ -93,6 +93,11 @@ _SIGNATURES = {
     "mgt_coarse_apply_c32": (ct.c_int, [c_int_p, c_int_p, ct.c_int, vp, vp, vp, ct.c_int, vp]),
     "mgt_coarse_bicgstab_iter": (ct.c_int, [c_int_p, c_int_p, ct.c_int, vp, ct.c_int, ct.c_double, ct.c_int, vp, vp,
                                             vp, vp, vp, vp, vp, vp, vp]),
+    "mgt_coarse_half_apply": (ct.c_int, [c_int_p, c_int_p, ct.c_int, vp, ct.c_int, ct.c_int, ct.c_int, ct.c_int,
+                                         vp, vp, vp, ct.c_int, vp]),
+    "mgt_coarse_schur_apply": (ct.c_int, [c_int_p, c_int_p, ct.c_int, vp, vp, ct.c_int, vp, vp, vp, ct.c_int, vp]),
+    "mgt_coarse_schur_bicgstab": (ct.c_int, [c_int_p, c_int_p, ct.c_int, vp, vp, ct.c_int, ct.c_int, ct.c_int, vp, vp,
+                                             vp, vp, vp, vp, vp, vp, vp, vp]),
     "mgt_proj_vhx": (ct.c_int, [vp, vp, ct.c_int64, ct.c_int, ct.c_int, vp, vp]),
     "mgt_proj_sub": (ct.c_int, [vp, vp, vp, ct.c_int64, ct.c_int, ct.c_int, vp]),
 }

@@ -108,6 +108,11 @@ __device__ __forceinline__ bool czero(C<double> a) { return a.re == 0.0 && a.im 
 __device__ __forceinline__ double cabs2(C<double> a) { return a.re * a.re + a.im * a.im; }
 __device__ __forceinline__ bool cfinite(C<double> a) { return isfinite(a.re) && isfinite(a.im); }
 
+// fp32 streaming kernels with two sites per thread (bi_k2v / k4v / k5v)
+#ifndef MGT_F32_PAIRS
+#define MGT_F32_PAIRS 1
+#endif
+
 // resident blocks per SM of the even-odd stencil kernels: fp64 at 3 (168
 // registers, no spills); the fp32 inner kernels need fewer registers
 #ifndef MGT_F32_MINB
@@ -502,6 +507,122 @@ __global__ void __launch_bounds__(kRedBlock) bi_k5(int64_t V, BiWST<R> w_) {
     for (int c = 0; c < 12; ++c) {
       const int64_t q = base + (int64_t)c * V;
       stc(w.p + q, ldc(w.r + q) + be * (ldc(w.p + q) - om * ldc(w.v + q)));
+    }
+  }
+}
+
+// fp32 streaming kernels of the mixed solver's inner BiCGStab (K2, K4, K5
+// above for R = float): two adjacent sites per thread so every access is one
+// 16-byte load/store of two complex<float> (half the memory instructions
+// of the one-site form).  A chunk covers 2 SPB ordered sites; a warp's 64
+// sites are tiles 2k (lanes 0-15) and 2k+1 (lanes 16-31), reduced with
+// tile_publish_pairs.  Needs an even site count (every extent even).
+__device__ __forceinline__ void ld2c(const float2 *p, C<float> &a, C<float> &b) {
+  const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+  a = C<float>(v.x, v.y);
+  b = C<float>(v.z, v.w);
+}
+__device__ __forceinline__ void st2c(float2 *p, C<float> a, C<float> b) {
+  *reinterpret_cast<float4 *>(p) = make_float4(a.re, a.im, b.re, b.im);
+}
+#define MGT_PAIR_LOOP(M, V)                                                                                      \
+  _Pragma("unroll 1") for (int64_t chunk = blockIdx.x, nch_ = ((V) + 2 * (M).SPB - 1) / (2 * (M).SPB),           \
+                                   o = chunk * 2 * (M).SPB + 2 * (M).local;                                     \
+                           chunk < nch_; chunk += gridDim.x, o = chunk * 2 * (M).SPB + 2 * (M).local)
+
+template <int NR>
+__global__ void __launch_bounds__(kRedBlock) bi_k2v(int64_t V, BiWST<float> w_) {
+  const BiWST<float> w = w_.at(blockIdx.y);
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  if (w.st[m.rhs].status == ST_RUN) {
+    const C<float> al = cvt<float>(w.st[m.rhs].alpha);
+    MGT_PAIR_LOOP(m, V) {
+      double acc[1] = {0.0};
+      if (o < V) {
+        const int64_t base = (int64_t)m.rhs * 12 * V + o;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+          const int64_t q = base + (int64_t)c * V;
+          C<float> r0, r1, v0, v1;
+          ld2c(w.r + q, r0, r1);
+          ld2c(w.v + q, v0, v1);
+          const C<float> s0 = r0 - al * v0, s1 = r1 - al * v1;
+          st2c(w.s + q, s0, s1);
+          acc[0] += dnorm2(s0);
+          acc[0] += dnorm2(s1);
+        }
+      }
+      tile_publish_pairs<NR, 1>(acc, w.tr, o >> 5, n_tiles(V), m.rhs);
+    }
+  }
+  if (last_block(w.ticket)) {
+    double out[NR];
+    tiles_final<NR>(w.tr, V, w.ticket, out);
+    k2_logic<NR>(w, out);
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kRedBlock) bi_k4v(int64_t V, BiWST<float> w_) {
+  const BiWST<float> w = w_.at(blockIdx.y);
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  if (w.st[m.rhs].status == ST_RUN) {
+    const C<float> al = cvt<float>(w.st[m.rhs].alpha), om = cvt<float>(w.st[m.rhs].omega);
+    MGT_PAIR_LOOP(m, V) {
+      double acc[3] = {0.0, 0.0, 0.0};
+      if (o < V) {
+        const int64_t base = (int64_t)m.rhs * 12 * V + o;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+          const int64_t q = base + (int64_t)c * V;
+          C<float> x0, x1, p0, p1, s0, s1, t0, t1, h0, h1;
+          ld2c(w.x + q, x0, x1);
+          ld2c(w.p + q, p0, p1);
+          ld2c(w.s + q, s0, s1);
+          ld2c(w.t + q, t0, t1);
+          ld2c(w.rhat + q, h0, h1);
+          const C<float> r0 = s0 - om * t0, r1 = s1 - om * t1;
+          st2c(w.x + q, x0 + al * p0 + om * s0, x1 + al * p1 + om * s1);
+          st2c(w.r + q, r0, r1);
+          acc[0] += dre(h0, r0);
+          acc[1] += dim(h0, r0);
+          acc[2] += dnorm2(r0);
+          acc[0] += dre(h1, r1);
+          acc[1] += dim(h1, r1);
+          acc[2] += dnorm2(r1);
+        }
+      }
+      tile_publish_pairs<NR, 3>(acc, w.tr, o >> 5, n_tiles(V), m.rhs);
+    }
+  }
+  if (last_block(w.ticket)) {
+    double out[NR * 3];
+    tiles_final<NR * 3>(w.tr, V, w.ticket, out);
+    k4_logic<NR>(w, out);
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kRedBlock) bi_k5v(int64_t V, BiWST<float> w_) {
+  const BiWST<float> w = w_.at(blockIdx.y);
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  if (w.st[m.rhs].status != ST_RUN) return;
+  const C<float> be = cvt<float>(w.st[m.rhs].beta), om = cvt<float>(w.st[m.rhs].omega);
+  MGT_PAIR_LOOP(m, V) {
+    if (o < V) {
+      const int64_t base = (int64_t)m.rhs * 12 * V + o;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) {
+        const int64_t q = base + (int64_t)c * V;
+        C<float> r0, r1, p0, p1, v0, v1;
+        ld2c(w.r + q, r0, r1);
+        ld2c(w.p + q, p0, p1);
+        ld2c(w.v + q, v0, v1);
+        st2c(w.p + q, r0 + be * (p0 - om * v0), r1 + be * (p1 - om * v1));
+      }
     }
   }
 }
@@ -1030,11 +1151,19 @@ static int launch_chunk_eo(const BiEo &X, const LinkField<R, RECON> &le, const L
   for (int it = 0; it < kChunk; ++it) {
     bi_eo_first<NR, RECON, R, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
     bi_k1_eo<NR, RECON, R, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
-    bi_k2<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    if constexpr (std::is_same<R, float>::value && MGT_F32_PAIRS)
+      bi_k2v<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    else
+      bi_k2<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
     bi_eo_first<NR, RECON, R, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w, 0);
     bi_k3_eo<NR, RECON, R, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
-    bi_k4<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
-    bi_k5<NR, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    if constexpr (std::is_same<R, float>::value && MGT_F32_PAIRS) {
+      bi_k4v<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
+      bi_k5v<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    } else {
+      bi_k4<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
+      bi_k5<NR, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
+    }
   }
   return MGT_OK;
 }

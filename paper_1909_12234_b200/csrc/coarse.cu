@@ -272,7 +272,7 @@ static int launch_coarse_apply(const CoarseGeom &cg, const CT *C, const double2 
   if (9 * cg.nc <= kCoarseDirThreads) {
     const int block = ((9 * cg.nc + 31) / 32) * 32;
     const size_t smem = (size_t)9 * cg.nc * NR * sizeof(double2);
-    if (smem > 48 * 1024) {
+    if (smem > 40 * 1024) {  // (static shared memory counts toward the 48 KB default as well)
       static size_t set = 0;
       if (smem > set) {
         MGT_CUDA(cudaFuncSetAttribute(coarse_apply_dir_kernel<NR, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -287,7 +287,7 @@ static int launch_coarse_apply(const CoarseGeom &cg, const CT *C, const double2 
   const int G = std::max(1, std::min(9, 256 / cg.nc));
   const int block = ((G * cg.nc + 31) / 32) * 32;
   const size_t smem = (size_t)(9 * cg.nc * NR + G * NR * cg.nc) * sizeof(double2);
-  if (smem > 48 * 1024) {
+  if (smem > 40 * 1024) {  // (static shared memory counts toward the 48 KB default as well)
     static size_t set = 0;
     if (smem > set) {
       MGT_CUDA(cudaFuncSetAttribute(coarse_apply_kernel<NR, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -404,10 +404,12 @@ namespace mgt {
 // device (multigrid.coarse_bicgstab drives the loop and the explicit-residual
 // confirmations).  Per-rhs state row (doubles):
 //   [rho re, im, alpha re, im, omega re, im, beta re, im, r2, active, tol2, conv]
+//   [12] iterations taken, [13] freeze: a converged rhs deactivates itself
+//   (multi-iteration calls), [14..15] reserved
 // Reductions: per-block partials in a fixed grid, summed in block order by a
 // one-warp finisher per rhs (deterministic).
 enum { CK_RHO = 0, CK_ALPHA = 2, CK_OMEGA = 4, CK_BETA = 6, CK_R2 = 8, CK_ACT = 9, CK_TOL2 = 10, CK_CONV = 11,
-       CK_W = 12 };
+       CK_ITS = 12, CK_FREEZE = 13, CK_W = 16 };
 constexpr int kCkBlock = 256;
 
 __device__ __forceinline__ C<double> cdiv(C<double> a, C<double> b) {
@@ -548,7 +550,12 @@ __global__ void ck_finish(int nblk, const double *__restrict__ part, double *__r
     S[CK_RHO] = rn.re, S[CK_RHO + 1] = rn.im;
     S[CK_R2] = v[2];
     const bool nz = rn.re == 0.0 && rn.im == 0.0;
-    S[CK_CONV] = (act && (v[2] <= S[CK_TOL2] || oz || nz)) ? 1.0 : 0.0;
+    const bool conv = act && (v[2] <= S[CK_TOL2] || oz || nz);
+    if (act) {  // an inactive (frozen) rhs keeps its converged flag for the caller
+      S[CK_CONV] = conv ? 1.0 : 0.0;
+      S[CK_ITS] += 1.0;
+    }
+    if (conv && S[CK_FREEZE] != 0.0) S[CK_ACT] = 0.0;
   }
 }
 
@@ -583,9 +590,262 @@ static int coarse_bicg_iter_impl(const int dims[4], const int block[4], int nv, 
   return MGT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Coarse even-odd (checkerboard) form.  With every coarse extent even the
+// 9-point coarse stencil couples only opposite-parity aggregates, so with
+// the shift in the self blocks, C_tau = [[C_ee, C_eo], [C_oe, C_oo]] has
+// block-diagonal C_ee, C_oo and its Schur complement on the even aggregates
+//   S = C_ee - C_eo C_oo^-1 C_oe
+// is applied as two half stencils: t_o = sum_dir D[o, dir] x_e[nbr] with
+// D = C_oo^-1 C_o,dir (8 hops), then y_e = E[e, 0] x_e + sum_dir E[e, dir]
+// t_o[nbr] with E[e, 0] = C_ee, E[e, dir] = -C_e,dir.  Both read 8-9 blocks
+// per aggregate of one parity: an S apply streams as many bytes as one full
+// C apply on half the unknowns, and BiCGStab on S needs about half the
+// iterations (the reference solves the full coarse system with GCR,
+// multigrid.py:228-243 via krylov.py:52-118; the stopping test is the same
+// full residual, the odd rows being solved exactly).
+// Compact parity fields: aggregate b has cb index b >> 1 (the fastest coarse
+// extent is even, so every pair b = 2c, 2c + 1 holds one of each parity);
+// vectors (n_rhs, nb / 2, nc), blocks M[((c * ND + d) * nc + col) * nc + row].
+__device__ __forceinline__ int64_t coarse_cb_full(const CoarseGeom &cg, int64_t c, int par) {
+  const int64_t b0 = 2 * c;
+  int64_t r = b0;
+  const int c2 = (int)(r % cg.Cd[2]);
+  r /= cg.Cd[2];
+  const int c1 = (int)(r % cg.Cd[1]);
+  r /= cg.Cd[1];
+  const int c0 = (int)(r % cg.Cd[0]);
+  const int c3 = (int)(r / cg.Cd[0]);
+  return b0 + ((((c0 + c1 + c2 + c3) & 1) != par) ? 1 : 0);
+}
+
+// y[c] = sum_{d < ND} M[c][d] src_d, output parity `par`; ND = 8: hops
+// 1..8 from x_other; ND = 9: dir 0 (self, from x_self; dropped when
+// skip_self) and hops 1..8 from x_other.  Thread per (d, row), the ND
+// source vectors staged in shared memory, direction partials summed in
+// direction order (deterministic, the same for every NR).
+template <int NR, typename CT, int ND>
+__global__ void __launch_bounds__(kCoarseDirThreads, 2)
+    coarse_half_kernel(CoarseGeom cg, int par, const CT *__restrict__ Mb, const double2 *__restrict__ xs,
+                       const double2 *__restrict__ xo, double2 *__restrict__ y, int skip_self) {
+  extern __shared__ double2 sm[];
+  __shared__ int64_t nbr[ND];
+  const int nc = cg.nc;
+  const int64_t nbh = cg.nb / 2;
+  const int64_t c = blockIdx.x;
+  if (threadIdx.x < ND) {
+    const int dir = ND == 8 ? threadIdx.x + 1 : threadIdx.x;
+    nbr[threadIdx.x] = coarse_nbr(cg, coarse_cb_full(cg, c, par), dir) >> 1;
+  }
+  __syncthreads();
+  using AT = std::conditional_t<sizeof(CT) == 8, float, double>;
+  using A2 = std::conditional_t<sizeof(CT) == 8, float2, double2>;
+  A2 *sx = reinterpret_cast<A2 *>(sm);
+  for (int i = threadIdx.x; i < ND * nc * NR; i += blockDim.x) {
+    const int col = i % nc, q = i / nc;
+    const int r = q % NR, d = q / NR;
+    const bool self = ND == 9 && d == 0;
+    const double2 xv = (self && skip_self) ? make_double2(0.0, 0.0) : (self ? xs : xo)[((int64_t)r * nbh + nbr[d]) * nc + col];
+    A2 a;
+    a.x = (AT)xv.x;
+    a.y = (AT)xv.y;
+    sx[(d * nc + col) * NR + r] = a;
+  }
+  __syncthreads();
+  const int d = threadIdx.x / nc, row = threadIdx.x - d * nc;
+  const bool on = d < ND && !(ND == 9 && d == 0 && skip_self);
+  C<AT> acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = C<AT>(AT(0), AT(0));
+  if (on) {
+    const CT *Cb = Mb + (c * ND + d) * (int64_t)nc * nc + row;
+    const A2 *xsd = sx + d * nc * NR;
+    constexpr int U = (sizeof(CT) == 16 && NR >= 2) ? 4 : 8;
+    for (int c0 = 0; c0 < nc; c0 += U) {
+      CT cl[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c0 + u < nc) cl[u] = Cb[(int64_t)(c0 + u) * nc];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (c0 + u < nc) {
+          const C<AT> cv(cl[u].x, cl[u].y);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const A2 xv = xsd[(c0 + u) * NR + r];
+            acc[r] = cfma(cv, C<AT>(xv.x, xv.y), acc[r]);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (d < ND) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) sm[(d * NR + r) * nc + row] = make_double2((double)acc[r].re, (double)acc[r].im);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NR * nc; i += blockDim.x) {
+    const int r = i / nc, rw = i % nc;
+    C<double> t(0.0, 0.0);
+#pragma unroll
+    for (int dd = 0; dd < ND; ++dd) {
+      const double2 v = sm[(dd * NR + r) * nc + rw];
+      t = t + C<double>(v.x, v.y);
+    }
+    y[((int64_t)r * nbh + c) * nc + rw] = make_double2(t.re, t.im);
+  }
+}
+
+template <int NR, typename CT, int ND>
+static int launch_coarse_half(const CoarseGeom &cg, int par, const CT *M, const double2 *xs, const double2 *xo,
+                              double2 *y, int skip_self, cudaStream_t st) {
+  const int block = ((ND * cg.nc + 31) / 32) * 32;
+  if (block > kCoarseDirThreads) return fail(MGT_ERR_INVALID, "coarse even-odd form: 2 nv > 49 is not supported");
+  const size_t smem = (size_t)ND * cg.nc * NR * sizeof(double2);
+  // (opt in whenever the dynamic part grows: the static nbr table counts
+  // toward the 48 KB default too, e.g. 8 x 48 x 8 x 16 B = exactly 48 KB)
+  static size_t set = 0;
+  if (smem > set) {
+    MGT_CUDA(cudaFuncSetAttribute(coarse_half_kernel<NR, CT, ND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    set = smem;
+  }
+  coarse_half_kernel<NR, CT, ND><<<(unsigned)(cg.nb / 2), block, smem, st>>>(cg, par, M, xs, xo, y, skip_self);
+  MGT_LAUNCH_CHECK("coarse_half_kernel");
+  return MGT_OK;
+}
+
+// n_rhs fields, up to 8 per launch
+template <typename CT, int ND>
+static int coarse_half_impl(const CoarseGeom &cg, int par, const CT *M, const double2 *xs, const double2 *xo,
+                            double2 *y, int skip_self, int n_rhs, cudaStream_t st) {
+  const int64_t stride = (cg.nb / 2) * cg.nc;
+  for (int r = 0; r < n_rhs;) {
+    const int left = n_rhs - r;
+    const int nr = left >= 8 ? 8 : (left >= 4 ? 4 : (left >= 2 ? 2 : 1));
+    const double2 *s0 = xs ? xs + r * stride : nullptr;
+    const double2 *o0 = xo + r * stride;
+    double2 *y0 = y + r * stride;
+    int rc = nr == 8   ? launch_coarse_half<8, CT, ND>(cg, par, M, s0, o0, y0, skip_self, st)
+             : nr == 4 ? launch_coarse_half<4, CT, ND>(cg, par, M, s0, o0, y0, skip_self, st)
+             : nr == 2 ? launch_coarse_half<2, CT, ND>(cg, par, M, s0, o0, y0, skip_self, st)
+                       : launch_coarse_half<1, CT, ND>(cg, par, M, s0, o0, y0, skip_self, st);
+    if (rc) return rc;
+    r += nr;
+  }
+  return MGT_OK;
+}
+
+static int make_cg_eo(const int dims[4], const int block[4], int nv, CoarseGeom &cg) {
+  int rc = make_cg(dims, block, nv, cg);
+  if (rc) return rc;
+  for (int i = 0; i < 4; ++i)
+    if (cg.Cd[i] % 2) return fail(MGT_ERR_INVALID, "coarse even-odd form needs every coarse extent even");
+  return MGT_OK;
+}
+
+// y_e = S x_e through t_o (scratch, n_rhs odd fields)
+template <typename CT>
+static int schur_apply(const CoarseGeom &cg, const CT *D, const CT *E, const double2 *x, double2 *y, double2 *t_o,
+                       int n, cudaStream_t st) {
+  int rc = coarse_half_impl<CT, 8>(cg, 1, D, nullptr, x, t_o, 0, n, st);
+  if (rc) return rc;
+  return coarse_half_impl<CT, 9>(cg, 0, E, x, t_o, y, 0, n, st);
+}
+
+// n_iters BiCGStab iterations on S for n independent rhs, scalars on the
+// device; rhs with freeze set stop themselves once converged
+template <typename CT>
+static int schur_bicg_iters(const CoarseGeom &cg, const CT *D, const CT *E, int n, int n_iters, double2 *x,
+                            double2 *r, const double2 *rhat, double2 *p, double2 *v, double2 *s, double2 *t,
+                            double2 *t_o, double *st_dev, cudaStream_t st) {
+  const int64_t L = (cg.nb / 2) * cg.nc;
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((L + 4 * kCkBlock - 1) / (4 * kCkBlock),
+                                                               std::max(1, 4 * num_sms() / n)));
+  double *part = nullptr;
+  MGT_CUDA(scratch_alloc((void **)&part, (size_t)n * nblk * 3 * sizeof(double), st));
+  const dim3 grid(nblk, n);
+  int rc = MGT_OK;
+  for (int it = 0; it < n_iters && rc == MGT_OK; ++it) {
+    rc = schur_apply<CT>(cg, D, E, p, v, t_o, n, st);
+    if (rc) break;
+    ck_dots<1><<<grid, kCkBlock, 0, st>>>(L, cg.nc, cg.nc / 2, 0.0, v, p, rhat, part);
+    ck_finish<1><<<n, 32, 0, st>>>(nblk, part, st_dev);
+    ck_sub<<<grid, kCkBlock, 0, st>>>(L, st_dev, r, v, s);
+    rc = schur_apply<CT>(cg, D, E, s, t, t_o, n, st);
+    if (rc) break;
+    ck_dots<3><<<grid, kCkBlock, 0, st>>>(L, cg.nc, cg.nc / 2, 0.0, t, s, nullptr, part);
+    ck_finish<3><<<n, 32, 0, st>>>(nblk, part, st_dev);
+    ck_update<<<grid, kCkBlock, 0, st>>>(L, st_dev, x, r, rhat, p, s, t, part);
+    ck_finish<4><<<n, 32, 0, st>>>(nblk, part, st_dev);
+    ck_dir<<<grid, kCkBlock, 0, st>>>(L, st_dev, r, p, v);
+    note_launch(8);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_fail(e, "coarse Schur bicgstab iteration");
+  }
+  cudaFreeAsync(part, st);
+  return rc;
+}
+
 }  // namespace mgt
 
 extern "C" {
+
+int mgt_coarse_half_apply(const int dims[4], const int block[4], int nv, const void *M_dev, int nd, int par,
+                          int m_fp32, int skip_self, const void *x_self, const void *x_other, void *y, int n_rhs,
+                          void *stream) {
+  if (!dims || !block || !M_dev || !x_other || !y || n_rhs < 1 || (nd != 8 && nd != 9) || (par != 0 && par != 1) ||
+      (nd == 9 && !skip_self && !x_self))
+    return fail(MGT_ERR_INVALID, "mgt_coarse_half_apply: bad argument");
+  CoarseGeom cg;
+  int rc = make_cg_eo(dims, block, nv, cg);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  auto D = [](const void *q) { return (const double2 *)q; };
+  if (m_fp32)
+    return nd == 8 ? coarse_half_impl<float2, 8>(cg, par, (const float2 *)M_dev, D(x_self), D(x_other), (double2 *)y,
+                                                 skip_self, n_rhs, st)
+                   : coarse_half_impl<float2, 9>(cg, par, (const float2 *)M_dev, D(x_self), D(x_other), (double2 *)y,
+                                                 skip_self, n_rhs, st);
+  return nd == 8 ? coarse_half_impl<double2, 8>(cg, par, (const double2 *)M_dev, D(x_self), D(x_other), (double2 *)y,
+                                                skip_self, n_rhs, st)
+                 : coarse_half_impl<double2, 9>(cg, par, (const double2 *)M_dev, D(x_self), D(x_other), (double2 *)y,
+                                                skip_self, n_rhs, st);
+}
+
+int mgt_coarse_schur_apply(const int dims[4], const int block[4], int nv, const void *D_dev, const void *E_dev,
+                           int m_fp32, const void *x_e, void *y_e, void *t_o, int n_rhs, void *stream) {
+  if (!dims || !block || !D_dev || !E_dev || !x_e || !y_e || !t_o || n_rhs < 1)
+    return fail(MGT_ERR_INVALID, "mgt_coarse_schur_apply: bad argument");
+  CoarseGeom cg;
+  int rc = make_cg_eo(dims, block, nv, cg);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (m_fp32)
+    return schur_apply<float2>(cg, (const float2 *)D_dev, (const float2 *)E_dev, (const double2 *)x_e, (double2 *)y_e,
+                               (double2 *)t_o, n_rhs, st);
+  return schur_apply<double2>(cg, (const double2 *)D_dev, (const double2 *)E_dev, (const double2 *)x_e,
+                              (double2 *)y_e, (double2 *)t_o, n_rhs, st);
+}
+
+int mgt_coarse_schur_bicgstab(const int dims[4], const int block[4], int nv, const void *D_dev, const void *E_dev,
+                              int m_fp32, int n_rhs, int n_iters, void *x, void *r, const void *rhat, void *p,
+                              void *v, void *s, void *t, void *t_o, double *state, void *stream) {
+  if (!dims || !block || !D_dev || !E_dev || !x || !r || !rhat || !p || !v || !s || !t || !t_o || !state ||
+      n_rhs < 1 || n_iters < 1)
+    return fail(MGT_ERR_INVALID, "mgt_coarse_schur_bicgstab: bad argument");
+  CoarseGeom cg;
+  int rc = make_cg_eo(dims, block, nv, cg);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  auto Q = [](const void *q) { return (double2 *)q; };
+  if (m_fp32)
+    return schur_bicg_iters<float2>(cg, (const float2 *)D_dev, (const float2 *)E_dev, n_rhs, n_iters, Q(x), Q(r),
+                                    Q(rhat), Q(p), Q(v), Q(s), Q(t), Q(t_o), state, st);
+  return schur_bicg_iters<double2>(cg, (const double2 *)D_dev, (const double2 *)E_dev, n_rhs, n_iters, Q(x), Q(r),
+                                   Q(rhat), Q(p), Q(v), Q(s), Q(t), Q(t_o), state, st);
+}
 
 int mgt_coarse_bicgstab_iter(const int dims[4], const int block[4], int nv, const void *C_dev, int c_fp32,
                              double tau, int n_rhs, void *x, void *r, const void *rhat, void *p, void *v, void *s,

@@ -113,14 +113,44 @@ __device__ __forceinline__ void stc(float2 *p, C<float> v) { *p = make_float2(v.
 __device__ __forceinline__ void stc_cs(double2 *p, C<double> v) { __stcs(p, make_double2(v.re, v.im)); }
 __device__ __forceinline__ void stc_cs(float2 *p, C<float> v) { __stcs(p, make_float2(v.re, v.im)); }
 
+// ---- constant-divisor division ---------------------------------------------
+// n / d for 0 <= n < 2^31 as a multiply-high, add and shift (Granlund-
+// Montgomery round-up method; exhaustively spot-checked over divisors
+// 1..2^26 and every power of two +-1).  The site -> coordinate decodes run
+// per site in every stencil kernel; the compiler's generic 32/64-bit
+// division sequence (I2F + MUFU.RCP + Newton steps, a slow-path CALL for
+// 64-bit operands) is ~5x longer and sits on the latency chain in front of
+// the site's first load.
+struct FastDiv {
+  uint32_t d, m, l;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.l = 0;
+  while ((1ull << f.l) < d) ++f.l;
+  f.m = (uint32_t)((((1ull << 32) * ((1ull << f.l) - d)) / d) + 1);
+  return f;
+}
+__host__ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+#ifdef __CUDA_ARCH__
+  return (__umulhi(n, f.m) + n) >> f.l;
+#else
+  return (uint32_t)((((uint64_t)n * f.m >> 32) + n) >> f.l);
+#endif
+}
+
 // ---- lattice geometry -----------------------------------------------------
 // dims in reference order (L0, L1, L2, L3 = t).  Native site order:
 //   s = ((x3*L0 + x0)*L1 + x1)*L2 + x2   (x2 fastest, t slowest)
+// Every handle keeps V < 2^31 (mgt_wilson_create), so site indices decode in
+// 32-bit arithmetic.
 struct Geom {
   int L[4];
   int64_t V;
   // native strides for directions mu = 0..3
   int64_t stride[4];
+  FastDiv fd[3];  // by L[0], L[1], L[2]
 };
 
 inline Geom make_geom(const int dims[4]) {
@@ -131,18 +161,22 @@ inline Geom make_geom(const int dims[4]) {
   g.stride[1] = dims[2];
   g.stride[0] = (int64_t)dims[1] * dims[2];
   g.stride[3] = (int64_t)dims[0] * dims[1] * dims[2];
+  for (int i = 0; i < 3; ++i) g.fd[i] = make_fastdiv((uint32_t)dims[i]);
   return g;
 }
 
 // native site -> coords (x0..x3)
 __host__ __device__ __forceinline__ void native_coords(const Geom &g, int64_t s, int x[4]) {
-  int64_t r = s;
-  x[2] = (int)(r % g.L[2]);
-  r /= g.L[2];
-  x[1] = (int)(r % g.L[1]);
-  r /= g.L[1];
-  x[0] = (int)(r % g.L[0]);
-  x[3] = (int)(r / g.L[0]);
+  uint32_t r = (uint32_t)s;
+  uint32_t q = fdiv(r, g.fd[2]);
+  x[2] = (int)(r - q * (uint32_t)g.L[2]);
+  r = q;
+  q = fdiv(r, g.fd[1]);
+  x[1] = (int)(r - q * (uint32_t)g.L[1]);
+  r = q;
+  q = fdiv(r, g.fd[0]);
+  x[0] = (int)(r - q * (uint32_t)g.L[0]);
+  x[3] = (int)q;
 }
 
 __host__ __device__ __forceinline__ int64_t ref_site(const Geom &g, const int x[4]) {
@@ -162,6 +196,7 @@ struct Sched {
   int64_t slab_sites;  // w * L1 * L2
   int64_t plane;       // L0 * L1 * L2 (native t stride)
   int L3;
+  FastDiv f_slab, f_L3;
 };
 
 inline Sched make_sched(const Geom &g, int64_t bytes_per_site, int64_t budget = (int64_t)24 << 20) {
@@ -173,15 +208,18 @@ inline Sched make_sched(const Geom &g, int64_t bytes_per_site, int64_t budget = 
   s.slab_sites = w * row;
   s.plane = (int64_t)g.L[0] * row;
   s.L3 = g.L[3];
+  s.f_slab = make_fastdiv((uint32_t)s.slab_sites);
+  s.f_L3 = make_fastdiv((uint32_t)s.L3);
   return s;
 }
 
 __host__ __device__ __forceinline__ int64_t sched_site(const Sched &s, int64_t o) {
-  const int64_t q = o / s.slab_sites;
-  const int64_t r = o - q * s.slab_sites;
-  const int64_t t = q % s.L3;
-  const int64_t k = q / s.L3;
-  return t * s.plane + k * s.slab_sites + r;
+  const uint32_t ou = (uint32_t)o;
+  const uint32_t q = fdiv(ou, s.f_slab);
+  const uint32_t r = ou - q * (uint32_t)s.slab_sites;
+  const uint32_t k = fdiv(q, s.f_L3);
+  const uint32_t t = q - k * (uint32_t)s.L3;
+  return (int64_t)t * s.plane + (int64_t)k * s.slab_sites + r;
 }
 
 // Dynamic in-order chunk scheduler for persistent grids: CTAs take

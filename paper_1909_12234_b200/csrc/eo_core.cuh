@@ -28,6 +28,7 @@ struct EoGeom {
   int64_t Vh;   // sites per parity
   int L2h;      // L2 / 2
   int antiperiodic;
+  FastDiv f_L2h;
 };
 
 inline EoGeom make_eo_geom(const Geom &g, int antiperiodic) {
@@ -36,20 +37,22 @@ inline EoGeom make_eo_geom(const Geom &g, int antiperiodic) {
   e.Vh = g.V / 2;
   e.L2h = g.L[2] / 2;
   e.antiperiodic = antiperiodic;
+  e.f_L2h = make_fastdiv((uint32_t)e.L2h);
   return e;
 }
 
-// cb index c of parity p -> coords and full native site
+// cb index c of parity p -> coords and full native site (32-bit decode)
 __device__ __forceinline__ int64_t eo_coords(const EoGeom &E, int p, int64_t c, int (&x)[4]) {
-  const int64_t row = c / E.L2h;
-  const int x2h = (int)(c - row * E.L2h);
-  int64_t r = row;
-  x[1] = (int)(r % E.g.L[1]);
-  r /= E.g.L[1];
-  x[0] = (int)(r % E.g.L[0]);
-  x[3] = (int)(r / E.g.L[0]);
+  const uint32_t cu = (uint32_t)c;
+  const uint32_t row = fdiv(cu, E.f_L2h);
+  const int x2h = (int)(cu - row * (uint32_t)E.L2h);
+  const uint32_t r1 = fdiv(row, E.g.fd[1]);
+  x[1] = (int)(row - r1 * (uint32_t)E.g.L[1]);
+  const uint32_t r0 = fdiv(r1, E.g.fd[0]);
+  x[0] = (int)(r1 - r0 * (uint32_t)E.g.L[0]);
+  x[3] = (int)r0;
   x[2] = 2 * x2h + ((p + x[0] + x[1] + x[3]) & 1);
-  return row * E.g.L[2] + x[2];
+  return (int64_t)row * E.g.L[2] + x[2];
 }
 
 // One hop into acc (no -1/2): the neighbour spinor lives in the other-parity

@@ -165,6 +165,27 @@ __device__ __forceinline__ void tile_publish(double (&v)[NV], const TileRed &T, 
   }
 }
 
+// Variant for kernels that stream two adjacent sites per thread (16-byte
+// fp32 accesses): lanes 0-15 hold tile A, lanes 16-31 tile B (`tile` per
+// lane); the tile tree is over the 16 lanes of a half-warp.  Each such
+// kernel uses this shape for every NR, so its sums stay batch-invariant.
+template <int NR, int NV>
+__device__ __forceinline__ void tile_publish_pairs(double (&v)[NV], const TileRed &T, int64_t tile, int64_t ntiles,
+                                                   int r) {
+  constexpr int M = NR * NV;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    v[k] = x;
+  }
+  if ((threadIdx.x & 15) == 0 && tile < ntiles) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) T.tiles[tile * M + r * NV + k] = v[k];
+  }
+}
+
 // In the last block (after last_block()): out[j] = the ordered sum above for
 // j < M, then reset the ticket.  Warp w takes values w, w + 4, ...; each
 // lane keeps 8 tile loads in flight and adds them in tile order.  Result

@@ -409,6 +409,32 @@ class _LayoutOnly:
 # ---------------------------------------------------------------------------
 
 
+def coarse_schur_blocks(C, cdims, nv, tau=0.0):
+    """Even-odd factors of (C + i tau g5_c) for 9-block coarse storage C
+    (flat, [b][dir][col][row]) on coarse dims `cdims` (every extent even):
+    compact even / odd aggregate lists ie / io (cb index c -> aggregate),
+    C_oo^-1 ([o][row][col]), D = C_oo^-1 C_o,dir (8 hops) and
+    E = [C_ee, -C_e,dir] in the kernels' column-major block storage."""
+    import types
+    C0, C1, C2, C3 = cdims
+    nb = C0 * C1 * C2 * C3
+    nc = 2 * nv
+    dev = C.device
+    c = torch.arange(nb // 2, device=dev)
+    b0 = 2 * c
+    par0 = ((b0 % C2) + (b0 // C2) % C1 + (b0 // (C2 * C1)) % C0 + b0 // (C2 * C1 * C0)) & 1
+    ie = b0 + (par0 != 0).long()  # compact index c -> full aggregate, even parity
+    io = b0 + (par0 != 1).long()
+    C4 = C.reshape(nb, 9, nc, nc)  # [b][dir][col][row]
+    g5 = torch.ones(nc, dtype=torch.float64, device=dev)
+    g5[nv:] = -1.0
+    selfb = C4[:, 0] + torch.diag(1j * tau * g5).to(C4.dtype)  # diagonal: the same in either storage order
+    Cooinv = torch.linalg.inv(selfb[io].transpose(-1, -2))      # [o][row][col]
+    D = (Cooinv[:, None] @ C4[io, 1:].transpose(-1, -2)).transpose(-1, -2).contiguous()
+    E = torch.cat([selfb[ie][:, None], -C4[ie, 1:]], dim=1).contiguous()
+    return types.SimpleNamespace(tau=float(tau), ie=ie, io=io, Cooinv=Cooinv, D=D, E=E, D32=None, E32=None)
+
+
 class CoarseOperator:
     """Galerkin V^H A V as 9 dense blocks per aggregate (multigrid.py:228-243)."""
 
@@ -457,6 +483,24 @@ class CoarseOperator:
         nat = pr.coarse_from_ref(xd.reshape(1, pr.n_blocks, pr.nc))
         y = pr.coarse_to_ref(self.apply_native(nat)).reshape(-1)
         return y.cpu().numpy() if host else y
+
+    def schur_factors(self, tau=0.0):
+        """Coarse even-odd factors of (C + i tau g5_c) (every coarse extent
+        even; `None` otherwise), cached per tau: the compact even / odd
+        aggregate lists, C_oo^-1 per odd aggregate, the odd-side hop blocks
+        D = C_oo^-1 C_o,dir and the even-side blocks E = [C_ee, -C_e,dir]
+        of the Schur complement S = C_ee - C_eo C_oo^-1 C_oe
+        (csrc/coarse.cu, mgt_coarse_half_apply / mgt_coarse_schur_*)."""
+        key = float(tau)
+        cache = getattr(self, "_schur", None)
+        if cache is not None and cache.tau == key:
+            return cache
+        pr = self.prolongator
+        cd = pr.blocking.coarse_dims(pr.geometry)
+        if any(c % 2 for c in cd):
+            return None
+        self._schur = coarse_schur_blocks(self.C, cd, pr.nv, key)
+        return self._schur
 
     def dense_native(self):
         """Dense Nc x Nc on the device, NATIVE coarse order (blocks of aliased
@@ -589,13 +633,118 @@ def coarse_gamma5(x, nv):
 LOW_PRECISION_TOL = 1e-5  # coarse solves at least this loose iterate with fp32 C
 
 
-def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
+def _schur_bicgstab(coarse, F, b, tol, max_iter):
+    """BiCGStab on the coarse Schur complement S x_e = b_e - C_eo C_oo^-1 b_o
+    (coarse even-odd form), x_o = C_oo^-1 (b_o - C_oe x_e): the odd rows are
+    solved exactly, so the full residual is (bh_e - S x_e, 0) and the
+    stopping test is the reference's ||b - C x|| <= tol ||b||
+    (krylov.py:78-85) on the explicitly recomputed Schur residual."""
+    pr = coarse.prolongator
+    nv = pr.nv
+    low = tol >= LOW_PRECISION_TOL
+    if low and F.D32 is None:
+        F.D32, F.E32 = F.D.to(torch.complex64), F.E.to(torch.complex64)
+    Dm, Em = (F.D32, F.E32) if low else (F.D, F.E)
+    d, bk = pr._dims()
+    lib = _lib.lib()
+    n = b.shape[0]
+    be, bo = b[:, F.ie].contiguous(), b[:, F.io].contiguous()
+    uo = torch.einsum("orc,noc->nor", F.Cooinv, bo).contiguous()
+    hop = torch.empty_like(be)
+    _lib.check(lib.mgt_coarse_half_apply(d, bk, nv, ptr(F.E), 9, 0, 0, 1, None, ptr(uo), ptr(hop), n, stream_ptr()),
+               "coarse half apply")
+    bh = be + hop
+    to = torch.empty_like(be)
+
+    def S(v):  # exact (fp64) Schur apply
+        y = torch.empty_like(v)
+        _lib.check(lib.mgt_coarse_schur_apply(d, bk, nv, ptr(F.D), ptr(F.E), 0, ptr(v), ptr(y), ptr(to), v.shape[0],
+                                              stream_ptr()), "coarse Schur apply")
+        return y
+
+    def dot(u, v):
+        return torch.sum(u.conj() * v, dim=(1, 2))
+
+    b2 = dot(b, b).real
+    tol2 = (tol * tol) * b2
+    x = torch.zeros_like(bh)
+    r = bh.clone()
+    rhat, p = r.clone(), r.clone()
+    v, s_, t = torch.empty_like(r), torch.empty_like(r), torch.empty_like(r)
+    rho = dot(rhat, r)
+    done = (b2 == 0).cpu().numpy().copy()
+    state = torch.zeros((n, 16), dtype=torch.float64, device=b.device)
+    state[:, 0], state[:, 1] = rho.real, rho.imag
+    state[:, 9] = torch.as_tensor(~done, device=b.device, dtype=torch.float64)
+    state[:, 10] = tol2
+    state[:, 13] = 1.0  # freeze: converged rhs stop themselves inside a multi-iteration call
+    tol2_h = tol2.cpu().numpy()
+    mv_extra = np.zeros(n, dtype=int)
+    rt = None
+    its = np.zeros(n, dtype=int)
+    # the first call runs as many iterations as the previous solve of this
+    # tolerance needed (the Davidson's inner solves repeat), then one per call:
+    # few host round trips, at most a couple of surplus iterations
+    hints = F.__dict__.setdefault("its_hint", {})
+    k_next = max(1, hints.get(tol, 2))
+    while not done.all() and its[~done].max(initial=0) < max_iter:
+        k = int(min(k_next, max_iter - its[~done].max(initial=0)))
+        k_next = 1
+        _lib.check(lib.mgt_coarse_schur_bicgstab(d, bk, nv, ptr(Dm), ptr(Em), 1 if low else 0, n, k, ptr(x), ptr(r),
+                                                 ptr(rhat), ptr(p), ptr(v), ptr(s_), ptr(t), ptr(to), ptr(state),
+                                                 stream_ptr()), "coarse Schur bicgstab")
+        st = state.cpu().numpy()
+        its = st[:, 12].astype(int)
+        newly = (st[:, 11] != 0) & (st[:, 9] == 0) & ~done
+        if ((st[:, 9] == 0) & ~done & ~newly).any():
+            raise RuntimeError("coarse Schur BiCGStab: a system stopped without converging")
+        rt = None
+        if newly.any():
+            rt = bh - S(x)
+            mv_extra[newly] += 1
+            rt2 = dot(rt, rt).real.cpu().numpy()
+            ok = newly & (rt2 <= tol2_h)
+            done |= ok
+            again = newly & ~ok
+            if again.any():  # the recursion drifted from the true residual: restart from it
+                ag = torch.as_tensor(np.flatnonzero(again), device=b.device)
+                r[ag] = rt[ag]
+                rhat[ag] = rt[ag]
+                p[ag] = rt[ag]
+                rr = dot(rt[ag], rt[ag])
+                state[ag, 0], state[ag, 1] = rr.real, rr.imag
+                state[ag, 9] = 1.0
+                state[ag, 11] = 0.0
+    hints[tol] = max(1, int(its.max(initial=1)) - 1)
+    if rt is None:
+        rt = bh - S(x)
+    xo = torch.empty_like(uo)
+    _lib.check(lib.mgt_coarse_half_apply(d, bk, nv, ptr(F.D), 8, 1, 0, 0, None, ptr(x), ptr(xo), n, stream_ptr()),
+               "coarse half apply")
+    xo = uo - xo
+    xf = torch.empty_like(b)
+    xf[:, F.ie] = x
+    xf[:, F.io] = xo
+    rel = (dot(rt, rt).real / torch.where(b2 > 0, b2, 1)).sqrt().cpu().numpy()
+    # matvecs in full-operator units: 2 Schur applies per iteration (each ~ one C apply)
+    reps = [(int(its[i]), float(rel[i]), bool(rel[i] <= tol or float(b2[i]) == 0.0), int(2 * its[i] + mv_extra[i] + 1))
+            for i in range(n)]
+    return xf, reps
+
+
+def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0, even_odd=True):
     """BiCGStab on the coarse operator (C + i tau g5_c) for native coarse
     fields b (n, nb, 2nv), every rhs with its own scalars; zero start,
     convergence confirmed on the explicit residual (krylov.py:78-85).
     The matvec is the coarse block-stencil kernel; the short BLAS-1 runs as
     batched device tensor ops (coarse vectors are Nc = 48 x aggregates long).
-    Returns (x, [(iterations, relres, converged, matvecs)])."""
+    Returns (x, [(iterations, relres, converged, matvecs)]).
+    even_odd (default): every coarse extent even -> BiCGStab on the coarse
+    Schur complement (`_schur_bicgstab`, about half the iterations)."""
+    if even_odd:
+        F = coarse.schur_factors(tau)
+        if F is not None:
+            return _schur_bicgstab(coarse, F, b.contiguous(), tol, max_iter)
     nv = coarse.prolongator.nv
     # loose solves (the coarse Davidson's inner tol 1e-3) iterate with the
     # fp32 copy of C; the explicit-residual confirmation below uses fp64 C
@@ -630,7 +779,7 @@ def coarse_bicgstab(coarse, b, tol, max_iter, tau=0.0):
     its = np.zeros(n, dtype=int)
     mv = np.zeros(n, dtype=int)
     done = (b2 == 0).cpu().numpy().copy()
-    state = torch.zeros((n, 12), dtype=torch.float64, device=b.device)
+    state = torch.zeros((n, 16), dtype=torch.float64, device=b.device)
     state[:, 0], state[:, 1] = rho.real, rho.imag
     state[:, 9] = torch.as_tensor(~done, device=b.device, dtype=torch.float64)
     state[:, 10] = tol2

@@ -123,8 +123,9 @@ def test_coarse_bicgstab_solves(gold, setup):
     rng = np.random.default_rng(4)
     bh = rng.normal(size=(3, C.dim)) + 1j * rng.normal(size=(3, C.dim))
     b = pro.coarse_from_ref(torch.as_tensor(bh, device="cuda").reshape(3, pro.n_blocks, pro.nc))
-    for tau in (0.0, 0.3):
-        x, reps = MG.coarse_bicgstab(C, b, 1e-11, 500, tau)
+    assert C.schur_factors() is not None  # even coarse extents: the Schur path is the default
+    for tau, eo in ((0.0, True), (0.3, True), (0.0, False), (0.3, False)):
+        x, reps = MG.coarse_bicgstab(C, b, 1e-11, 500, tau, even_odd=eo)
         assert all(r[2] for r in reps)
         xr = pro.coarse_to_ref(x).reshape(3, -1).cpu().numpy()
         for i in range(3):
@@ -147,8 +148,8 @@ def test_coarse_bicgstab_loose_fp32_path_and_edge_cases(gold, setup):
     bh = rng.normal(size=(9, C.dim)) + 1j * rng.normal(size=(9, C.dim))
     bh[4] = 0.0
     b = pro.coarse_from_ref(torch.as_tensor(bh, device="cuda").reshape(9, pro.n_blocks, pro.nc))
-    for tol, tau in ((1e-3, 0.0), (1e-5, 0.2)):
-        x, reps = MG.coarse_bicgstab(C, b, tol, 500, tau)
+    for tol, tau, eo in ((1e-3, 0.0, True), (1e-5, 0.2, True), (1e-3, 0.0, False), (1e-5, 0.2, False)):
+        x, reps = MG.coarse_bicgstab(C, b, tol, 500, tau, even_odd=eo)
         xr = pro.coarse_to_ref(x).reshape(9, -1).cpu().numpy()
         Gt = G + 1j * tau * np.diag(g5c)
         for i in range(9):
@@ -159,8 +160,9 @@ def test_coarse_bicgstab_loose_fp32_path_and_edge_cases(gold, setup):
                 continue
             true_rel = np.linalg.norm(bh[i] - Gt @ xr[i]) / np.linalg.norm(bh[i])
             assert true_rel <= tol and abs(true_rel - rel) <= 1e-3 * tol
-    _, reps = MG.coarse_bicgstab(C, b[:2], 1e-12, 1, 0.0)
-    assert all(not r[2] and r[0] == 1 for r in reps)
+    for eo in (True, False):
+        _, reps = MG.coarse_bicgstab(C, b[:2], 1e-12, 1, 0.0, even_odd=eo)
+        assert all(not r[2] and r[0] == 1 for r in reps)
 
 
 def test_coarse_davidson_and_rank_r_oblique_deflation(gold, setup):
