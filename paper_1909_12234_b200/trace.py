@@ -415,9 +415,32 @@ def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probe
         g, h = _oblique_gh(pr, ubn, Y, z)
         return torch.sum(h.conj() * (g @ minv.T), dim=1).cpu().numpy()
 
-    samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
+    if probes.slots_per_group == 1:
+        # the corrections need only the probes, which are regenerated from
+        # their seeds: one pass over Y (r fine fields, 25.7 GB at 32^3 x 64,
+        # r = 64) and P per DEFER_BATCH probes instead of per solve batch
+        done = []
+
+        def collect(j0, z, x):
+            done.append((j0, z.shape[0]))
+
+        def finish_corr():
+            n = probes.sample_count
+            out = np.empty(n, dtype=np.complex128)
+            per = max(1, int(DEFER_BYTES // max(1, 16 * op.dim)))
+            for j0 in range(0, n, per):
+                j1 = min(n, j0 + per)
+                out[j0:j1] = correction(j0, probes.noise_native(j0, j1), None)
+            return out
+
+        samples, flagged = group_samples_gpu(inv_op, probes, deferred=(collect, finish_corr))
+    else:
+        samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
     _warn_flagged(flagged)
     return finish(fac.t0, samples, inv_op.n_solves - before, flagged)
+
+
+DEFER_BYTES = 16 << 30  # probe fields regenerated at once for a deferred correction pass
 
 
 def _oblique_setup(op, inv_op, pr, coarse_triplets, rank):
