@@ -102,25 +102,69 @@ def generate_null_vectors(op, n, tol=1e-2, max_iter=200, seed=0):
         raise ValueError("need n >= 1 null vectors")
     rng = np.random.default_rng(seed)
     N = op.dim
-    vecs = op.new_field(n)
-    ratios = np.empty(n)
-    degenerate = np.zeros(n, dtype=bool)
     # the start y0 = normal(N) + 1j normal(N) of the reference: the same
     # stream and values as rng.normal (loc 0, scale 1), replayed by parallel
     # host threads (rng.NormalStream, bitwise equal; the next vector's draws
     # are decoded while this one relaxes on the GPU) into pinned buffers and
     # combined on the device
+    #
+    # A producer thread decodes draw pair k + 1 (and k + 2) into spare pinned
+    # buffers while vector k relaxes on the GPU: the host stream and the GPU
+    # relaxation overlap (32^3 x 64: 57 + 45 ms per vector sequentially).
+    import queue
+    import threading
+
     from .rng import NormalStream
     normals = NormalStream(rng)
-    re_h = torch.empty(N, dtype=torch.float64).pin_memory()
-    im_h = torch.empty(N, dtype=torch.float64).pin_memory()
+    free, full = queue.Queue(), queue.Queue()
+    for _ in range(2):
+        free.put((torch.empty(N, dtype=torch.float64).pin_memory(), torch.empty(N, dtype=torch.float64).pin_memory()))
+    stop = threading.Event()
+
+    def produce():
+        try:
+            while not stop.is_set():
+                try:
+                    bufs = free.get(timeout=0.05)
+                except queue.Empty:
+                    continue
+                normals.take(N, out=bufs[0].numpy())
+                normals.take(N, out=bufs[1].numpy())
+                full.put(bufs)
+        except BaseException as e:  # surfaced by the consumer
+            full.put(e)
+
+    producer = threading.Thread(target=produce, name="mgt-nullvec-draws", daemon=True)
+    producer.start()
+
+    def next_start():
+        bufs = full.get()
+        if isinstance(bufs, BaseException):
+            raise bufs
+        y0 = op.to_native(torch.complex(bufs[0].to(device(), non_blocking=True),
+                                        bufs[1].to(device(), non_blocking=True)))
+        ev = torch.cuda.Event()
+        ev.record()
+        ev.synchronize()  # the copies out of the pinned pair are done: hand it back
+        free.put(bufs)
+        return y0
+
+    try:
+        return _relax_null_vectors(op, n, tol, max_iter, seed, next_start)
+    finally:
+        stop.set()
+        producer.join()
+
+
+def _relax_null_vectors(op, n, tol, max_iter, seed, next_start):
+    """The relaxation loop of generate_null_vectors (multigrid.py:83-113):
+    next_start() yields the successive Gaussian starts y0."""
+    vecs = op.new_field(n)
+    ratios = np.empty(n)
+    degenerate = np.zeros(n, dtype=bool)
     for i in range(n):
         for attempt in range(3):
-            normals.take(N, out=re_h.numpy())
-            normals.take(N, out=im_h.numpy())
-            y0 = op.to_native(torch.complex(re_h.to(device(), non_blocking=True),
-                                            im_h.to(device(), non_blocking=True)))
-            torch.cuda.current_stream().synchronize()  # the pinned buffers are refilled next
+            y0 = next_start()
             b = -op.apply_native(y0)
             d, its, conv, why, _ = gcr_relax(op, b, tol, max_iter, max_iter)
             y = y0 + d
