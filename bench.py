@@ -509,8 +509,7 @@ def probes_config4(M, rank, world, dims=(16, 16, 16, 16), s=128, k=64, tol=1e-8,
     res, setup, setup_first = _timed_setup(
         lambda: E.inexact_eigensolve(op, op.gamma5_diag, conf, E.shift_inverter_factory(op, conf.inner)), world)
     inv = M.TruncatedInverse(op, M.SolveConfig(tol=tol))
-    est, el = _sharded_estimate(M, lambda p: TR.deflate_orthogonal(inv, res.vectors, p, guess=True), geo, s, 200,
-                                rank, world)
+    est, el = _sharded_estimate(M, lambda p: TR.deflate_orthogonal(inv, res.vectors, p), geo, s, 200, rank, world)
     return {"config": f"16^4 eps=0.2 m0=0.1, k=64 inexact Davidson (block {block}, inner 1e-3, outer 1e-3), "
                       "orthogonal deflation, s=128 rademacher tol=1e-8 (BASELINE configs[3])",
             "value": s / el, "unit": "probes/s", "seconds": el, "setup_seconds": setup,

@@ -20,6 +20,9 @@ from .krylov import TruncatedInverse
 from .probing import ProbeSet
 
 
+DEFER_BYTES = 16 << 30  # probe fields regenerated at once for a deferred correction pass
+
+
 class DeflationContractError(ValueError):
     pass
 
@@ -304,7 +307,23 @@ def deflate_orthogonal(inv_op, U, probes, op=None, guess=False):
         samples, flagged = group_samples_gpu(inv_op, probes, guess=start)
         _warn_flagged(flagged)
         return finish(t0, samples, inv_op.n_solves - before, flagged)
-    samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
+    if probes.slots_per_group == 1:
+        # the corrections need only the probes: regenerate them from their
+        # seeds after the solves and project them in a few wide products
+        # (cuBLAS ZGEMM for s >= 32) instead of two skinny projections per
+        # solve batch inside the concurrent solve streams
+        def finish_corr():
+            n = probes.sample_count
+            out = np.empty(n, dtype=np.complex128)
+            per = max(1, int(DEFER_BYTES // max(1, 16 * base.dim)))
+            for j0 in range(0, n, per):
+                j1 = min(n, j0 + per)
+                out[j0:j1] = correction(j0, probes.noise_native(j0, j1), None)
+            return out
+
+        samples, flagged = group_samples_gpu(inv_op, probes, deferred=(lambda j0, z, x: None, finish_corr))
+    else:
+        samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
     _warn_flagged(flagged)
     return finish(t0, samples, inv_op.n_solves - before, flagged)
 
@@ -438,9 +457,6 @@ def deflate_oblique_coarse(op, inv_op, prolongator, coarse_triplets, rank, probe
         samples, flagged = group_samples_gpu(inv_op, probes, correction=correction)
     _warn_flagged(flagged)
     return finish(fac.t0, samples, inv_op.n_solves - before, flagged)
-
-
-DEFER_BYTES = 16 << 30  # probe fields regenerated at once for a deferred correction pass
 
 
 def _oblique_setup(op, inv_op, pr, coarse_triplets, rank):
