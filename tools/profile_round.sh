@@ -14,7 +14,7 @@ SB="python tools/solver_bench.py --dims 32x32x32x32 --groups 4 --nprobe 8 --mixe
 $SB > $O/${P}_solver_plain.log 2>&1 || exit 3
 ncu --set full --clock-control none --import-source on -k regex:bi_k1_eo -s 20 -c 1 \
    -o $O/${P}_k1eo_f32 $SB > $O/${P}_ncu_k1eo_f32.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:bi_k4 -s 20 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:bi_k4v -s 20 -c 1 \
    -o $O/${P}_k4_f32 $SB > $O/${P}_ncu_k4_f32.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:bi_k1_eo -s 20 -c 1 \
    -o $O/${P}_k1eo_f64 python tools/solver_bench.py --dims 32x32x32x32 --groups 4 --nprobe 8 --mixed 0 \
