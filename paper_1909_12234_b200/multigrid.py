@@ -615,44 +615,73 @@ class CoarseSchurInverse:
         y_e = S^-1 (h_e - A h_o),   y_o = C_oo^-1 h_o - B y_e.
     The reference forms tr(C^-1) by a dense factorisation of the whole
     Nc x Nc operator (trace.py:203-217); this does one dense inverse of
-    half the size plus two half-size GEMMs (~3x fewer flops), exact in
-    fp64 arithmetic (same t0 to rounding)."""
+    half the size; S and the trace term are assembled from the 48 x 48
+    blocks (the hops couple opposite parities only, so S and A B have the
+    2-hop block pattern), exact in fp64 arithmetic (same t0 to rounding)."""
 
     def __init__(self, coarse):
         pr = coarse.prolongator
-        C0, C1, C2, C3 = pr.blocking.coarse_dims(pr.geometry)
+        cd = pr.blocking.coarse_dims(pr.geometry)
+        C0, C1, C2, C3 = cd
         nb, nc = pr.n_blocks, pr.nc
         b = np.arange(nb)
         par = ((b % C2) + (b // C2) % C1 + (b // (C2 * C1)) % C0 + b // (C2 * C1 * C0)) & 1
         dev = device()
         cols = np.arange(nc)
-        iE = torch.as_tensor((np.flatnonzero(par == 0)[:, None] * nc + cols).reshape(-1), device=dev)
-        iO = torch.as_tensor((np.flatnonzero(par == 1)[:, None] * nc + cols).reshape(-1), device=dev)
-        ne, no = len(iE) // nc, len(iO) // nc
-        D = coarse.dense_native()
-        Ceo = D[iE][:, iO]
-        Coe = D[iO][:, iE]
-        Cee = D[iE][:, iE]
-        Coo = D[iO][:, iO]
-        del D
-        Coo_b = Coo.reshape(no, nc, no, nc).diagonal(dim1=0, dim2=2).permute(2, 0, 1).contiguous()
-        off = Coo.reshape(no, nc, no, nc).abs().sum(dim=(1, 3))
-        off.fill_diagonal_(0.0)
-        if off.max().item() > 0.0:
-            raise RuntimeError("coarse operator: odd-odd block is not block diagonal")
-        del Coo
-        self.Cooinv = torch.linalg.inv(Coo_b)  # (no, nc, nc)
-        A = torch.einsum("rja,jab->rjb", Ceo.reshape(ne * nc, no, nc), self.Cooinv).reshape(ne * nc, no * nc)
-        B = torch.einsum("jab,jbc->jac", self.Cooinv, Coe.reshape(no, nc, ne * nc)).reshape(no * nc, ne * nc)
-        del Ceo
-        S = Cee - A @ Coe
-        del Cee, Coe
-        self.Sinv = torch.linalg.inv(S)
+        ev, od = np.flatnonzero(par == 0), np.flatnonzero(par == 1)
+        iE = torch.as_tensor((ev[:, None] * nc + cols).reshape(-1), device=dev)
+        iO = torch.as_tensor((od[:, None] * nc + cols).reshape(-1), device=dev)
+        ne, no = len(ev), len(od)
+        pos = np.empty(nb, dtype=np.int64)  # aggregate -> index within its parity
+        pos[ev] = np.arange(ne)
+        pos[od] = np.arange(no)
+        nbr = coarse_neighbours(cd)
+        # block-sparse pieces (matrix form [row][col]; C storage is column-major):
+        # every hop couples opposite parities, so C_eo / C_oe have 8 blocks per
+        # block row and S = C_ee - C_eo C_oo^-1 C_oe has the 2-hop pattern
+        Mb = coarse.C.reshape(nb, 9, nc, nc).transpose(-1, -2)
+        Mo = Mb[torch.as_tensor(od, device=dev)]                       # (no, 9, nc, nc)
+        Me = Mb[torch.as_tensor(ev, device=dev)]                       # (ne, 9, nc, nc)
+        self.Cooinv = torch.linalg.inv(Mo[:, 0])                       # (no, nc, nc)
+        oe = torch.as_tensor(pos[nbr[ev, 1:]], device=dev)             # (ne, 8) odd neighbours of even
+        eo = torch.as_tensor(pos[nbr[od, 1:]], device=dev)             # (no, 8) even neighbours of odd
+        Ae = Me[:, 1:] @ self.Cooinv[oe]                               # A blocks C_e,d C_oo^-1   (ne, 8, nc, nc)
+        Bo = self.Cooinv[:, None] @ Mo[:, 1:]                          # B blocks C_oo^-1 C_o,d'  (no, 8, nc, nc)
+        er, orr = torch.arange(ne, device=dev), torch.arange(no, device=dev)
+        S = torch.zeros((ne, nc, ne, nc), dtype=coarse.C.dtype, device=dev)
+        S[er, :, er, :] = Me[:, 0]
+        for d in range(8):
+            o = oe[:, d]
+            for d2 in range(8):
+                # block (e, e2) += -C_e,d C_oo^-1 C_o,d2; e -> e2 is a translation,
+                # so the targets are distinct for fixed (d, d2)
+                S[er, :, eo[o, d2], :] -= Ae[:, d] @ Mo[o, 1 + d2]
+        self.Sinv = torch.linalg.inv(S.reshape(ne * nc, ne * nc))
         del S
-        tr_sab = torch.sum((self.Sinv @ A) * B.transpose(0, 1))
+        # tr(S^-1 A B) over the 2-hop blocks (e -> e2) of A B:
+        # sum <S^-1[e2, e], (A_e,d B_o,d2)^T>
+        Sb = self.Sinv.reshape(ne, nc, ne, nc)
+        tr_sab = torch.zeros((), dtype=coarse.C.dtype, device=dev)
+        for d in range(8):
+            o = oe[:, d]
+            for d2 in range(8):
+                P = Ae[:, d] @ Bo[o, d2]                               # block (e, e2) of A B
+                tr_sab = tr_sab + torch.sum(Sb[eo[o, d2], :, er, :] * P.transpose(-1, -2))
         self.t0 = complex((torch.diagonal(self.Sinv).sum() + torch.diagonal(self.Cooinv, dim1=1, dim2=2).sum()
                            + tr_sab).item())
-        self.A, self.B, self.iE, self.iO, self.no, self.nc = A, B, iE, iO, no, nc
+        # dense A = C_eo C_oo^-1 and B = C_oo^-1 C_oe for the per-probe
+        # products (scatter-add: on extent-2 coarse lattices the +mu and -mu
+        # neighbours coincide and add up, as in C)
+        A = torch.zeros((ne, nc, no, nc), dtype=coarse.C.dtype, device=dev)
+        B = torch.zeros((no, nc, ne, nc), dtype=coarse.C.dtype, device=dev)
+        ar = torch.arange(nc, device=dev)
+        for d in range(8):
+            A.index_put_((er[:, None, None], ar[None, :, None], oe[:, d][:, None, None], ar[None, None, :]),
+                         Ae[:, d], accumulate=True)
+            B.index_put_((orr[:, None, None], ar[None, :, None], eo[:, d][:, None, None], ar[None, None, :]),
+                         Bo[:, d], accumulate=True)
+        self.A, self.B = A.reshape(ne * nc, no * nc), B.reshape(no * nc, ne * nc)
+        self.iE, self.iO, self.no, self.nc = iE, iO, no, nc
 
     def apply_rows(self, H):
         """rows (C^-1 h)^T for the rows h of H (n, Nc), native coarse order."""
