@@ -45,6 +45,40 @@ __global__ void sub_kernel(int64_t n, const double2 *__restrict__ b, const doubl
     r[i] = make_double2(b[i].x - y[i].x, b[i].y - y[i].y);
 }
 
+// Device-scalar variants for the GCR loop: the coefficient (complex, from a
+// dot product left in device memory) is applied as sgn * c; a set breakdown
+// flag (device double) turns the update into a no-op, exactly as the host
+// loop's `break` skips it.
+__global__ void axpy2_dev_kernel(int64_t n, const double *__restrict__ c, double sgn, const double2 *__restrict__ x,
+                                 double2 *__restrict__ y, const double2 *__restrict__ u, double2 *__restrict__ w,
+                                 const double *__restrict__ flag) {
+  if (flag && *flag != 0.0) return;
+  const C<double> a(sgn * c[0], sgn * c[1]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    stc(y + i, ldc(y + i) + a * ldc(x + i));
+    if (w) stc(w + i, ldc(w + i) + a * ldc(u + i));
+  }
+}
+
+// a, b *= 1 / sqrt(nrm2[0])   (the host loop's 1.0 / std::sqrt(|q|^2))
+__global__ void scale2_dev_kernel(int64_t n, const double *__restrict__ nrm2, double2 *__restrict__ a,
+                                  double2 *__restrict__ b, const double *__restrict__ flag) {
+  if (*flag != 0.0) return;
+  const double s = 1.0 / sqrt(nrm2[0]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = a[i];
+    a[i] = make_double2(v.x * s, v.y * s);
+    v = b[i];
+    b[i] = make_double2(v.x * s, v.y * s);
+  }
+}
+
+// breakdown test of gcr_solve (krylov.py:95-97): ||q|| <= 1e-14 ||q0||
+__global__ void gcr_flag_kernel(const double *__restrict__ q0sq, const double *__restrict__ qnsq, double *flag) {
+  const double q0 = sqrt(q0sq[0]), qn = sqrt(qnsq[0]);
+  *flag = (qn <= 1e-14 * fmax(q0, 1e-300)) ? 1.0 : 0.0;
+}
+
 struct Gcr {
   mgt_wilson_s *h;
   cudaStream_t st;
@@ -88,7 +122,7 @@ extern "C" {
 
 size_t mgt_gcr_workspace_bytes(mgt_wilson_t h, int m) {
   if (!h || m < 1) return 0;
-  return (size_t)(2 * m + 3) * 12 * h->g.V * sizeof(double2) + 256;
+  return (size_t)(2 * m + 3) * 12 * h->g.V * sizeof(double2) + 256 + (size_t)(10 + 2 * m) * sizeof(double);
 }
 
 int mgt_gcr_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m, int max_iter, double tol,
@@ -109,7 +143,7 @@ int mgt_gcr_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m, int max
   // scratch: reuse z as the apply temporary where safe; scalars after the fields
   g.dbuf = (double *)(Q + (size_t)m * g.n);
   static thread_local double *hb = nullptr;
-  if (!hb) MGT_CUDA(cudaMallocHost((void **)&hb, 4 * sizeof(double)));
+  if (!hb) MGT_CUDA(cudaMallocHost((void **)&hb, 16 * sizeof(double)));
   g.hbuf = hb;
   const int64_t nb = g.n * sizeof(double2);
   int rc;
@@ -143,31 +177,37 @@ int mgt_gcr_solve(mgt_wilson_t h, const void *b_dev, void *x_dev, int m, int max
     MGT_CUDA(cudaMemcpyAsync(z, r, nb, cudaMemcpyDeviceToDevice, g.st));
     if ((rc = wilson_apply_native(h, z, q, 1, 0, 0.0, g.st))) return rc;
     ++matvecs;
-    double q0;
-    if ((rc = g.norm(q, q0))) return rc;
+    // the iteration's scalars stay on the device (sc[]): one host round trip
+    // per iteration instead of one per dot product; the same arithmetic and
+    // order as the host-scalar loop (modified Gram-Schmidt, krylov.py:86-111)
+    double *sc = g.dbuf;  // [0] |q0|^2, [2] |q|^2, [4] alpha, [6] |r|^2, [8] flag, [10 + 2j] beta_j
+    if ((rc = mgt_cdot(q, q, g.n, 1, sc + 0, g.st))) return rc;
     for (int j = 0; j < stored; ++j) {
-      C<double> beta;
       double2 *qj = Q + (size_t)j * g.n, *zj = Z + (size_t)j * g.n;
-      if ((rc = g.dot(qj, q, beta))) return rc;
-      if ((rc = g.axpy2(C<double>(-beta.re, -beta.im), qj, q, zj, z))) return rc;
+      if ((rc = mgt_cdot(qj, q, g.n, 1, sc + 10 + 2 * j, g.st))) return rc;
+      axpy2_dev_kernel<<<grid_for(g.n, 256, 8), 256, 0, g.st>>>(g.n, sc + 10 + 2 * j, -1.0, qj, q, zj, z, nullptr);
+      MGT_LAUNCH_CHECK("axpy2_dev_kernel");
     }
-    double qn;
-    if ((rc = g.norm(q, qn))) return rc;
-    if (qn <= 1e-14 * std::max(q0, 1e-300)) {
+    if ((rc = mgt_cdot(q, q, g.n, 1, sc + 2, g.st))) return rc;
+    gcr_flag_kernel<<<1, 1, 0, g.st>>>(sc + 0, sc + 2, sc + 8);
+    scale2_dev_kernel<<<grid_for(g.n, 256, 8), 256, 0, g.st>>>(g.n, sc + 2, q, z, sc + 8);
+    MGT_LAUNCH_CHECK("scale2_dev_kernel");
+    if ((rc = mgt_cdot(q, r, g.n, 1, sc + 4, g.st))) return rc;
+    axpy2_dev_kernel<<<grid_for(g.n, 256, 8), 256, 0, g.st>>>(g.n, sc + 4, 1.0, z, x, nullptr, nullptr, sc + 8);
+    axpy2_dev_kernel<<<grid_for(g.n, 256, 8), 256, 0, g.st>>>(g.n, sc + 4, -1.0, q, r, nullptr, nullptr, sc + 8);
+    MGT_LAUNCH_CHECK("axpy2_dev_kernel");
+    if ((rc = mgt_cdot(r, r, g.n, 1, sc + 6, g.st))) return rc;
+    MGT_CUDA(cudaMemcpyAsync(g.hbuf, sc, 10 * sizeof(double), cudaMemcpyDeviceToHost, g.st));
+    MGT_CUDA(cudaStreamSynchronize(g.st));
+    if (g.hbuf[8] != 0.0) {  // breakdown: x and r were left untouched
       reason = 2;
       break;
     }
-    scale2_kernel<<<grid_for(g.n, 256, 8), 256, 0, g.st>>>(g.n, 1.0 / qn, q, z);
-    MGT_LAUNCH_CHECK("scale2_kernel");
-    C<double> alpha;
-    if ((rc = g.dot(q, r, alpha))) return rc;
-    if ((rc = g.axpy2(alpha, z, x, q, nullptr))) return rc;  // x += alpha z
-    if ((rc = g.axpy2(C<double>(-alpha.re, -alpha.im), q, r))) return rc;             // r -= alpha q
     MGT_CUDA(cudaMemcpyAsync(Z + (size_t)stored * g.n, z, nb, cudaMemcpyDeviceToDevice, g.st));
     MGT_CUDA(cudaMemcpyAsync(Q + (size_t)stored * g.n, q, nb, cudaMemcpyDeviceToDevice, g.st));
     ++stored;
     ++it;
-    if ((rc = g.norm(r, rn))) return rc;
+    rn = std::sqrt(g.hbuf[6]);
     rel = rn / bn;
     if (stored >= m) {
       stored = 0;
