@@ -25,6 +25,16 @@
 
 #include "comm.cuh"
 #include "eo_core.cuh"
+// two-sites-per-thread fp32 stencils (eo_pair.cuh): compiled in with
+// -DMGT_F32_STENCIL_PAIRS=1, then on by default (env MGT_F32_STENCIL_PAIRS=0
+// switches back).  Measured equal or slower than the one-site kernels
+// (profiles/r02s4_pair_stencil_ab.txt), so the default build leaves them out.
+#ifndef MGT_F32_STENCIL_PAIRS
+#define MGT_F32_STENCIL_PAIRS 0
+#endif
+#if MGT_F32_STENCIL_PAIRS
+#include "eo_pair.cuh"
+#endif
 #include "handle.cuh"
 #include "reduce.cuh"
 
@@ -907,6 +917,117 @@ __global__ void __launch_bounds__(kRedBlock, MINB) bi_k3_eo(BiEo X, LinkField<R,
   if (last_block(w.ticket)) k3_finish<NR>(w, Vh);
 }
 
+#if MGT_F32_STENCIL_PAIRS
+// ---------------------------------------------------------------------------
+// fp32 stencil kernels with two adjacent cb sites per thread (eo_pair.cuh):
+// the same three roles as bi_eo_first / bi_k1_eo / bi_k3_eo for lattices with
+// L2 % 4 == 0.  A block iteration covers 2 * SPB ordered sites; lanes 0-15 of
+// a warp hold one 32-site tile, lanes 16-31 the next (tile_publish_pairs), so
+// the reductions stay a function of the site index only (batch-invariant).
+#define MGT_DYN_PAIR_LOOP(M, V, CTR, NCH)                                                     \
+  NCH = ((V) + 2 * (M).SPB - 1) / (2 * (M).SPB);                                              \
+  for (int64_t chunk = next_chunk(CTR), o = chunk * 2 * (M).SPB + 2 * (M).local; chunk < NCH; \
+       chunk = next_chunk(CTR), o = chunk * 2 * (M).SPB + 2 * (M).local)
+
+template <int NR, int RECON, int MINB>
+__global__ void __launch_bounds__(kRedBlock, MINB) bi_eo_first_v(BiEo X, LinkField<float, RECON> le,
+                                                                 LinkField<float, RECON> lo, const float2 *f,
+                                                                 BiWST<float> w_) {
+  const BiWST<float> w = w_.at(blockIdx.y);
+  f += (int64_t)blockIdx.y * w_.gfield;
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool act = w.st[m.rhs].status == ST_RUN;
+  const int64_t Vh = X.E.Vh;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  int64_t nchunks = 0;
+  MGT_DYN_PAIR_LOOP(m, Vh, w.ctr2, nchunks) {
+    if (act && o < Vh) {
+      const int64_t c = sched_site(X.sh, o);
+      C<float> y[2][4][3], cc[2][4][3];
+      eo_eval_pair<RECON>(X.E, 1, X.R.first, f + off, nullptr, lo, le, c, y, cc);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) st2(w.tmp + off + (int64_t)(a * 3 + k) * Vh + c, y[0][a][k], y[1][a][k]);
+    }
+  }
+}
+
+template <int NR, int RECON, int MINB>
+__global__ void __launch_bounds__(kRedBlock, MINB) bi_k1_eo_v(BiEo X, LinkField<float, RECON> le,
+                                                              LinkField<float, RECON> lo, BiWST<float> w_) {
+  const BiWST<float> w = w_.at(blockIdx.y);
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool run_me = w.st[m.rhs].status == ST_RUN;
+  const int64_t Vh = X.E.Vh;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  int64_t nchunks = 0;
+  MGT_DYN_PAIR_LOOP(m, Vh, w.ctr, nchunks) {
+    double acc[2] = {0.0, 0.0};
+    if (run_me && o < Vh) {
+      const int64_t c = sched_site(X.sh, o);
+      C<float> y[2][4][3], cc[2][4][3];
+      eo_eval_pair<RECON>(X.E, 0, X.R.second, w.tmp + off, w.p + off, le, lo, c, y, cc);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int64_t q = off + (int64_t)(a * 3 + k) * Vh + c;
+          st2(w.v + q, y[0][a][k], y[1][a][k]);
+          C<float> rh0, rh1;
+          ld2(w.rhat + q, rh0, rh1);
+          acc[0] += dre(rh0, y[0][a][k]);
+          acc[1] += dim(rh0, y[0][a][k]);
+          acc[0] += dre(rh1, y[1][a][k]);
+          acc[1] += dim(rh1, y[1][a][k]);
+        }
+    }
+    if (run_me) tile_publish_pairs<NR, 2>(acc, w.tr, o >> 5, n_tiles(Vh), m.rhs);
+  }
+  (void)nchunks;
+  if (last_block(w.ticket)) k1_finish<NR>(w, Vh);
+}
+
+template <int NR, int RECON, int MINB>
+__global__ void __launch_bounds__(kRedBlock, MINB) bi_k3_eo_v(BiEo X, LinkField<float, RECON> le,
+                                                              LinkField<float, RECON> lo, BiWST<float> w_) {
+  const BiWST<float> w = w_.at(blockIdx.y);
+  if (!any_status<NR>(w.st, ST_RUN)) return;
+  RhsMap<NR> m;
+  const bool run_me = w.st[m.rhs].status == ST_RUN;
+  const int64_t Vh = X.E.Vh;
+  const int64_t off = (int64_t)m.rhs * 12 * Vh;
+  int64_t nchunks = 0;
+  MGT_DYN_PAIR_LOOP(m, Vh, w.ctr, nchunks) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    if (run_me && o < Vh) {
+      const int64_t c = sched_site(X.sh, o);
+      C<float> y[2][4][3], cc[2][4][3];
+      eo_eval_pair<RECON>(X.E, 0, X.R.second, w.tmp + off, w.s + off, le, lo, c, y, cc);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          st2(w.t + off + (int64_t)(a * 3 + k) * Vh + c, y[0][a][k], y[1][a][k]);
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const C<float> tt = y[s][a][k], ss = cc[s][a][k];
+            acc[0] += dre(tt, ss);
+            acc[1] += dim(tt, ss);
+            acc[2] += dnorm2(tt);
+          }
+        }
+    }
+    if (run_me) tile_publish_pairs<NR, 3>(acc, w.tr, o >> 5, n_tiles(Vh), m.rhs);
+  }
+  (void)nchunks;
+  if (last_block(w.ticket)) k3_finish<NR>(w, Vh);
+}
+
+#endif  // MGT_F32_STENCIL_PAIRS
+
 // true Schur residual r = bh - S x (= the full residual, odd rows exact)
 template <int NR, int RECON>
 __global__ void __launch_bounds__(kRedBlock, 3) bi_resid_eo(BiEo X, LinkField<double, RECON> le,
@@ -1144,19 +1265,35 @@ static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &l
   return MGT_OK;
 }
 
-template <int NR, int RECON, typename R = double, int MINB = eo_minb<R>()>
+template <int NR, int RECON, typename R = double, int MINB = eo_minb<R>(), bool PAIR = false>
 static int launch_chunk_eo(const BiEo &X, const LinkField<R, RECON> &le, const LinkField<R, RECON> &lo,
                            const BiWST<R> &w, dim3 gd, dim3 g1, dim3 grid, cudaStream_t st) {
   const int64_t Vh = X.E.Vh;
   for (int it = 0; it < kChunk; ++it) {
-    bi_eo_first<NR, RECON, R, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
-    bi_k1_eo<NR, RECON, R, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+#if MGT_F32_STENCIL_PAIRS
+    if constexpr (PAIR) {
+      bi_eo_first_v<NR, RECON, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w);
+      bi_k1_eo_v<NR, RECON, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    } else
+#endif
+    {
+      bi_eo_first<NR, RECON, R, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w, 0);
+      bi_k1_eo<NR, RECON, R, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    }
     if constexpr (std::is_same<R, float>::value && MGT_F32_PAIRS)
       bi_k2v<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
     else
       bi_k2<NR, 0, R><<<grid, kRedBlock, 0, st>>>(Vh, w);
-    bi_eo_first<NR, RECON, R, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w, 0);
-    bi_k3_eo<NR, RECON, R, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+#if MGT_F32_STENCIL_PAIRS
+    if constexpr (PAIR) {
+      bi_eo_first_v<NR, RECON, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w);
+      bi_k3_eo_v<NR, RECON, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    } else
+#endif
+    {
+      bi_eo_first<NR, RECON, R, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.s, w, 0);
+      bi_k3_eo<NR, RECON, R, MINB><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
+    }
     if constexpr (std::is_same<R, float>::value && MGT_F32_PAIRS) {
       bi_k4v<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
       bi_k5v<NR><<<grid, kRedBlock, 0, st>>>(Vh, w);
@@ -1439,7 +1576,7 @@ __global__ void mx_next(BiWS w_, int cycle, int max_cycles) {
 // 2,048 rhs-warps of a 32-rhs stencil pass fit one wave instead of 1.15;
 // config-1 probes/s +10 %); large ones at 3 (168 registers, no spills, the
 // better choice once the pass is many waves long).
-template <int NR, int RECON, int MINB32 = eo_minb<float>()>
+template <int NR, int RECON, int MINB32 = eo_minb<float>(), bool PAIR = false>
 static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b,
                              double2 *x, char *ws, const WSLayout &Lw, double tol, const double *tols, int max_iter,
                              int64_t *report, double *relres, double *dot_out, int G, cudaStream_t st) {
@@ -1466,14 +1603,25 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
   if (!g_str) g_str = resident_grid(bi_k4<NR>, kRedBlock, (int64_t)1 << 40);
   if (!g_e1) g_e1 = resident_grid(bi_eo_first<NR, RECON>, kRedBlock, (int64_t)1 << 40);
   if (!g_e2) g_e2 = resident_grid(bi_k1_eo<NR, RECON>, kRedBlock, (int64_t)1 << 40);
-  if (!g_f1) g_f1 = resident_grid(bi_eo_first<NR, R32, float, MINB32>, kRedBlock, (int64_t)1 << 40);
-  if (!g_f2) g_f2 = resident_grid(bi_k1_eo<NR, R32, float, MINB32>, kRedBlock, (int64_t)1 << 40);
+#if MGT_F32_STENCIL_PAIRS
+  if constexpr (PAIR) {
+    if (!g_f1) g_f1 = resident_grid(bi_eo_first_v<NR, R32, MINB32>, kRedBlock, (int64_t)1 << 40);
+    if (!g_f2) g_f2 = resident_grid(bi_k1_eo_v<NR, R32, MINB32>, kRedBlock, (int64_t)1 << 40);
+  } else
+#endif
+  {
+    if (!g_f1) g_f1 = resident_grid(bi_eo_first<NR, R32, float, MINB32>, kRedBlock, (int64_t)1 << 40);
+    if (!g_f2) g_f2 = resident_grid(bi_k1_eo<NR, R32, float, MINB32>, kRedBlock, (int64_t)1 << 40);
+  }
   const int64_t need = (Vs + RhsMap<NR>::SPB - 1) / RhsMap<NR>::SPB;
-  auto per_group = [&](int resident) {
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, std::max(1, resident / G)));
+  auto per_group_n = [&](int resident, int64_t n) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, std::max(1, resident / G)));
   };
+  auto per_group = [&](int resident) { return per_group_n(resident, need); };
+  // the pair stencils take 2 * SPB sites per block iteration
+  const int64_t need32 = PAIR ? (need + 1) / 2 : need;
   const dim3 grid(per_group(g_str), G), gd(per_group(g_e2), G), g1(per_group(g_e1), G);
-  const dim3 fd(per_group(g_f2), G), f1(per_group(g_f1), G);
+  const dim3 fd(per_group_n(g_f2, need32), G), f1(per_group_n(g_f1, need32), G);
   MGT_CUDA(cudaMemsetAsync(w.ticket, 0, 256 * (size_t)G, st));
   MGT_CUDA(cudaMemsetAsync(w32.ticket, 0, 256 * (size_t)G, st));
   bi_eo_split<NR><<<grid, kRedBlock, 0, st>>>(X, b, w, P.g5out);
@@ -1486,7 +1634,7 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
   cudaGraphExec_t exec = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    GraphKey key{h, ws, NR, RECON, flags, 2, G, tau};
+    GraphKey key{h, ws, NR, RECON, flags, PAIR ? 3 : 2, G, tau};
     auto it = g_graphs.find(key);
     if (it != g_graphs.end()) {
       exec = it->second;
@@ -1495,7 +1643,7 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
       MGT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
       cudaGraph_t graph;
       MGT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-      launch_chunk_eo<NR, R32, float, MINB32>(X, le32, lo32, w32, fd, f1, grid, cap);
+      launch_chunk_eo<NR, R32, float, MINB32, PAIR>(X, le32, lo32, w32, fd, f1, grid, cap);
       cudaError_t e = cudaStreamEndCapture(cap, &graph);
       cudaStreamDestroy(cap);
       if (e != cudaSuccess) return cuda_fail(e, "mixed bicgstab graph capture");
@@ -1580,11 +1728,37 @@ static int64_t small_mixed_vh() {  // MGT_SMALL_VH overrides (A/B)
   }
   return v;
 }
+#if MGT_F32_STENCIL_PAIRS
+// MGT_F32_STENCIL_PAIRS=0 keeps the one-site fp32 stencils (A/B);
+// MGT_PAIR_MIN_VH: smallest half volume that takes the pair stencils
+static bool f32_pair_stencils() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MGT_F32_STENCIL_PAIRS");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+static int64_t pair_min_vh() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char *e = getenv("MGT_PAIR_MIN_VH");
+    v = e ? atoll(e) : 0;
+  }
+  return v;
+}
+#endif
 template <int NR, int RECON>
 static int solve_group_mixed_any(mgt_wilson_s *h, const WilsonParams &P, int flags, double tau, const double2 *b,
                                  double2 *x, char *ws, const WSLayout &Lw, double tol, const double *tols,
                                  int max_iter, int64_t *report, double *relres, double *dot_out, int G,
                                  cudaStream_t st) {
+#if MGT_F32_STENCIL_PAIRS
+  // two-sites-per-thread fp32 stencils (eo_pair.cuh) need L2/2 even
+  if (f32_pair_stencils() && h->g.L[2] % 4 == 0 && h->g.V / 2 > pair_min_vh())
+    return solve_group_mixed<NR, RECON, eo_minb<float>(), true>(h, P, flags, tau, b, x, ws, Lw, tol, tols, max_iter,
+                                                                report, relres, dot_out, G, st);
+#endif
   if (h->g.V / 2 <= small_mixed_vh())
     return solve_group_mixed<NR, RECON, 4>(h, P, flags, tau, b, x, ws, Lw, tol, tols, max_iter, report, relres,
                                            dot_out, G, st);
