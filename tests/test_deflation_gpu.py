@@ -31,7 +31,16 @@ def setup(gold):
 
 @pytest.mark.parametrize("k,s,n", [(64, 1, 49152), (64, 4, 49152), (64, 128, 20000), (5, 3, 1001), (70, 9, 777),
                                    (208, 8, 49152), (70, 6, 777), (8, 136, 49152), (3, 20, 1001), (1, 9, 513),
-                                   (64, 16, 49152), (144, 16, 7777), (40, 32, 3001), (64, 33, 2049)])
+                                   (64, 16, 49152), (144, 16, 7777), (40, 32, 3001), (64, 33, 2049),
+                                   # even lengths, 4 < s <= 16, k > 8: the FP64 tensor-core (DMMA) kernel,
+                                   # ragged vector / column / length tails
+                                   (70, 9, 778), (20, 5, 1002), (144, 16, 7778), (65, 12, 4098), (9, 8, 6),
+                                   (129, 7, 49154),
+                                   # whole 32-element tiles: the bulk-copy (cp.async.bulk + mbarrier) pipeline,
+                                   # fewer tiles than CTAs, ragged vector blocks
+                                   (129, 7, 49248), (70, 9, 800), (9, 8, 32), (200, 16, 64), (65, 5, 12288),
+                                   # at least two 256-element tiles per SM: the pipelined X - V H kernel
+                                   (70, 9, 76800), (144, 16, 75776), (203, 8, 78848), (12, 5, 76032)])
 def test_projection_kernels_vs_numpy(cuda, k, s, n):
     from paper_1909_12234_b200 import linalg as LA
     rng = np.random.default_rng(k + s)
