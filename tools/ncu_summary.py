@@ -24,6 +24,10 @@ def main(path):
             if k in h:
                 i = h.index(k)
                 print(f"  {k:70s} {r[i]:>16s} {u[i]}")
+        # tensor-pipe metrics (DMMA kernels): whatever this ncu names them
+        for i, k in enumerate(h):
+            if k not in KEYS and ("dmma" in k or "pipe_tensor" in k or "pipe_fp64" in k) and r[i] not in ("", "0", "n/a"):
+                print(f"  {k:70s} {r[i]:>16s} {u[i]}")
 
 
 if __name__ == "__main__":

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """One V^H X call at 16^4 (len 786,432), k = 64, s = $S (default 4): the
-ncu capture target for the few-column projection kernel."""
+ncu capture target for the few-column projection kernels (V^H X, then
+X - V H)."""
 import os
 import sys
 
@@ -14,7 +15,8 @@ def main():
     n = 12 * 16 ** 4
     V = torch.randn((64, n), dtype=torch.complex128, device="cuda")
     X = torch.randn((s, n), dtype=torch.complex128, device="cuda")
-    LA.vhx(V, X)
+    H = LA.vhx(V, X)
+    LA.sub_vh(V, H.contiguous(), X)
     torch.cuda.synchronize()
 
 
