@@ -8,6 +8,7 @@
 #include <string>
 #include <tuple>
 
+#include "dslash_pipe.cuh"
 #include "handle.cuh"
 #include "reduce.cuh"
 
@@ -190,6 +191,31 @@ static int launch_apply(const mgt_wilson_s *h, const WilsonParams &P, const void
   return MGT_OK;
 }
 
+// cp.async-staged apply (dslash_pipe.cuh): single rhs, dynamic chunks
+template <typename R, int RECON>
+static int launch_pipe(const mgt_wilson_s *h, const WilsonParams &P, const void *x, void *y, cudaStream_t st) {
+  constexpr int DEPTH = MGT_PIPE_DEPTH, LD = MGT_PIPE_LD;
+  auto kern = wilson_apply_pipe_kernel<R, RECON, DEPTH, LD>;
+  constexpr size_t smem = (size_t)DEPTH * 12 * 128 * sizeof(cplx<R>);
+  LinkField<R, RECON> lf{reinterpret_cast<const cplx<R> *>(h->links), h->g.V};
+  static int per_sm = 0;  // per template instance
+  if (!per_sm) {
+    MGT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int carve = 100;
+    if (const char *v = getenv("MGT_PIPE_CARVEOUT")) carve = atoi(v);
+    MGT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    const int b = blocks_per_sm(reinterpret_cast<const void *>(kern), 128, smem);
+    if (b < 1) return b < 0 ? MGT_ERR_CUDA : fail(MGT_ERR_CUDA, "wilson_apply_pipe_kernel does not fit an SM");
+    per_sm = b;
+  }
+  const int64_t need = (h->g.V + 127) / 128;
+  const int grid = (int)std::min<int64_t>((int64_t)num_sms() * per_sm, need);
+  unsigned long long *ctr = take_counter(h, st);
+  kern<<<grid, 128, smem, st>>>(P, reinterpret_cast<const cplx<R> *>(x), reinterpret_cast<cplx<R> *>(y), lf, ctr);
+  MGT_LAUNCH_CHECK("wilson_apply_pipe_kernel");
+  return MGT_OK;
+}
+
 // rhs-interleaved apply: fields at ((comp*V + site)*NR + rhs).  Thread
 // (site, rhs) = (tid / NR, tid % NR): the NR lanes of a site load the same
 // link address in one request (one sector set per NR rhs) and a warp's
@@ -280,6 +306,8 @@ static int apply_groups(const mgt_wilson_s *h, const WilsonParams &P, const void
     } else {
       if (h->variant == 1)
         rc = launch_split2<R, RECON>(h, P, xb + r * field, yb + r * field, st);
+      else if (h->variant == 2 && h->dyn_sched)
+        rc = launch_pipe<R, RECON>(h, P, xb + r * field, yb + r * field, st);
       else
         rc = launch_apply<R, RECON, 1>(h, P, xb + r * field, yb + r * field, st);
       r += 1;
