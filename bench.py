@@ -279,12 +279,11 @@ def run_ours(args):
         launches = _lib.launch_count() - l0
         # the K timed steps last ~40 ms, one nvidia-smi poll: keep the same
         # kernel running (untimed) so the sampler sees the clocks under this load
-        t_obs = time.perf_counter()
-        while time.perf_counter() - t_obs < 1.0:
-            for _ in range(10):
-                apply(x, out=y)
-            torch.cuda.synchronize()
-    ms_max = _max_over_ranks(ms, world)
+        # (a step count every rank agrees on: the N > 1 apply exchanges halos)
+        ms_max = _max_over_ranks(ms, world)
+        for _ in range(int(min(5000, max(10, 1000.0 / max(ms_max, 1e-3))))):
+            apply(x, out=y)
+        barrier()
     ms_kernel = ms if world == 1 else timed(kernel_only, args.steps)
     bytes_per_site = BYTES_PER_SITE_F64 if args.prec == 64 else BYTES_PER_SITE_F64 / 2
     value = bytes_per_site * V * world / (ms_max * 1e-3) / 1e9

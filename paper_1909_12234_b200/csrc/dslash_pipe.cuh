@@ -1,20 +1,30 @@
 // Wilson-Dirac plain apply with the neighbour spinors staged through shared
-// memory by asynchronous copies (cp.async / LDGSTS), sm_100a.
+// memory by asynchronous copies (cp.async / LDGSTS), sm_100a.  Opt-in
+// (MGT_DSLASH_VARIANT=2): measured SLOWER than the register-staged kernel.
 //
 // The thread-per-site kernel (dslash_core.cuh) keeps one hop's loads in
-// flight per thread in registers and then waits for them: at 12 warps per SM
-// the 9 dependent memory phases of a site (8 hops + centre) leave HBM idle
-// half of the time (ncu: 4.9 TB/s of DRAM traffic, long-scoreboard stalls).
-// Here every thread copies the 12 neighbour components of the hops
-// DEPTH items ahead straight into its own shared-memory slots -- loads in
-// flight hold no registers -- and the links of the next LD hops are staged
-// in the registers the spinor staging gave back.  The pipeline runs across
-// chunk boundaries (the next chunk's index is fetched one chunk ahead), so
-// a thread always has DEPTH spinor items and LD links in flight.
+// flight per thread in registers and then waits for them (ncu: 4.9 TB/s of
+// DRAM traffic, long-scoreboard stalls at 12 warps per SM).  Here every
+// thread copies the 12 neighbour components of the hops DEPTH items ahead
+// straight into its own shared-memory slots -- loads in flight hold no
+// registers -- and the links of the next LD hops are staged in registers.
+// The pipeline runs across chunk boundaries (the next chunk's index is
+// fetched one chunk ahead, one block barrier per chunk), so a thread always
+// has DEPTH spinor items and LD links in flight.
 //
-// Same per-site arithmetic, in the same order, as wilson_eval: results are
-// bitwise those of the register-staged kernel.  (Operator definition:
-// reference lattice.py:274-318 restated in 4D, see dslash_core.cuh.)
+// Result (profiles/r02s5_smem_staged_dslash_ab_rejected.txt): 0.62-0.68x
+// the default at 32^4 / 48^3 x 96 in fp64 (263 vs 178 us, 2.73 vs 1.79 ms),
+// 0.65-0.72x in fp32.  Every staged byte crosses the L1 data banks twice
+// (LDGSTS write + LDS read: l1tex throughput 61 % at 3.1 TB/s of DRAM
+// traffic, against 33 % for the register-staged kernel at 4.9 TB/s), so the
+// shared-memory path saturates before HBM does; deeper pipelines (DEPTH 3)
+// and a two-hop link lookahead (spills) do not change that.  Kept as the
+// measured answer to "stage the neighbour sites through shared memory".
+//
+// Same per-site arithmetic, in the same order, as wilson_eval (equal to the
+// default kernel up to FMA contraction, tests/test_operator_gpu.py).
+// (Operator definition: reference lattice.py:274-318 restated in 4D, see
+// dslash_core.cuh.)
 #pragma once
 #include <type_traits>
 
@@ -26,7 +36,7 @@ namespace mgt {
 #define MGT_PIPE_DEPTH 2
 #endif
 #ifndef MGT_PIPE_LD
-#define MGT_PIPE_LD 2
+#define MGT_PIPE_LD 1
 #endif
 
 template <int BYTES>
