@@ -25,6 +25,8 @@ def main():
     for _ in range(2):
         solver.solve_native(z, 1e-8, 4000, want_dot=True, mixed=True)
     torch.cuda.synchronize()
+    import time
+    time.sleep(float(os.environ.get("IDLE_S", "0")))  # IDLE_S=3: start the profiled solve from an idle (cool) GPU
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         x, reps, q = solver.solve_native(z, 1e-8, 4000, want_dot=True, mixed=True)
         torch.cuda.synchronize()
