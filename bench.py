@@ -293,7 +293,7 @@ def run_ours(args):
         # runs into the board power cap and the SM clock drops (DESIGN 5).
         # Keep it running, untimed for `value`, to report that regime too
         # (a step count every rank agrees on: the N > 1 apply exchanges halos).
-        n_sus = int(min(5000, max(10, 1500.0 / max(ms_max, 1e-3))))
+        n_sus = 2 if args.skip_sustained else int(min(5000, max(10, 1500.0 / max(ms_max, 1e-3))))
         for _ in range(n_sus // 2):
             apply(x, out=y)
         barrier()
@@ -640,6 +640,8 @@ def main():
     ap.add_argument("--config5", action="store_true", help="(default now) run BASELINE configs[4]")
     ap.add_argument("--skip-config5", action="store_true", help="skip BASELINE configs[4] (~45 s)")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-sustained", action="store_true",
+                    help="profiling runs: 2 instead of ~1.5 s of extra launches for the `sustained` key")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.impl == "reference":
