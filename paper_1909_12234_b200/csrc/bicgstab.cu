@@ -133,6 +133,30 @@ constexpr int eo_minb() {
   return sizeof(R) == 4 ? MGT_F32_MINB : 3;
 }
 
+// Experiment (off by default, -DMGT_F32_BLOCKED=1): the mixed solver's fp32
+// fields (its own workspace: r, rhat, p, v, s, t, x, tmp) in the row-blocked
+// layout of eo_core.cuh (EoGeom::Bh): the stencil kernels address them
+// through eo_base / eo_cstride, mx_begin / mx_accum translate from / to the
+// fp64 component planes, and the streaming kernels (bi_k2v / k4v / k5v) are
+// position-wise, so they do not care.  Motivation: a microbenchmark
+// (tools/micro/many_planes.cu) streams 48 component planes at 2.2 TB/s and
+// the same bytes in a blocked layout at 5.7-6.0 TB/s, and a 4-rhs stencil
+// pass touches ~200 distinct 2 MB pages per SM at a time.  Result
+// (profiles/r02s5_blocked_f32_fields_ab_rejected.txt): correct (same
+// iteration counts, solver tests pass) and SLOWER -- bi_eo_first 150 -> 154
+// us, bi_k1_eo 242 -> 262, bi_k3_eo 251 -> 353 (32^4, 4 rhs), solver -8 %:
+// the stencils are not limited by the number of pages they stream.
+#ifndef MGT_F32_BLOCKED
+#define MGT_F32_BLOCKED 0
+#endif
+#if MGT_F32_BLOCKED && MGT_F32_STENCIL_PAIRS
+#error "the two-sites-per-thread fp32 stencils (eo_pair.cuh) address SoA planes: build them with -DMGT_F32_BLOCKED=0"
+#endif
+template <typename R>
+constexpr bool eo_blk() {
+  return sizeof(R) == 4 && MGT_F32_BLOCKED;
+}
+
 #define MGT_SITE_LOOP(M, V) for (int64_t o = (M).first(); o < (V); o += (M).stride())
 
 // Dynamically scheduled loop over chunks of RhsMap<NR>::SPB ordered sites
@@ -840,11 +864,13 @@ __global__ void __launch_bounds__(kRedBlock, MINB) bi_eo_first(BiEo X, LinkField
     if (act && o < Vh) {
       const int64_t c = sched_site(X.sh, o);
       C<R> y[4][3], cc[4][3];
-      eo_eval<R, RECON>(X.E, 1, X.R.first, f + off, nullptr, lo, le, c, y, cc);
+      constexpr bool BLK = eo_blk<R>();
+      eo_eval<R, RECON, BLK>(X.E, 1, X.R.first, f + off, nullptr, lo, le, c, y, cc);
+      const int64_t cs = eo_cstride<BLK>(X.E), bc = off + eo_base<BLK>(X.E, c);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) stc(w.tmp + off + (int64_t)(a * 3 + k) * Vh + c, y[a][k]);
+        for (int k = 0; k < 3; ++k) stc(w.tmp + bc + (int64_t)(a * 3 + k) * cs, y[a][k]);
     }
   }
 }
@@ -865,12 +891,14 @@ __global__ void __launch_bounds__(kRedBlock, MINB) bi_k1_eo(BiEo X, LinkField<R,
     if (run_me && o < Vh) {
       const int64_t c = sched_site(X.sh, o);
       C<R> y[4][3], cc[4][3];
-      eo_eval<R, RECON>(X.E, 0, X.R.second, w.tmp + off, w.p + off, le, lo, c, y, cc);
+      constexpr bool BLK = eo_blk<R>();
+      eo_eval<R, RECON, BLK>(X.E, 0, X.R.second, w.tmp + off, w.p + off, le, lo, c, y, cc);
+      const int64_t cs = eo_cstride<BLK>(X.E), bc = off + eo_base<BLK>(X.E, c);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          const int64_t q = off + (int64_t)(a * 3 + k) * Vh + c;
+          const int64_t q = bc + (int64_t)(a * 3 + k) * cs;
           stc(w.v + q, y[a][k]);
           C<R> rh = ldc(w.rhat + q);
           acc[0] += dre(rh, y[a][k]);
@@ -899,12 +927,14 @@ __global__ void __launch_bounds__(kRedBlock, MINB) bi_k3_eo(BiEo X, LinkField<R,
     if (run_me && o < Vh) {
       const int64_t c = sched_site(X.sh, o);
       C<R> y[4][3], cc[4][3];
-      eo_eval<R, RECON>(X.E, 0, X.R.second, w.tmp + off, w.s + off, le, lo, c, y, cc);
+      constexpr bool BLK = eo_blk<R>();
+      eo_eval<R, RECON, BLK>(X.E, 0, X.R.second, w.tmp + off, w.s + off, le, lo, c, y, cc);
+      const int64_t cs = eo_cstride<BLK>(X.E), bc = off + eo_base<BLK>(X.E, c);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          stc(w.t + off + (int64_t)(a * 3 + k) * Vh + c, y[a][k]);
+          stc(w.t + bc + (int64_t)(a * 3 + k) * cs, y[a][k]);
           const C<R> tt = y[a][k], ss = cc[a][k];
           acc[0] += dre(tt, ss);
           acc[1] += dim(tt, ss);
@@ -1474,7 +1504,7 @@ static int solve_group(mgt_wilson_s *h, const WilsonParams &P, int flags, double
 // inner start: r = rhat = p = (float) r64 for the rhs still running (zero
 // otherwise), x = 0; inner tol2 = max(delta^2 |r|^2, 0.81 tol2_64)
 template <int NR>
-__global__ void __launch_bounds__(kRedBlock) mx_begin(int64_t V, BiWS w64_, BiWST<float> w_, double delta) {
+__global__ void __launch_bounds__(kRedBlock) mx_begin(int64_t V, EoGeom E, BiWS w64_, BiWST<float> w_, double delta) {
   const BiWS w64 = w64_.at(blockIdx.y);
   const BiWST<float> w = w_.at(blockIdx.y);
   RhsMap<NR> m;
@@ -1482,15 +1512,17 @@ __global__ void __launch_bounds__(kRedBlock) mx_begin(int64_t V, BiWS w64_, BiWS
   MGT_CHUNK_LOOP(m, V) {
     double acc[1] = {0.0};
     if (o < V) {
+      constexpr bool BLK = eo_blk<float>();
       const int64_t base = (int64_t)m.rhs * 12 * V + o;
+      const int64_t b32 = (int64_t)m.rhs * 12 * V + eo_base<BLK>(E, o), cs = eo_cstride<BLK>(E);
 #pragma unroll
       for (int c = 0; c < 12; ++c) {
-        const int64_t q = base + (int64_t)c * V;
+        const int64_t q = base + (int64_t)c * V, q32 = b32 + (int64_t)c * cs;
         const C<float> bb = act ? cvt<float>(ldc(w64.r + q)) : C<float>(0.f, 0.f);
-        stc(w.r + q, bb);
-        stc(w.rhat + q, bb);
-        stc(w.p + q, bb);
-        stc(w.x + q, C<float>(0.f, 0.f));
+        stc(w.r + q32, bb);
+        stc(w.rhat + q32, bb);
+        stc(w.p + q32, bb);
+        stc(w.x + q32, C<float>(0.f, 0.f));
         acc[0] += dnorm2(bb);
       }
     }
@@ -1522,17 +1554,19 @@ __global__ void __launch_bounds__(kRedBlock) mx_begin(int64_t V, BiWS w64_, BiWS
 // x_e += (double) e for the rhs whose inner cycle ran; they are marked CONV so
 // the fp64 residual kernels recompute their true residual
 template <int NR>
-__global__ void __launch_bounds__(kRedBlock) mx_accum(int64_t V, BiWS w64_, BiWST<float> w_) {
+__global__ void __launch_bounds__(kRedBlock) mx_accum(int64_t V, EoGeom E, BiWS w64_, BiWST<float> w_) {
   const BiWS w64 = w64_.at(blockIdx.y);
   const BiWST<float> w = w_.at(blockIdx.y);
   RhsMap<NR> m;
   if (w64.st[m.rhs].status == ST_RUN) {
     MGT_SITE_LOOP(m, V) {
+      constexpr bool BLK = eo_blk<float>();
       const int64_t base = (int64_t)m.rhs * 12 * V + o;
+      const int64_t b32 = (int64_t)m.rhs * 12 * V + eo_base<BLK>(E, o), cs = eo_cstride<BLK>(E);
 #pragma unroll
       for (int c = 0; c < 12; ++c) {
         const int64_t q = base + (int64_t)c * V;
-        const C<float> e = ldc(w.x + q);
+        const C<float> e = ldc(w.x + b32 + (int64_t)c * cs);
         const C<double> xx = ldc(w64.x + q);
         stc(w64.x + q, C<double>(xx.re + (double)e.re, xx.im + (double)e.im));
       }
@@ -1675,7 +1709,7 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
   int rc = fetch(w.st);
   if (rc) return rc;
   for (int cycle = 0; cycle < kMaxCycles && any_run(); ++cycle) {
-    mx_begin<NR><<<grid, kRedBlock, 0, st>>>(Vs, w, w32, delta);
+    mx_begin<NR><<<grid, kRedBlock, 0, st>>>(Vs, X.E, w, w32, delta);
     MGT_LAUNCH_CHECK("mx_begin");
     for (int round = 0; round < 1000000; ++round) {
       MGT_CUDA(cudaGraphLaunch(exec, st));
@@ -1684,7 +1718,7 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
       if (rc) return rc;
       if (!any_run()) break;
     }
-    mx_accum<NR><<<grid, kRedBlock, 0, st>>>(Vs, w, w32);
+    mx_accum<NR><<<grid, kRedBlock, 0, st>>>(Vs, X.E, w, w32);
     bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.x, w, 1);
     bi_resid_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
     mx_next<NR><<<dim3(1, G), 32, 0, st>>>(w, cycle, kMaxCycles);

@@ -29,6 +29,14 @@ struct EoGeom {
   int L2h;      // L2 / 2
   int antiperiodic;
   FastDiv f_L2h;
+  // row-blocked field addressing (BLK, the mixed solver's fp32 fields): the
+  // 12 components of the Bh = L1 * L2 / 2 parity sites that share (x3, x0)
+  // are contiguous -- element (comp, cb) at cb + blk * 11 * Bh + comp * Bh,
+  // blk = cb / Bh = x3 * L0 + x0.  A warp's 12 component loads then fall in
+  // one 12 * Bh * 8 B region (a 2 MB page holds all components of a site's
+  // neighbourhood) instead of 12 planes Vh * 8 B apart.
+  int64_t Bh, B11;
+  FastDiv f_Bh;
 };
 
 inline EoGeom make_eo_geom(const Geom &g, int antiperiodic) {
@@ -38,6 +46,9 @@ inline EoGeom make_eo_geom(const Geom &g, int antiperiodic) {
   e.L2h = g.L[2] / 2;
   e.antiperiodic = antiperiodic;
   e.f_L2h = make_fastdiv((uint32_t)e.L2h);
+  e.Bh = (int64_t)g.L[1] * e.L2h;
+  e.B11 = 11 * e.Bh;
+  e.f_Bh = make_fastdiv((uint32_t)(e.Bh > 0 ? e.Bh : 1));
   return e;
 }
 
@@ -55,13 +66,29 @@ __device__ __forceinline__ int64_t eo_coords(const EoGeom &E, int p, int64_t c, 
   return (int64_t)row * E.g.L[2] + x[2];
 }
 
+// Addressing of a parity field: element (comp, cb) at eo_base + comp * eo_cstride.
+template <bool BLK>
+__device__ __forceinline__ int64_t eo_cstride(const EoGeom &E) {
+  return BLK ? E.Bh : E.Vh;
+}
+template <bool BLK>
+__device__ __forceinline__ int64_t eo_base(const EoGeom &E, int64_t cb, int64_t blk) {
+  return BLK ? cb + blk * E.B11 : cb;
+}
+// the same from the cb index alone
+template <bool BLK>
+__device__ __forceinline__ int64_t eo_base(const EoGeom &E, int64_t cb) {
+  return BLK ? cb + (int64_t)fdiv((uint32_t)cb, E.f_Bh) * E.B11 : cb;
+}
+
 // One hop into acc (no -1/2): the neighbour spinor lives in the other-parity
 // field `in` at cb index nb >> 1; forward link from the output parity's
 // links at c, backward link from the input parity's links at nb >> 1.
-template <int MU, bool FWD, typename R, int RECON>
+template <int MU, bool FWD, typename R, int RECON, bool BLK = false>
 __device__ __forceinline__ void eo_hop(const EoGeom &E, const cplx<R> *__restrict__ in,
                                        const LinkField<R, RECON> &lout, const LinkField<R, RECON> &lin,
-                                       int64_t site, int64_t c, const int (&x)[4], R gin, C<R> (&acc)[4][3]) {
+                                       int64_t site, int64_t c, const int (&x)[4], R gin, C<R> (&acc)[4][3],
+                                       int64_t blk = 0) {
   const int L = E.g.L[MU];
   const int64_t st = E.g.stride[MU];
   int64_t nb;
@@ -74,14 +101,20 @@ __device__ __forceinline__ void eo_hop(const EoGeom &E, const cplx<R> *__restric
     if (MU == 3 && E.antiperiodic && x[3] == 0) ph = R(-1);
   }
   const int64_t cn = nb >> 1;
-  const int64_t Vh = E.Vh;
+  // the neighbour's (x3, x0) block: x1 / x2 hops stay in the site's block
+  if constexpr (BLK && (MU == 0 || MU == 3)) {
+    const int step = FWD ? ((x[MU] == L - 1) ? -(L - 1) : 1) : ((x[MU] == 0) ? (L - 1) : -1);
+    blk += (MU == 0) ? step : step * E.g.L[0];
+  }
+  const int64_t Vh = eo_cstride<BLK>(E);
+  const cplx<R> *inb = in + eo_base<BLK>(E, cn, blk);
   C<R> h[2][3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    C<R> p0 = ldc(in + (0 * 3 + k) * Vh + cn);
-    C<R> p1 = ldc(in + (1 * 3 + k) * Vh + cn);
-    C<R> p2 = gin * ldc(in + (2 * 3 + k) * Vh + cn);
-    C<R> p3 = gin * ldc(in + (3 * 3 + k) * Vh + cn);
+    C<R> p0 = ldc(inb + (0 * 3 + k) * Vh);
+    C<R> p1 = ldc(inb + (1 * 3 + k) * Vh);
+    C<R> p2 = gin * ldc(inb + (2 * 3 + k) * Vh);
+    C<R> p3 = gin * ldc(inb + (3 * 3 + k) * Vh);
     C<R> b0, b1;
     b_mul<MU>(p2, p3, b0, b1);
     if constexpr (FWD) {
@@ -141,13 +174,14 @@ struct EoCoef {
 
 // 8-hop sum at cb site c of parity pout, raw centre value (ctr may be null)
 // returned in cc, result in y.
-template <typename R, int RECON>
+template <typename R, int RECON, bool BLK = false>
 __device__ __forceinline__ void eo_eval(const EoGeom &E, int pout, const EoCoef &K, const cplx<R> *__restrict__ in,
                                         const cplx<R> *__restrict__ ctr, const LinkField<R, RECON> &lout,
                                         const LinkField<R, RECON> &lin, int64_t c, C<R> (&y)[4][3],
                                         C<R> (&cc)[4][3]) {
   int x[4];
   const int64_t site = eo_coords(E, pout, c, x);
+  const int64_t blk = BLK ? (int64_t)x[3] * E.g.L[0] + x[0] : 0;
   const R gin = (R)K.gin;
   C<R> acc[4][3];
 #pragma unroll
@@ -155,21 +189,21 @@ __device__ __forceinline__ void eo_eval(const EoGeom &E, int pout, const EoCoef 
 #pragma unroll
     for (int k = 0; k < 3; ++k) acc[a][k] = C<R>(R(0), R(0));
 #define MGT_HOP_FENCE asm volatile("" ::: "memory")
-  eo_hop<3, true>(E, in, lout, lin, site, c, x, gin, acc);
+  eo_hop<3, true, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
-  eo_hop<3, false>(E, in, lout, lin, site, c, x, gin, acc);
+  eo_hop<3, false, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
-  eo_hop<0, true>(E, in, lout, lin, site, c, x, gin, acc);
+  eo_hop<0, true, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
-  eo_hop<0, false>(E, in, lout, lin, site, c, x, gin, acc);
+  eo_hop<0, false, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
-  eo_hop<1, true>(E, in, lout, lin, site, c, x, gin, acc);
+  eo_hop<1, true, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
-  eo_hop<1, false>(E, in, lout, lin, site, c, x, gin, acc);
+  eo_hop<1, false, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
-  eo_hop<2, true>(E, in, lout, lin, site, c, x, gin, acc);
+  eo_hop<2, true, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
-  eo_hop<2, false>(E, in, lout, lin, site, c, x, gin, acc);
+  eo_hop<2, false, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
 #undef MGT_HOP_FENCE
   const R ch = (R)K.ch, gc = (R)K.gc, go = (R)K.go;
@@ -181,7 +215,7 @@ __device__ __forceinline__ void eo_eval(const EoGeom &E, int pout, const EoCoef 
     for (int k = 0; k < 3; ++k) {
       C<R> v = ch * acc[a][k];
       if (ctr) {
-        C<R> z = ldc(ctr + (a * 3 + k) * E.Vh + c);
+        C<R> z = ldc(ctr + (a * 3 + k) * eo_cstride<BLK>(E) + eo_base<BLK>(E, c, blk));
         cc[a][k] = z;
         if (a >= 2) z = gc * z;
         v = v + (a < 2 ? dcu : dcd) * z;
