@@ -156,6 +156,16 @@ template <typename R>
 constexpr bool eo_blk() {
   return sizeof(R) == 4 && MGT_F32_BLOCKED;
 }
+// 1: fp32 K1 / K3 load the centre field (and K1's rhat) before the hops
+// instead of after them (two latency phases fewer).  Measured 3 % SLOWER
+// (32^4: 425 -> 440 us per iteration and rhs): off.
+#ifndef MGT_F32_PRELOAD
+#define MGT_F32_PRELOAD 0
+#endif
+template <typename R>
+constexpr bool eo_pre() {
+  return sizeof(R) == 4 && MGT_F32_PRELOAD;
+}
 
 #define MGT_SITE_LOOP(M, V) for (int64_t o = (M).first(); o < (V); o += (M).stride())
 
@@ -891,16 +901,27 @@ __global__ void __launch_bounds__(kRedBlock, MINB) bi_k1_eo(BiEo X, LinkField<R,
     if (run_me && o < Vh) {
       const int64_t c = sched_site(X.sh, o);
       C<R> y[4][3], cc[4][3];
-      constexpr bool BLK = eo_blk<R>();
-      eo_eval<R, RECON, BLK>(X.E, 0, X.R.second, w.tmp + off, w.p + off, le, lo, c, y, cc);
+      constexpr bool BLK = eo_blk<R>(), PRE = eo_pre<R>();
       const int64_t cs = eo_cstride<BLK>(X.E), bc = off + eo_base<BLK>(X.E, c);
+      C<R> rhp[4][3];
+      if constexpr (PRE) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) rhp[a][k] = ldc(w.rhat + bc + (int64_t)(a * 3 + k) * cs);
+      }
+      eo_eval<R, RECON, BLK, PRE>(X.E, 0, X.R.second, w.tmp + off, w.p + off, le, lo, c, y, cc);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           const int64_t q = bc + (int64_t)(a * 3 + k) * cs;
           stc(w.v + q, y[a][k]);
-          C<R> rh = ldc(w.rhat + q);
+          C<R> rh;
+          if constexpr (PRE)
+            rh = rhp[a][k];
+          else
+            rh = ldc(w.rhat + q);
           acc[0] += dre(rh, y[a][k]);
           acc[1] += dim(rh, y[a][k]);
         }
@@ -928,7 +949,7 @@ __global__ void __launch_bounds__(kRedBlock, MINB) bi_k3_eo(BiEo X, LinkField<R,
       const int64_t c = sched_site(X.sh, o);
       C<R> y[4][3], cc[4][3];
       constexpr bool BLK = eo_blk<R>();
-      eo_eval<R, RECON, BLK>(X.E, 0, X.R.second, w.tmp + off, w.s + off, le, lo, c, y, cc);
+      eo_eval<R, RECON, BLK, eo_pre<R>()>(X.E, 0, X.R.second, w.tmp + off, w.s + off, le, lo, c, y, cc);
       const int64_t cs = eo_cstride<BLK>(X.E), bc = off + eo_base<BLK>(X.E, c);
 #pragma unroll
       for (int a = 0; a < 4; ++a)

@@ -250,7 +250,13 @@ __device__ __forceinline__ void wilson_thop_halo(const WilsonParams &P, const Li
 
 // y = G_out [ diag z - 1/2 hop(z) ],  z = G_in x.  Also returns the raw input
 // x at the site (xc, before G_in) for fused epilogues.
-template <typename R, int RECON, int SS = 1>
+// EARLY (callers that do not need xc): the centre value is loaded together
+// with the first hop's neighbours and folded into the accumulators at once,
+// acc = -2 diag z, so the site has 8 dependent memory phases instead of 9
+// (the centre's registers are free again before the accumulators of the
+// second hop are live); y = G_out (-1/2 acc).  Same terms, summed in a
+// different order than the default (differences at rounding level).
+template <typename R, int RECON, int SS = 1, bool EARLY = false>
 __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R> *__restrict__ in,
                                             const LinkField<R, RECON> &links, int64_t site,
                                             C<R> (&y)[4][3], C<R> (&xc)[4][3], int rhs = 0) {
@@ -259,10 +265,22 @@ __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R>
   const R g5in = (R)P.g5in;
   const bool ap = P.antiperiodic != 0;
   C<R> acc[4][3];
+  if constexpr (EARLY) {
+    const C<R> dup2((R)(-2.0 * P.diag_up_re), (R)(-2.0 * P.diag_up_im));
+    const C<R> ddn2((R)(-2.0 * P.diag_dn_re), (R)(-2.0 * P.diag_dn_im));
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) acc[a][c] = C<R>(R(0), R(0));
+      for (int c = 0; c < 3; ++c) {
+        C<R> v = ldc(in + ((a * 3 + c) * P.g.V + site) * SS);
+        acc[a][c] = a >= 2 ? ddn2 * (g5in * v) : dup2 * v;
+      }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[a][c] = C<R>(R(0), R(0));
+  }
   // The compiler would otherwise hoist the loads of all 8 hops (168 loads per
   // thread) and spill; one hop's 21 independent 16-byte loads in flight per
   // thread is already ~4x the bytes-in-flight HBM needs at this occupancy.
@@ -294,6 +312,17 @@ __device__ __forceinline__ void wilson_eval(const WilsonParams &P, const cplx<R>
   const C<R> ddn((R)P.diag_dn_re, (R)P.diag_dn_im);
   const R half = R(0.5);
   const R g5out = (R)P.g5out;
+  if constexpr (EARLY) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xc[a][c] = C<R>(R(0), R(0));
+        const C<R> r = (-half) * acc[a][c];
+        y[a][c] = a >= 2 ? g5out * r : r;
+      }
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
 #pragma unroll

@@ -174,7 +174,10 @@ struct EoCoef {
 
 // 8-hop sum at cb site c of parity pout, raw centre value (ctr may be null)
 // returned in cc, result in y.
-template <typename R, int RECON, bool BLK = false>
+// PRE: the centre values are loaded before the first hop instead of after
+// the last one (their latency hides behind the 8 hops; 24 more live
+// registers in fp32, so only the fp32 solver kernels ask for it).
+template <typename R, int RECON, bool BLK = false, bool PRE = false>
 __device__ __forceinline__ void eo_eval(const EoGeom &E, int pout, const EoCoef &K, const cplx<R> *__restrict__ in,
                                         const cplx<R> *__restrict__ ctr, const LinkField<R, RECON> &lout,
                                         const LinkField<R, RECON> &lin, int64_t c, C<R> (&y)[4][3],
@@ -189,6 +192,16 @@ __device__ __forceinline__ void eo_eval(const EoGeom &E, int pout, const EoCoef 
 #pragma unroll
     for (int k = 0; k < 3; ++k) acc[a][k] = C<R>(R(0), R(0));
 #define MGT_HOP_FENCE asm volatile("" ::: "memory")
+  if constexpr (PRE) {
+    if (ctr) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          cc[a][k] = ldc(ctr + (a * 3 + k) * eo_cstride<BLK>(E) + eo_base<BLK>(E, c, blk));
+    }
+    MGT_HOP_FENCE;
+  }
   eo_hop<3, true, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
   MGT_HOP_FENCE;
   eo_hop<3, false, R, RECON, BLK>(E, in, lout, lin, site, c, x, gin, acc, blk);
@@ -215,7 +228,11 @@ __device__ __forceinline__ void eo_eval(const EoGeom &E, int pout, const EoCoef 
     for (int k = 0; k < 3; ++k) {
       C<R> v = ch * acc[a][k];
       if (ctr) {
-        C<R> z = ldc(ctr + (a * 3 + k) * eo_cstride<BLK>(E) + eo_base<BLK>(E, c, blk));
+        C<R> z;
+        if constexpr (PRE)
+          z = cc[a][k];
+        else
+          z = ldc(ctr + (a * 3 + k) * eo_cstride<BLK>(E) + eo_base<BLK>(E, c, blk));
         cc[a][k] = z;
         if (a >= 2) z = gc * z;
         v = v + (a < 2 ? dcu : dcd) * z;

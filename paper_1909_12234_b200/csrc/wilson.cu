@@ -115,6 +115,12 @@ __global__ void links_from_ref_kernel(Geom g, const double2 *__restrict__ ref, c
 #ifndef MGT_F64_APPLY_MINB
 #define MGT_F64_APPLY_MINB 3
 #endif
+// 1: the plain apply loads the centre with the first hop (wilson_eval EARLY,
+// 8 instead of 9 dependent memory phases per site).  Measured 5-6 % SLOWER at
+// every lattice (48^3 x 96 fp64 1.77 -> 1.88 ms): off.
+#ifndef MGT_APPLY_EARLY_CENTRE
+#define MGT_APPLY_EARLY_CENTRE 0
+#endif
 template <typename R, int RECON, int NR>
 __global__ void __launch_bounds__(128, (sizeof(R) == 8 ? MGT_F64_APPLY_MINB : MGT_F32_APPLY_MINB))
     wilson_apply_kernel(WilsonParams P, const cplx<R> *__restrict__ in, cplx<R> *__restrict__ out,
@@ -135,7 +141,7 @@ __global__ void __launch_bounds__(128, (sizeof(R) == 8 ? MGT_F64_APPLY_MINB : MG
     const cplx<R> *inr = in + (int64_t)rhs * 12 * P.g.V;
     cplx<R> *outr = out + (int64_t)rhs * 12 * P.g.V;
     C<R> y[4][3], xc[4][3];
-    wilson_eval<R, RECON>(P, inr, links, site, y, xc);
+    wilson_eval<R, RECON, 1, MGT_APPLY_EARLY_CENTRE != 0>(P, inr, links, site, y, xc);
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
