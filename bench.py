@@ -375,7 +375,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": dict(clk.summary(t_w0 - 0.02, t_w1 + 0.02),
                            window="nvidia-smi polled during the W warm-up + K timed steps"),
-            "sustained": {"value": bytes_per_site * V * world / (ms_sus * 1e-3) / 1e9, "unit": "GB/s",
+            "sustained": None if args.skip_sustained else {"value": bytes_per_site * V * world / (ms_sus * 1e-3) / 1e9, "unit": "GB/s",
                           "ms_per_step": ms_sus, "steps": n_sus - n_sus // 2, "after_steps": n_sus // 2,
                           "frac": bytes_per_site * V * world / (ms_sus * 1e-3) / 1e9 / peak / world,
                           "clocks": clk.summary(t_s0, t_s1),
