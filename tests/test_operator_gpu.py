@@ -210,3 +210,48 @@ def test_smem_staged_apply_matches_default(cuda, monkeypatch, prec, recon):
             A = W.build_wilson4d_csr(gauge.links.cpu().numpy(), dims, 0.1)
             xv = _rand(b.dim, 4)
             assert _rel(b.apply(xv), A @ xv) < 1e-12
+
+
+@pytest.mark.parametrize("dims,boundary", [((4, 6, 4, 8), "antiperiodic"), ((6, 4, 2, 6), "periodic"),
+                                           ((8, 8, 8, 8), "antiperiodic")])
+def test_host_buffer_apply_pipeline(cuda, dims, boundary):
+    """The e2e path of bench.py: LatticeOperator.apply on HOST vectors in the
+    reference layout through mgt_wilson_apply_host (x0-chunked H2D -> layout
+    -> stencil -> layout -> D2H on three streams; lattice.py:214-217 is the
+    call it stands in for).  Against the oracle CSR at 1e-12, bitwise equal
+    to the device-resident apply for every chunk count (1, 2, 3, L0, more
+    than L0), flag variant, row-batched input, numpy / pageable / pinned
+    buffers; the chunks' periodic x0 neighbours (first and last chunk) are
+    the interesting sites."""
+    M, geo, gauge, op, links = _setup(dims, 0.3, seed=2, recon=12, boundary=boundary)
+    A = W.build_wilson4d_csr(links, dims, 0.1, antiperiodic=boundary == "antiperiodic")
+    g5 = W.gamma5_diag(geo.site_count)
+    x = _rand(op.dim, 21)
+
+    def dev(v):  # the device-resident path (to_native -> mgt_wilson_apply -> from_native)
+        return op.apply(torch.from_numpy(v).cuda()).cpu().numpy()
+
+    ref = dev(x)
+    assert _rel(ref, A @ x) < 1e-12
+    assert np.array_equal(op.apply(x), ref)  # 1-D numpy input takes the host pipeline
+    for nch in (1, 2, 3, dims[0], dims[0] + 5):
+        y = op.apply_host(x, nchunks=nch)
+        assert isinstance(y, np.ndarray) and np.array_equal(y, ref), nch
+    # flag variants and the shift
+    assert _rel(op.apply_host(x, flags=1), A @ (g5 * x)) < 1e-12
+    assert _rel(op.apply_host(x, flags=2), g5 * (A @ x)) < 1e-12
+    assert _rel(op.apply_host(x, flags=4), A.conj().T @ x) < 1e-12
+    assert _rel(op.apply_host(x, tau=0.4, nchunks=3), A @ x + 0.4j * g5 * x) < 1e-12
+    # row-batched input, pinned tensors, caller-provided output
+    X = np.stack([_rand(op.dim, 30 + j) for j in range(3)])
+    xt = torch.from_numpy(X).pin_memory()
+    out = torch.empty_like(xt).pin_memory()
+    yt = op.apply_host(xt, out=out, nchunks=2)
+    assert yt.data_ptr() == out.data_ptr()
+    for j in range(3):
+        assert np.array_equal(out[j].numpy(), dev(X[j]))
+    with pytest.raises(ValueError):
+        op.apply_host(np.zeros(op.dim + 1, dtype=np.complex128))
+    # complex64 operator: host data stays complex128, the arithmetic is fp32
+    op32 = M.build_wilson(gauge, 0.1, prec=32, recon=12)
+    assert _rel(op32.apply_host(x, nchunks=3), A @ x) < 2e-6
