@@ -1318,9 +1318,9 @@ static int launch_chunk(const WilsonParams &P, const LinkField<double, RECON> &l
 
 template <int NR, int RECON, typename R = double, int MINB = eo_minb<R>(), bool PAIR = false>
 static int launch_chunk_eo(const BiEo &X, const LinkField<R, RECON> &le, const LinkField<R, RECON> &lo,
-                           const BiWST<R> &w, dim3 gd, dim3 g1, dim3 grid, cudaStream_t st) {
+                           const BiWST<R> &w, dim3 gd, dim3 g1, dim3 grid, cudaStream_t st, int iters = kChunk) {
   const int64_t Vh = X.E.Vh;
-  for (int it = 0; it < kChunk; ++it) {
+  for (int it = 0; it < iters; ++it) {
 #if MGT_F32_STENCIL_PAIRS
     if constexpr (PAIR) {
       bi_eo_first_v<NR, RECON, MINB><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.p, w);
@@ -1626,6 +1626,65 @@ __global__ void mx_next(BiWS w_, int cycle, int max_cycles) {
   }
 }
 
+// Device-side loop control of the inner iterations (CUDA conditional graph
+// node, WHILE): the body -- kWhileBody iterations and this kernel -- repeats
+// while any rhs of the launch is still running, so a cycle of the mixed
+// solve is ONE graph launch with no host round trip between iteration
+// chunks and at most kWhileBody - 1 early-exit iterations past convergence
+// (the chunked replay costs a status copy + synchronise + graph launch,
+// ~60 us, per 8 iterations: 16 % of an 8^4 solve, 3 % at 16^4).
+#ifndef MGT_WHILE_BODY
+#define MGT_WHILE_BODY 2
+#endif
+constexpr int kWhileBody = MGT_WHILE_BODY;
+__global__ void bi_while_cond(cudaGraphConditionalHandle handle, const BiState *st, int G, int NR) {
+  bool any = false;
+  for (int i = threadIdx.x; i < G * kMaxGroup; i += 32)
+    if ((i % kMaxGroup) < NR && st[i].status == ST_RUN) any = true;
+  any = __any_sync(0xffffffffu, any);
+  if (threadIdx.x == 0) cudaGraphSetConditional(handle, any ? 1u : 0u);
+}
+
+// Build the WHILE graph around `body(stream)`; nullptr when the runtime
+// refuses (the caller falls back to the chunked replay).
+template <class Body>
+static cudaGraphExec_t build_while_graph(const BiState *st_dev, int G, int NR, Body body) {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
+  cudaGraphConditionalHandle handle{};
+  ok = ok && cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+  cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  ok = ok && cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess;
+  if (ok) {
+    cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+    ok = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaStreamBeginCaptureToGraph(cap, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+                   cudaSuccess;
+    if (ok) {
+      body(cap);
+      bi_while_cond<<<1, 32, 0, cap>>>(handle, st_dev, G, NR);
+      cudaGraph_t out = nullptr;
+      ok = cudaStreamEndCapture(cap, &out) == cudaSuccess;
+    }
+  }
+  ok = ok && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+  if (cap) cudaStreamDestroy(cap);
+  if (g) cudaGraphDestroy(g);
+  if (!ok) {
+    cudaGetLastError();
+    if (exec) cudaGraphExecDestroy(exec);
+    return nullptr;
+  }
+  return exec;
+}
+
 // MINB32: resident blocks per SM of the fp32 stencil kernels (their launch
 // bounds).  Small lattices run at 4 (128 registers, 16 warps/SM: at 8^4 the
 // 2,048 rhs-warps of a 32-rhs stencil pass fit one wave instead of 1.15;
@@ -1708,6 +1767,30 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
       g_graphs[key] = exec;
     }
   }
+  // the device-controlled loop: opt-in (MGT_SOLVE_WHILE=1).  Measured equal
+  // to the chunked replay within 1 % at 8^4 .. 32^4 (a loop trip of the
+  // conditional node costs about what the host round trip it removes does;
+  // profiles/r02s6_while_graph_ab.txt), so the default stays the simpler path.
+  static bool while_unsupported = false;
+  const char *wv = getenv("MGT_SOLVE_WHILE");
+  const bool use_while = wv && atoi(wv) != 0 && !while_unsupported;
+  cudaGraphExec_t exec_w = nullptr;
+  if (use_while) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    GraphKey key{h, ws, NR, RECON, flags, PAIR ? 13 : 12, G, tau};
+    auto it = g_graphs.find(key);
+    if (it != g_graphs.end()) {
+      exec_w = it->second;
+    } else {
+      exec_w = build_while_graph(w32.st, G, NR, [&](cudaStream_t cap) {
+        launch_chunk_eo<NR, R32, float, MINB32, PAIR>(X, le32, lo32, w32, fd, f1, grid, cap, kWhileBody);
+      });
+      if (exec_w)
+        g_graphs[key] = exec_w;
+      else
+        while_unsupported = true;  // not supported here: keep the chunked replay
+    }
+  }
   BiState *hs = state_mailbox(G * kMaxGroup);
   if (!hs) return fail(MGT_ERR_CUDA, "pinned state mailbox");
   auto fetch = [&](const BiState *dst) -> int {
@@ -1732,13 +1815,21 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
   for (int cycle = 0; cycle < kMaxCycles && any_run(); ++cycle) {
     mx_begin<NR><<<grid, kRedBlock, 0, st>>>(Vs, X.E, w, w32, delta);
     MGT_LAUNCH_CHECK("mx_begin");
-    for (int round = 0; round < 1000000; ++round) {
-      MGT_CUDA(cudaGraphLaunch(exec, st));
-      note_launch(7 * kChunk);
-      rc = fetch(w32.st);
-      if (rc) return rc;
-      if (!any_run()) break;
+    if (exec_w) {
+      MGT_CUDA(cudaGraphLaunch(exec_w, st));  // iterates on the device until no rhs is running
+    } else {
+      for (int round = 0; round < 1000000; ++round) {
+        MGT_CUDA(cudaGraphLaunch(exec, st));
+        note_launch(7 * kChunk);
+        rc = fetch(w32.st);
+        if (rc) return rc;
+        if (!any_run()) break;
+      }
     }
+    int its_before = 0;
+    if (exec_w)
+      for (int g = 0; g < G; ++g)
+        for (int r = 0; r < NR; ++r) its_before = std::max(its_before, hs[g * kMaxGroup + r].iters);
     mx_accum<NR><<<grid, kRedBlock, 0, st>>>(Vs, X.E, w, w32);
     bi_eo_first<NR, RECON><<<g1, kRedBlock, 0, st>>>(X, le, lo, w.x, w, 1);
     bi_resid_eo<NR, RECON><<<gd, kRedBlock, 0, st>>>(X, le, lo, w);
@@ -1747,6 +1838,13 @@ static int solve_group_mixed(mgt_wilson_s *h, const WilsonParams &P, int flags, 
     MGT_LAUNCH_CHECK("mixed residual");
     rc = fetch(w.st);
     if (rc) return rc;
+    if (exec_w) {  // launches of the device-controlled loop, from the iterations it added
+      int its_after = 0;
+      for (int g = 0; g < G; ++g)
+        for (int r = 0; r < NR; ++r) its_after = std::max(its_after, hs[g * kMaxGroup + r].iters);
+      const int trips = std::max(1, (its_after - its_before + kWhileBody - 1) / kWhileBody);
+      note_launch((uint64_t)trips * (7 * kWhileBody + 1));
+    }
   }
   bi_eo_final<NR, RECON><<<grid, kRedBlock, 0, st>>>(X, le, lo, x, w);
   MGT_LAUNCH_CHECK("bi_eo_final (mixed)");

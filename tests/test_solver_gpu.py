@@ -265,3 +265,34 @@ def test_gmres_and_gcr_edge_cases_and_estimator(cuda):
     zn = op.to_native(torch.as_tensor(np.stack([P.rademacher_numpy(op.dim, 5)])).cuda())
     xb, reps, dq = inv.solve_native(zn, want_dot=True)
     assert reps[0].converged and abs(dq[0] - est.samples[0]) <= 1e-9 * abs(est.samples[0])
+
+
+def test_device_controlled_iteration_loop(cuda, monkeypatch):
+    """MGT_SOLVE_WHILE=1: a cycle of the mixed solve is one CUDA graph launch
+    whose WHILE conditional node repeats the iteration kernels on the device
+    until no rhs is running (no host round trip between iteration chunks).
+    Same kernels in the same order as the chunked replay: bitwise the same
+    solutions, quadratic forms, iteration counts and reports."""
+    import torch
+    import paper_1909_12234_b200 as M
+    from paper_1909_12234_b200 import krylov as K
+    dims = (8, 8, 8, 8)
+    geo = M.LatticeGeometry(dims, "antiperiodic")
+    op = M.build_wilson(M.generate_gauge(geo, "su3", eps=0.2, seed=0), 0.1)
+    probes = M.build_probe_set(geo, 12, 9, dilution=False, kind="rademacher", seed=3)
+    z = probes.noise_native(0, 9)
+    solver = K.BiCGStab(op, max_rhs=12)
+    monkeypatch.delenv("MGT_SOLVE_WHILE", raising=False)
+    x0, r0, q0 = solver.solve_native(z, 1e-8, 4000, want_dot=True, mixed=True)
+    monkeypatch.setenv("MGT_SOLVE_WHILE", "1")
+    x1, r1, q1 = solver.solve_native(z, 1e-8, 4000, want_dot=True, mixed=True)
+    x2, r2, q2 = solver.solve_native(z, 1e-3, 4000, want_dot=True, mixed=True)
+    monkeypatch.delenv("MGT_SOLVE_WHILE", raising=False)
+    assert torch.equal(x0, x1) and torch.equal(torch.as_tensor(q0), torch.as_tensor(q1))
+    assert [r.iterations for r in r0] == [r.iterations for r in r1]
+    assert all(r.converged and r.final_relres <= 1e-8 for r in r1)
+    assert all(r.converged and r.final_relres <= 1e-3 for r in r2)
+    # max_iter is honoured on the device (the loop ends when every rhs stopped)
+    monkeypatch.setenv("MGT_SOLVE_WHILE", "1")
+    x3, r3, _ = solver.solve_native(z[:2], 1e-12, 3, want_dot=True, mixed=True)
+    assert all((not r.converged) and r.iterations <= 4 for r in r3)
